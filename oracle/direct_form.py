@@ -1,0 +1,121 @@
+"""CPU-DF: the paper's FFT direct form (FIF), plain numpy, fp64.
+
+TEST INFRASTRUCTURE, NOT PRODUCT CODE.  Only tests/, __graft_entry__.smoke()
+and bench.py's cpu_baseline / --impl reference legs may import this module.
+It shares no code with the CUDA path (paper_1802_01359_b200/csrc).
+
+This is the second oracle engine.  It follows PAPER.md §4 step by step:
+  * eigenvalues of W = DFT of the filter row w ("by
+    means of the Fast Fourier Transform since (Lambdas) is equivalent to the
+    DFT of the sequence {w_1q}") -- the row is built in the time domain exactly
+    as in oracle/fif_oracle.c (h sampled, /sum, h(*)h);
+  * IMF = IDFT((I-D)^N DFT(s))                       (Eq. One step_algo);
+  * N: "compute (One step_algo) for subsequently bigger values of N0 and stop
+    whenever SD is less or equal to delta", SD evaluated
+    through Parseval as a LINEAR scan N = 1, 2, ...;
+  * s = s - IMF in the time domain, re-transformed for the next IMF
+    (Alg. 2).
+It is pinned against the time-domain oracle (fif_oracle.c) in
+tests/test_oracle_pins.py and used where the literal iteration is too slow.
+Readings A1-A15 are the same as fif_oracle.c.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+WINDOW_TRI_SQ = 0
+WINDOW_TRI_SQ_WIDE = 1
+
+
+def count_extrema(r: np.ndarray) -> int:
+    """Reading A4: strict sign changes of r[j+1]-r[j], zeros dropped, no wrap."""
+    d = np.diff(np.asarray(r, dtype=np.float64))
+    sg = np.sign(d)
+    sg = sg[sg != 0]
+    return int(np.count_nonzero(sg[1:] != sg[:-1]))
+
+
+def filter_half_length(xi: float, n: int, k: int, window: int = WINDOW_TRI_SQ) -> int:
+    """Readings A1/A3/A8: L = clamp(floor(fl(fl(xi*n)/k)), 2, floor((n-1)/4))."""
+    q = math.floor((float(xi) * float(n)) / float(k))  # Python floats are IEEE fp64, no FMA
+    L = 2 * q if window == WINDOW_TRI_SQ_WIDE else q
+    return int(min(max(L, 2), (n - 1) // 4))
+
+
+def filter_row(n: int, L: int) -> np.ndarray:
+    """Circulant row c of w = h(*)h, h_j = (1-|j|/L)/sum."""
+    j = np.arange(-(L - 1), L, dtype=np.float64)
+    h = 1.0 - np.abs(j) / L
+    h = h / h.sum()
+    w = np.convolve(h, h)  # length 4L-3, centred at index 2L-2
+    H = 2 * L - 2
+    row = np.zeros(n, dtype=np.float64)
+    for d in range(-H, H + 1):
+        row[d % n] += w[d + H]
+    return row
+
+
+def eigenvalues(n: int, L: int) -> np.ndarray:
+    """lambda_p = DFT of the filter row (PAPER.md:543 Eq. Lambdas), real part, bins 0..n/2."""
+    return np.fft.rfft(filter_row(n, L)).real
+
+
+def sd_curve(rhat: np.ndarray, lam: np.ndarray, n: int, max_inner: int) -> np.ndarray:
+    """SD_N for N = 1..max_inner via Parseval:
+    SD_N^2 = sum c_k lam^2 a^{2(N-1)} |r_k|^2 / sum c_k a^{2(N-1)} |r_k|^2, a = 1-lam clamped to [0,1]."""
+    a = np.clip(1.0 - lam, 0.0, 1.0)
+    c = np.full(lam.shape, 2.0)
+    c[0] = 1.0
+    if n % 2 == 0:
+        c[-1] = 1.0
+    p = c * (rhat.real ** 2 + rhat.imag ** 2)
+    q = p * lam * lam
+    x = np.ones_like(a)
+    a2 = a * a
+    out = np.empty(max_inner)
+    for N in range(1, max_inner + 1):
+        P = float(np.dot(p, x))
+        Q = float(np.dot(q, x))
+        out[N - 1] = math.sqrt(Q) / math.sqrt(P) if P > 0.0 else 0.0
+        x = x * a2
+    return out
+
+
+def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ):
+    """Full FIF decomposition of one real signal.  Returns dict with imfs [(max_imfs+1), n]
+    (trend in slot M), M, l (2L per IMF), N, k (extrema counts), sd (SD_N, SD_{N-1})."""
+    s = np.asarray(s, dtype=np.float64)
+    n = s.shape[0]
+    r = s.copy()
+    imfs = np.zeros((max_imfs + 1, n))
+    ls, Ns, ks, sds = [], [], [], []
+    M = 0
+    while M < max_imfs:
+        k = count_extrema(r)
+        ks.append(k)
+        if k < 2:
+            break
+        L = filter_half_length(xi, n, k, window)
+        lam = eigenvalues(n, L)
+        rhat = np.fft.rfft(r)
+        curve = sd_curve(rhat, lam, n, max_inner)
+        hit = np.nonzero(curve <= delta)[0]
+        N = int(hit[0]) + 1 if hit.size else max_inner
+        imf = np.fft.irfft(damping(lam, N) * rhat, n)
+        imfs[M] = imf
+        r = r - imf
+        ls.append(2 * L)
+        Ns.append(N)
+        sds.append((curve[N - 1], curve[N - 2] if N > 1 else float("nan")))
+        M += 1
+    if M == max_imfs:
+        ks.append(count_extrema(r))
+    imfs[M] = r
+    return {"imfs": imfs, "M": M, "l": ls, "N": Ns, "k": ks, "sd": sds}
+
+
+def damping(lam: np.ndarray, N: int) -> np.ndarray:
+    """(1 - lambda)^N with 1 - lambda clamped to [0, 1] (PAPER.md:688 (I-D)^N)."""
+    return np.clip(1.0 - np.asarray(lam, dtype=np.float64), 0.0, 1.0) ** N

@@ -1,0 +1,395 @@
+"""Pins for the oracle (oracle/fif_oracle.c, oracle/direct_form.py) against what
+PAPER.md and mathematics fix -- never against the oracle itself or the CUDA path.
+
+Each test names the passage it follows.  A plausible mistake in the oracle (a
+dropped term, a wrong sign or index, a transposed operand, an off-by-one in N)
+fails at least one of these:
+  * window / eigenvalues: three independent routes (cosine sum PAPER.md:488,
+    DFT of the row PAPER.md:543, Fejer^4 closed form) + continuous limit :245
+  * dense brute force: W = Wh^2 as an explicit matrix, (I-W)^N s by
+    N mat-vecs and the SD rule on n <= 64
+  * pure tones: eigenvectors of W -> closed-form IMF and N
+  * zero-eigenvalue tone passes unchanged
+  * telescoping, no fake oscillations
+  * SPEC worked examples (tests/golden/spec_examples.json)
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import direct_form as df
+from paper_1802_01359_b200 import signals
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ----------------------------------------------------------------------------- helpers (independent routes)
+def extrema_by_definition(x):
+    """Independent definition: collapse runs of equal values, then count interior
+    points of the collapsed sequence that are strict local maxima or minima."""
+    c = [x[0]]
+    for v in x[1:]:
+        if v != c[-1]:
+            c.append(v)
+    k = 0
+    for i in range(1, len(c) - 1):
+        if (c[i] > c[i - 1] and c[i] > c[i + 1]) or (c[i] < c[i - 1] and c[i] < c[i + 1]):
+            k += 1
+    return k
+
+
+def circ_row_from_centered(v, n):
+    H = (len(v) - 1) // 2
+    row = np.zeros(n)
+    for d in range(-H, H + 1):
+        row[d % n] += v[d + H]
+    return row
+
+
+def dense_circulant(row):
+    """W_ij = c_{(i-j) mod n}."""
+    n = len(row)
+    i = np.arange(n)
+    return row[(i[:, None] - i[None, :]) % n]
+
+
+def fejer4(n, L, k):
+    """Closed form of the DFT of w = h(*)h with h_j = (L-|j|)/L^2:
+    w_hat_k = [sin(pi L k / n) / (L sin(pi k / n))]^4, w_hat_0 = 1 (derived)."""
+    k = np.asarray(k)
+    out = np.ones(k.shape)
+    nz = (k % n) != 0
+    kk = k[nz].astype(np.float64)
+    m = (L * k[nz]) % n
+    out[nz] = (np.sin(np.pi * m / n) / (L * np.sin(np.pi * kk / n))) ** 4
+    return out
+
+
+def cosine_sum_eigs(row):
+    """lambda_j = c_0 + 2 sum_{k>=1} c_k cos(2 pi j k / n) (Eq. eig2; symmetric row)."""
+    n = len(row)
+    out = np.empty(n // 2 + 1)
+    for j in range(n // 2 + 1):
+        acc = row[0]
+        for k in range(1, (n + 1) // 2):
+            acc += 2.0 * row[k] * math.cos(2.0 * math.pi * j * k / n)
+        if n % 2 == 0:
+            acc += row[n // 2] * math.cos(math.pi * j)
+        out[j] = acc
+    return out
+
+
+# ----------------------------------------------------------------------------- SPEC worked examples
+@pytest.mark.parametrize("ex", GOLDEN["count_extrema"], ids=lambda e: e["cite"])
+def test_count_extrema_spec_examples(ex):
+    assert oracle.count_extrema(np.array(ex["signal"], float))[0] == ex["k"]
+    assert df.count_extrema(np.array(ex["signal"], float)) == ex["k"]
+
+
+@pytest.mark.parametrize("ex", GOLDEN["mask_length"], ids=lambda e: e["cite"])
+def test_mask_length_spec_examples(ex):
+    assert 2 * oracle.filter_half_length(ex["nu"], ex["n"], ex["k"]) == ex["l"]
+    assert 2 * df.filter_half_length(ex["nu"], ex["n"], ex["k"]) == ex["l"]
+
+
+def test_triangle_spec_example():
+    ex = GOLDEN["triangle"][0]
+    h = oracle.triangle(ex["L"])
+    np.testing.assert_allclose(circ_row_from_centered(h, ex["n"]), ex["row"], rtol=0, atol=1e-16)
+
+
+def test_n0_bound_spec_examples():
+    for ex in GOLDEN["n0_bound"]:
+        assert oracle.n0_bound(ex["rhs"]) == ex["N0"], ex["cite"]
+    # the sequence N^N/(N+1)^(N+1) is the max of (1-l)^N l over [0,1]: check by brute force
+    for N in (1, 5, 37):
+        lam = np.linspace(0, 1, 200001)
+        assert abs(((1 - lam) ** N * lam).max() - N ** N / (N + 1) ** (N + 1)) < 1e-9
+
+
+def test_damping_spec_example():
+    ex = GOLDEN["damping"][0]
+    assert abs(df.damping(np.array([ex["lam"]]), ex["N"])[0] - ex["factor"]) < 1e-15
+
+
+# ----------------------------------------------------------------------------- extrema / mask length
+def test_count_extrema_brute_force():
+    rng = np.random.default_rng(7)
+    for trial in range(400):
+        n = int(rng.integers(3, 40))
+        x = rng.integers(-3, 4, n).astype(float)  # many ties / plateaus
+        assert oracle.count_extrema(x)[0] == extrema_by_definition(list(x)), x
+        assert df.count_extrema(x) == extrema_by_definition(list(x))
+    for trial in range(50):
+        x = rng.standard_normal(int(rng.integers(3, 500)))
+        assert oracle.count_extrema(x)[0] == extrema_by_definition(list(x))
+
+
+def test_filter_half_length_rule():
+    """l = 2 floor(nu n / k), L clamped to [2, floor((n-1)/4)] (reading A3)."""
+    rng = np.random.default_rng(3)
+    checked = 0
+    for _ in range(3000):
+        n = int(rng.integers(9, 1 << 20))
+        k = int(rng.integers(1, n))
+        xi = float(rng.choice([1.6, 1.0, 2.0, 0.75, rng.uniform(0.5, 3.0)]))
+        exact = Fraction(xi) * n / k
+        if abs(exact - round(exact)) < Fraction(1, 10 ** 9):
+            continue  # fp64 rounding may legitimately decide these (reading A8)
+        q = math.floor(exact)
+        L = min(max(q, 2), (n - 1) // 4)
+        assert oracle.filter_half_length(xi, n, k) == L
+        Lw = min(max(2 * q, 2), (n - 1) // 4)
+        assert oracle.filter_half_length(xi, n, k, oracle.WINDOW_TRI_SQ_WIDE) == Lw
+        checked += 1
+    assert checked > 2500
+    # exact-integer quotient decided in fp64 (A8): 1.6 * 81920 / 1024 = 128 exactly
+    assert oracle.filter_half_length(1.6, 5 << 14, 1024) == 128
+
+
+# ----------------------------------------------------------------------------- window & spectrum (P3, P4)
+@pytest.mark.parametrize("L", [1, 2, 3, 5, 8, 16, 33])
+def test_window_shape(L):
+    """w = h(*)h: nonneg, symmetric, unit sum (Def. window); h(*)h by numpy.convolve."""
+    h = oracle.triangle(L)
+    w = oracle.window(L)
+    assert len(w) == 4 * L - 3
+    np.testing.assert_allclose(h.sum(), 1.0, atol=1e-15)
+    np.testing.assert_allclose(w, np.convolve(h, h), atol=1e-17)
+    np.testing.assert_allclose(w, w[::-1], atol=0)
+    assert (w >= 0).all() and abs(w.sum() - 1) < 1e-14
+    # h_j = (L - |j|) / L^2 (triangle of PAPER.md:238 sampled at j, unit sum)
+    j = np.arange(-(L - 1), L)
+    np.testing.assert_allclose(h, (L - np.abs(j)) / L ** 2, rtol=1e-14)
+
+
+@pytest.mark.parametrize("n,L", [(64, 2), (65, 7), (100, 24), (257, 32), (1024, 12), (1024, 16), (4096, 1023),
+                                 (3 << 10, 100), (5 << 10, 77)])
+def test_eigenvalue_routes_agree(n, L):
+    """Three routes: cosine sum, DFT of the row (numpy FFT) and the
+    Fejer^4 closed form must agree; Thm Spectra / Cor. double convolution invariants."""
+    row = circ_row_from_centered(oracle.window(L), n)
+    ev_fft = np.fft.rfft(row)
+    assert np.abs(ev_fft.imag).max() < 1e-14  # real spectrum
+    ev_cos = cosine_sum_eigs(row) if n <= 1024 else None
+    ev_cf = fejer4(n, L, np.arange(n // 2 + 1))
+    np.testing.assert_allclose(ev_fft.real, ev_cf, rtol=0, atol=5e-15)
+    if ev_cos is not None:
+        np.testing.assert_allclose(ev_cos, ev_cf, rtol=0, atol=5e-14)
+    np.testing.assert_allclose(df.eigenvalues(n, L), ev_cf, atol=5e-15)
+    assert abs(ev_cf[0] - 1) < 1e-15
+    assert (ev_fft.real[1:] < 1 - 1e-12).all()  # unique unit eigenvalue
+    assert (ev_fft.real > -1e-15).all()         # spectrum in [0,1)
+
+
+def test_delta_filter_all_ones():
+    """c0 = 1 -> all eigenvalues equal 1.  L = 1 gives h = w = delta."""
+    assert np.allclose(oracle.window(1), [1.0])
+    assert np.allclose(df.eigenvalues(33, 1), 1.0)
+
+
+def test_continuous_triangle_limit():
+    """Continuous FT of the unit-area triangle of half-width a (PAPER.md:245 with L=a):
+    w_hat(xi) = (1/a) sin^2(a pi xi)/(pi xi)^2 = sinc^2(a xi).  Our h at L samples on a grid of
+    n points is that triangle with a = L/n, so h_hat_k -> sinc^2(L k / n) for k << n, and
+    w_hat = h_hat^2."""
+    n, L = 1 << 16, 512
+    row = circ_row_from_centered(oracle.window(L), n)
+    ev = np.fft.rfft(row).real
+    k = np.arange(1, 400)
+    cont = np.sinc(L * k / n) ** 4
+    assert np.abs(ev[1:400] - cont).max() < 5e-5  # O((k/n)^2) + O(1/L^2) discretisation
+
+
+# ----------------------------------------------------------------------------- dense brute force (P2)
+@pytest.mark.parametrize("n", [16, 33, 64])
+def test_dense_brute_force_inner(n):
+    """(I-W)^N s with W = Wh^2 built as explicit matrices."""
+    rng = np.random.default_rng(n)
+    for L in range(2, (n - 1) // 4 + 1):
+        Wh = dense_circulant(circ_row_from_centered(oracle.triangle(L), n))
+        Wh = Wh / Wh.sum(axis=1, keepdims=True)  # scale each row by its sum
+        W = Wh @ Wh
+        s = rng.standard_normal(n)
+        A = np.eye(n) - W
+        for N in (1, 5, 50, 200):
+            ref = s.copy()
+            for _ in range(N):
+                ref = A @ ref
+            got, Ngot, _, _ = oracle.inner(s, L, 0.0, N)  # delta = 0: never stops early -> N applications
+            assert Ngot == N
+            assert np.abs(got - ref).max() <= 1e-12 * np.linalg.norm(s)
+
+
+@pytest.mark.parametrize("n", [16, 33, 64])
+def test_dense_brute_force_sd_rule(n):
+    """N = first m with ||s_{m+1}-s_m|| / ||s_m|| <= delta (reading A5)."""
+    rng = np.random.default_rng(100 + n)
+    for L in range(2, (n - 1) // 4 + 1):
+        Wh = dense_circulant(circ_row_from_centered(oracle.triangle(L), n))
+        W = Wh @ Wh
+        s = rng.standard_normal(n)
+        for delta in (0.3, 0.1, 1e-2, 1e-3):
+            c = s.copy()
+            Nref = 60
+            for m in range(1, 61):
+                cn = c - W @ c
+                sd = np.linalg.norm(cn - c) / np.linalg.norm(c)
+                c = cn
+                if sd <= delta:
+                    Nref = m
+                    break
+            imf, N, sdN, _ = oracle.inner(s, L, delta, 60)
+            assert N == Nref, (L, delta)
+            assert np.abs(imf - c).max() <= 1e-12 * np.linalg.norm(s)
+
+
+# ----------------------------------------------------------------------------- pure tones (P5, P8)
+def test_zero_eigenvalue_tone_passes_unchanged():
+    """w_hat_k = 0 exactly when L k = 0 mod n (n=1024, L=16, k=64): (I-W) fixes the tone, SD = 0,
+    N = 1 and IMF = tone (PAPER.md:102 chi_{w_hat=0}, :559-562 Z has ones there)."""
+    n, L, f = 1024, 16, 64
+    x = np.cos(2 * np.pi * f * np.arange(n) / n + 0.7)
+    imf, N, sd, _ = oracle.inner(x, L, 1e-3, 200)
+    assert N == 1 and sd < 1e-13
+    assert np.abs(imf - x).max() < 1e-13
+
+
+@pytest.mark.parametrize("f,L", [(64, 12), (40, 30), (100, 7), (511, 9)])  # w_hat_f small: (1-w)^200 stays far above rounding
+def test_pure_tone_closed_form(f, L):
+    """A tone at bin f is an eigenvector of W: (I-W)^N x = (1-w_hat_f)^N x and
+    SD_N = w_hat_f for every N, so N = 1 if w_hat_f <= delta else max_inner."""
+    n = 1024
+    x = np.cos(2 * np.pi * f * np.arange(n) / n + 0.3)
+    wf = fejer4(n, L, np.array([f]))[0]
+    for delta in (1e-3, 0.5):
+        imf, N, sd, _ = oracle.inner(x, L, delta, 200)
+        Nexp = 1 if wf <= delta else 200
+        assert N == Nexp
+        assert abs(sd - wf) <= 1e-12 + 1e-9 * wf
+        np.testing.assert_allclose(imf, (1 - wf) ** N * x, atol=1e-12)
+
+
+def test_pure_tone_full_pipeline():
+    """n=1024, f=64, phi=0.3 through the whole outer loop: k = 127 interior extrema, L = floor(1.6*1024/127) = 12,
+    IMF_1 = (1 - w_hat_64)^200 x (w_hat from the closed form)."""
+    n, f = 1024, 64
+    x = np.cos(2 * np.pi * f * np.arange(n) / n + 0.3)
+    o = oracle.decompose(x)
+    k = extrema_by_definition(list(x))
+    assert o["k"][0, 0] == k
+    L = math.floor(Fraction(1.6) * n / k)
+    assert o["l"][0, 0] == 2 * L
+    wf = fejer4(n, L, np.array([f]))[0]
+    assert o["N"][0, 0] == 200
+    np.testing.assert_allclose(o["imfs"][0, 0], (1 - wf) ** 200 * x, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- outer loop invariants (P1, P6)
+def _remainders(imfs, s, M):
+    r = [s.copy()]
+    for m in range(M):
+        r.append(r[-1] - imfs[m])
+    return r
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_telescoping_and_no_fake_oscillations(seed):
+    """sum IMFs + trend = s and |DFT(IMF)_k| <= |DFT(r)_k|."""
+    s = signals.cfg0_signal(seed)
+    o = oracle.decompose(s)
+    M = int(o["count"][0])
+    imfs = o["imfs"][0]
+    assert np.abs(imfs[: M + 1].sum(0) - s).max() <= 1e-13 * np.linalg.norm(s)
+    assert np.all(imfs[M + 1:] == 0)
+    rs = _remainders(imfs, s, M)
+    for m in range(M):
+        R = np.abs(np.fft.rfft(rs[m]))
+        F = np.abs(np.fft.rfft(imfs[m]))
+        assert (F <= R + 1e-9 * np.linalg.norm(rs[m])).all()
+
+
+def test_trend_and_termination():
+    """Monotone / constant signals: zero IMFs, trend = s.
+    White noise terminates within max_imfs (Thm IF_outer_conv analog)."""
+    n = 256
+    for s in (np.linspace(-1, 2, n), np.full(n, 3.0), np.linspace(0, 1, n) ** 2):
+        o = oracle.decompose(s)
+        assert o["count"][0] == 0
+        np.testing.assert_array_equal(o["imfs"][0, 0], s)
+    noise = np.random.default_rng(5).standard_normal(4096)
+    o = oracle.decompose(noise, max_imfs=10)
+    assert 1 <= o["count"][0] <= 10
+
+
+def test_nonfinite_input_flagged():
+    s = signals.cfg0_signal(0)
+    s[17] = np.nan
+    o = oracle.decompose(s)
+    assert o["count"][0] == -1
+
+
+# ----------------------------------------------------------------------------- SD monotonicity (P7)
+def test_sd_monotone_in_N():
+    """SD_N^2 = E_N[w_hat^2] under weights c p a^{2(N-1)}: non-increasing in N (P7).
+    This is what makes the GPU's cap-first probe + bisection equal to the paper's linear scan."""
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        n = int(rng.choice([64, 256, 1024, 4096]))
+        L = int(rng.integers(2, (n - 1) // 4 + 1))
+        lam = df.eigenvalues(n, L)
+        rhat = (rng.standard_normal(n // 2 + 1) + 1j * rng.standard_normal(n // 2 + 1)) * np.exp(
+            rng.uniform(-8, 3, n // 2 + 1))
+        curve = df.sd_curve(rhat, lam, n, 200)
+        assert (np.diff(curve) <= 1e-12 * curve[:-1]).all()
+
+
+# ----------------------------------------------------------------------------- the two engines agree
+def test_td_vs_direct_form_cfg0():
+    """The literal iteration (fif_oracle.c) and the paper's FFT direct form (direct_form.py) give
+    identical integers and IMFs to ~1e-11 (the direct form is the same iterate)."""
+    for s in (signals.cfg0_signal(0), signals.cfg0_signal(0, noise=0.0)):
+        o = oracle.decompose(s)
+        d = df.decompose(s)
+        M = int(o["count"][0])
+        assert M == d["M"]
+        assert list(o["l"][0, :M]) == d["l"]
+        assert list(o["N"][0, :M]) == d["N"]
+        floor = 1e-5 * np.linalg.norm(s)
+        for m in range(M + 1):
+            a, b = o["imfs"][0, m], d["imfs"][m]
+            assert np.linalg.norm(a - b) / max(np.linalg.norm(a), floor) < 1e-10
+
+
+@pytest.mark.slow
+def test_td_vs_direct_form_cfg1_sample():
+    s = signals.make_batch("cfg1", batch=4)
+    o = oracle.decompose(s)
+    for b in range(4):
+        d = df.decompose(s[b])
+        M = int(o["count"][b])
+        assert M == d["M"]
+        assert list(o["l"][b, :M]) == d["l"] and list(o["N"][b, :M]) == d["N"]
+        floor = 1e-5 * np.linalg.norm(s[b])
+        for m in range(M + 1):
+            a, c = o["imfs"][b, m], d["imfs"][m]
+            assert np.linalg.norm(a - c) / max(np.linalg.norm(a), floor) < 1e-10
+
+
+def test_wide_window_two_tone_separation():
+    """SPEC acceptance #8 under reading R3 (FIF_WINDOW_TRI_SQ_WIDE): sin(2pi 4t)+sin(2pi 32t),
+    n = 512: exactly two IMFs with max-abs > 0.5, correlated > 0.95 with the 32- and the 4-tone."""
+    n = 512
+    t = np.arange(n) / n
+    hi, lo = np.sin(2 * np.pi * 32 * t), np.sin(2 * np.pi * 4 * t)
+    o = oracle.decompose(hi + lo, window=oracle.WINDOW_TRI_SQ_WIDE)
+    M = int(o["count"][0])
+    sig = [o["imfs"][0, m] for m in range(M) if np.abs(o["imfs"][0, m]).max() > 0.5]
+    assert len(sig) == 2
+    assert np.corrcoef(sig[0], hi)[0, 1] > 0.95
+    assert np.corrcoef(sig[1], lo)[0, 1] > 0.95
