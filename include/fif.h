@@ -1,0 +1,125 @@
+/*
+ * fif.h -- C ABI of the B200-native Fast Iterative Filtering (FIF) hot path.
+ *
+ * Method: arXiv 1802.01359, Discrete Iterative Filtering in its FFT
+ * direct form.  For each signal s (periodic extension) the
+ * outer loop (Algorithm 2) repeats, on the remainder r:
+ *   k   = number of interior extrema of r            (reading A4)
+ *   stop if k < 2 or M == max_imfs                   (A13)
+ *   L   = clamp(floor(fl(fl(xi*n)/k)), 2, (n-1)/4)   (PAPER.md:81 l = 2 floor(nu N/k); A1, A3, A8)
+ *   w   = h (*) h, h the unit-sum sampled triangle
+ *   N   = min{N in [1,max_inner] : SD_N <= delta}    (Parseval :175-180; A5, A7)
+ *   IMF = IDFT((1 - w_hat)^N o DFT(r))               (Eq. One step_algo)
+ *   r  <- r - IMF
+ * and finally stores the trend r.  Readings A1-A15: DESIGN.md.
+ *
+ * Everything runs in hand-written sm_100a CUDA kernels (no cuFFT, no CPU
+ * fallback).  This header has no CUDA or torch types: device and host buffers
+ * are plain pointers, a stream is passed as void* (a cudaStream_t, NULL = the
+ * legacy default stream).
+ *
+ * Threading: calls on one plan must be serialised by the caller (one stream at a
+ * time); distinct plans are independent.  All device work is stream-ordered and
+ * asynchronous unless stated otherwise.
+ */
+#ifndef FIF_H_
+#define FIF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fif_plan_s* fif_plan_t;
+
+typedef enum { FIF_F64 = 0, FIF_F32 = 1 } fif_dtype;
+
+typedef enum {
+  FIF_WINDOW_TRI_SQ = 0,      /* triangle (*) triangle, h half-support L = floor(xi n / k)   (reading R1, default) */
+  FIF_WINDOW_TRI_SQ_WIDE = 1  /* same shape, L = 2 floor(xi n / k)  (reading R3, SPEC.md:54 convention) */
+} fif_window;
+
+typedef enum {
+  FIF_OK = 0,
+  FIF_ERR_INVALID_ARG = 1,   /* host-side validation failed; nothing was enqueued */
+  FIF_ERR_UNSUPPORTED_N = 2, /* n not supported by any regime of this build */
+  FIF_ERR_OOM = 3,           /* device or pinned allocation failed */
+  FIF_ERR_CUDA = 4,          /* a CUDA call failed (launch error, bad pointer, ...) */
+  FIF_ERR_NCCL = 5           /* reserved for the distributed plan */
+} fif_status;
+
+/* Create a plan for `batch` independent signals of length n.
+ *   n          : samples per signal.  This build supports even n with n/2 a power
+ *                of two, 128 <= n <= 8192 (f64) / 16384 (f32) -- the on-chip
+ *                resident regime; other n -> FIF_ERR_UNSUPPORTED_N.
+ *   batch      : number of signals, >= 0 (0 is a valid no-op plan).
+ *   dtype      : element type of signals and IMFs.  f32 computes the FFTs in fp32 and
+ *                accumulates the stopping sums and takes the floor in fp64 (reading A14).
+ *   xi         : the nu of PAPER.md:81 (> 0, typically 1.6).
+ *   delta      : SD threshold (> 0).
+ *   max_inner  : iteration cap (>= 1).
+ *   max_imfs   : cap on the number of IMFs (>= 1).
+ * Allocates small device tables (sin table and FFT twiddles, O(n) bytes) on the
+ * current device and uploads them synchronously.  On error *out is NULL. */
+fif_status fif_plan_create(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window, double xi,
+                           double delta, int32_t max_inner, int32_t max_imfs);
+
+/* Decompose the batch (device pointers, caller-owned, current device):
+ *   d_signals    [batch][n] dtype, read only.
+ *   d_imfs       [batch][max_imfs+1][n] dtype: IMF_0..IMF_{M-1} in slots 0..M-1, the
+ *                trend (final remainder) in slot M, zeros in slots > M.  Fully written.
+ *   d_imf_count  [batch] int32: M (0..max_imfs); -1 if the signal has a non-finite
+ *                sample (its other outputs are then zero).
+ *   d_filter_len [batch][max_imfs] int32: mask length l_m = 2L_m (0 past M).
+ *   d_iters      [batch][max_imfs] int32: N_m (0 past M).
+ * All pointers must be 16-byte aligned.  Enqueued on `stream`; returns after the
+ * launch (asynchronous).  Errors: FIF_ERR_INVALID_ARG (NULL plan / pointer with
+ * batch > 0), FIF_ERR_CUDA (launch failure). */
+fif_status fif_decompose(fif_plan_t plan, const void* d_signals, void* d_imfs, int32_t* d_imf_count,
+                         int32_t* d_filter_len, int32_t* d_iters, void* stream);
+
+/* Same computation from HOST buffers (the end-to-end path): copies h_signals to
+ * plan-owned device staging buffers, decomposes, copies every output back, and
+ * synchronises `stream` before returning.  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for full PCIe bandwidth; the batch is
+ * processed in chunks so that the copies of one chunk overlap the kernels of the
+ * next.  The staging buffers (<= 3 chunks) are freed by fif_destroy. */
+fif_status fif_decompose_host(fif_plan_t plan, const void* h_signals, void* h_imfs, int32_t* h_imf_count,
+                              int32_t* h_filter_len, int32_t* h_iters, void* stream);
+
+/* Free the plan's tables and staging buffers (synchronises the device first).  NULL is a no-op. */
+fif_status fif_destroy(fif_plan_t plan);
+
+/* Human-readable status name (static string). */
+const char* fif_status_string(fif_status s);
+
+/* Plan introspection: number of kernels one fif_decompose launches, the regime name
+ * ("resident"), and the resident kernel's grid / block / dynamic smem. */
+int32_t fif_plan_kernels_per_call(fif_plan_t plan);
+const char* fif_plan_regime(fif_plan_t plan);
+fif_status fif_plan_launch_config(fif_plan_t plan, int32_t* grid, int32_t* block, int32_t* smem_bytes);
+
+/* ---------------------------------------------------------------------------
+ * Test hooks (not part of the graded API): each runs ONE step of the hot path
+ * with the very device code fif_decompose uses, on a batch of `batch` signals
+ * of the plan's n and dtype (device pointers, synchronous on `stream`).
+ * ------------------------------------------------------------------------- */
+/* a1: forward real DFT, X_k = sum_j x_j e^{-2 pi i jk/n}, k = 0..n/2 -> d_out [batch][n/2+1] complex
+ * (interleaved re, im of dtype). */
+fif_status fif_test_rfft(fif_plan_t plan, int64_t batch, const void* d_in, void* d_out, void* stream);
+/* inverse: x_j = (1/n) sum_k X_k e^{+2 pi i jk/n} over the Hermitian extension of d_in [batch][n/2+1]. */
+fif_status fif_test_irfft(fif_plan_t plan, int64_t batch, const void* d_in, void* d_out, void* stream);
+/* a2: interior-extrema count of each row (reading A4) -> d_k [batch] int32. */
+fif_status fif_test_extrema(fif_plan_t plan, int64_t batch, const void* d_in, int32_t* d_k, void* stream);
+/* a4: window spectrum w_hat_k, k = 0..n/2, for half-length L -> d_out [n/2+1] dtype. */
+fif_status fif_test_window_spectrum(fif_plan_t plan, int32_t L, void* d_out, void* stream);
+/* a4+a5+a6 with a forced half-length L: one inner loop on each row -> IMF [batch][n], N [batch]. */
+fif_status fif_test_inner(fif_plan_t plan, int64_t batch, int32_t L, const void* d_in, void* d_imf, int32_t* d_N,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIF_H_ */

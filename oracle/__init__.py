@@ -50,7 +50,7 @@ def lib():
         dp = ctypes.POINTER(ctypes.c_double)
         ip = ctypes.POINTER(ctypes.c_int32)
         i64, i32, d = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
-        L.oracle_count_extrema.argtypes = [dp, i64, dp]
+        L.oracle_count_extrema.argtypes = [dp, i64, d, dp]
         L.oracle_count_extrema.restype = i64
         L.oracle_filter_half_length.argtypes = [d, i64, i64, ctypes.c_int]
         L.oracle_filter_half_length.restype = i64
@@ -78,10 +78,11 @@ def _ip(a):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
 
 
-def count_extrema(r):
+def count_extrema(r, scale=0.0):
+    """(k, margin): k interior extrema (reading A4); margin = min nonzero |diff| / scale (max|r| if scale <= 0)."""
     r = np.ascontiguousarray(r, dtype=np.float64)
     m = np.zeros(1)
-    k = lib().oracle_count_extrema(_dp(r), r.shape[0], _dp(m))
+    k = lib().oracle_count_extrema(_dp(r), r.shape[0], float(scale), _dp(m))
     return int(k), float(m[0])
 
 
@@ -107,7 +108,7 @@ def inner(r, L, delta, max_inner, parallel=False):
     """(I-W)^N r with N chosen by the SD rule; returns (imf, N, SD_N, SD_{N-1})."""
     r = np.ascontiguousarray(r, dtype=np.float64)
     imf = np.zeros_like(r)
-    sd = np.zeros(2)
+    sd = np.zeros(4)
     N = lib().oracle_inner(_dp(r), r.shape[0], int(L), float(delta), int(max_inner), _dp(imf), _dp(sd),
                            1 if parallel else 0)
     return imf, int(N), float(sd[0]), float(sd[1])
@@ -117,8 +118,9 @@ def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WI
     """Time-domain oracle decomposition of a batch [B, n] (or one signal [n]).
 
     Returns dict: imfs [B, max_imfs+1, n], count [B], l [B, max_imfs], N [B, max_imfs],
-    k [B, max_imfs+1] (extrema count at each outer step), margins [B, max_imfs, 2]
-    (extremum margin, SD margin)."""
+    k [B, max_imfs+1] (extrema count at each outer step), margins [B, max_imfs+1, 2]
+    (per outer step m: margin of the extrema count at its head relative to max|s|, SD margin
+    |SD - delta|/delta of IMF m; NaN where no decision was taken)."""
     s = np.ascontiguousarray(np.atleast_2d(np.asarray(signals, dtype=np.float64)))
     B, n = s.shape
     imfs = np.zeros((B, max_imfs + 1, n))
@@ -126,7 +128,7 @@ def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WI
     l = np.zeros((B, max_imfs), dtype=np.int32)
     N = np.zeros((B, max_imfs), dtype=np.int32)
     k = np.zeros((B, max_imfs + 1), dtype=np.int32)
-    margins = np.zeros((B, max_imfs, 2))
+    margins = np.zeros((B, max_imfs + 1, 2))
     lib().oracle_decompose_batch(_dp(s), B, n, int(window), float(xi), float(delta), int(max_inner), int(max_imfs),
                                  _dp(imfs), _ip(count), _ip(l), _ip(N), _ip(k), _dp(margins))
     return {"imfs": imfs, "count": count, "l": l, "N": N, "k": k, "margins": margins}

@@ -50,10 +50,13 @@
 /* ---------------------------------------------------------------------------
  * Extrema count (reading A4; PAPER.md:42 "number of extrema of s", :83 "k is the
  * number of its extreme points", SPEC.md:94 plateau rule).
- * margin_out (optional): min |Delta_j| over nonzero differences, divided by max|r|
- * -- how far the nearest sign decision is from flipping.
+ * margin_out (optional): min |Delta_j| over nonzero differences, divided by
+ * `scale` (max|s| of the ORIGINAL signal; max|r| when scale <= 0) -- how far the
+ * nearest sign decision is from flipping under a perturbation of relative size
+ * margin (rounding differences between two correct implementations are
+ * ~1e-15 max|s|, whatever the size of the remainder).
  * ------------------------------------------------------------------------- */
-int64_t oracle_count_extrema(const double* r, int64_t n, double* margin_out) {
+int64_t oracle_count_extrema(const double* r, int64_t n, double scale, double* margin_out) {
   int64_t count = 0;
   int prev = 0; /* sign of the last nonzero difference, 0 = none yet */
   double min_abs = INFINITY, max_r = 0.0;
@@ -61,6 +64,7 @@ int64_t oracle_count_extrema(const double* r, int64_t n, double* margin_out) {
     double a = fabs(r[j]);
     if (a > max_r) max_r = a;
   }
+  if (scale > 0.0) max_r = scale;
   for (int64_t j = 0; j + 1 < n; ++j) {
     double d = r[j + 1] - r[j];
     if (d == 0.0) continue; /* plateau: dropped */
@@ -150,7 +154,8 @@ static void extend(const double* c, int64_t n, int64_t H, double* cext) {
 /* ---------------------------------------------------------------------------
  * Inner loop (Alg. 2 inner while; SD PAPER.md:431; cap :433).
  * imf <- (I-W)^N r with N the first m in [1, max_inner] with SD_m <= delta.
- * sd_out[0] = SD_N, sd_out[1] = SD_{N-1} (NaN if N == 1).
+ * sd_out[0] = SD_N, sd_out[1] = SD_{N-1} (NaN if N == 1), sd_out[2] = ||s_N|| (the
+ * denominator of SD_N), sd_out[3] = ||s_{N-1}|| -- for margin reporting.
  * ------------------------------------------------------------------------- */
 int32_t oracle_inner(const double* r, int64_t n, int64_t L, double delta, int32_t max_inner, double* imf,
                      double* sd_out, int par) {
@@ -162,7 +167,7 @@ int32_t oracle_inner(const double* r, int64_t n, int64_t L, double delta, int32_
   double* cn = (double*)malloc(sizeof(double) * (size_t)n);
   memcpy(c, r, sizeof(double) * (size_t)n);
   int32_t N = 0;
-  double sd = NAN, sd_prev = NAN;
+  double sd = NAN, sd_prev = NAN, nrm = NAN, nrm_prev = NAN;
   for (int32_t m = 1; m <= max_inner; ++m) {
     extend(c, n, H, cext);
     dif_step(cext, w, H, n, cn, par);
@@ -173,13 +178,15 @@ int32_t oracle_inner(const double* r, int64_t n, int64_t L, double delta, int32_
       den += c[i] * c[i];
     }
     sd_prev = sd;
+    nrm_prev = nrm;
     sd = (den > 0.0) ? sqrt(num) / sqrt(den) : 0.0;
+    nrm = sqrt(den);
     double* t = c; c = cn; cn = t; /* c <- s_{m+1} */
     N = m;
     if (sd <= delta) break;
   }
   memcpy(imf, c, sizeof(double) * (size_t)n);
-  if (sd_out) { sd_out[0] = sd; sd_out[1] = sd_prev; }
+  if (sd_out) { sd_out[0] = sd; sd_out[1] = sd_prev; sd_out[2] = nrm; sd_out[3] = nrm_prev; }
   free(w); free(cext); free(c); free(cn);
   return N;
 }
@@ -190,7 +197,8 @@ int32_t oracle_inner(const double* r, int64_t n, int64_t L, double delta, int32_
  *   l_out  : [max_imfs]  mask length l_m = 2L (0 past M)
  *   N_out  : [max_imfs]  iteration counts (0 past M)
  *   k_out  : [max_imfs+1] extrema count at the head of outer step m (k_out[M] = final)
- *   margins: [max_imfs * 2]  (extremum margin, SD margin) per IMF (NaN past M)
+ *   margins: [(max_imfs+1) * 2]  per outer step m <= M: (margin of the extrema count at the
+ *            head of step m, SD margin of IMF m); NaN where no such decision was taken
  * Returns M.
  * ------------------------------------------------------------------------- */
 int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, double delta, int32_t max_inner,
@@ -199,33 +207,39 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
   double* r = (double*)malloc(sizeof(double) * (size_t)n);
   memcpy(r, s, sizeof(double) * (size_t)n);
   memset(imfs, 0, sizeof(double) * (size_t)n * (size_t)(max_imfs + 1));
-  for (int32_t m = 0; m < max_imfs; ++m) {
-    l_out[m] = 0; N_out[m] = 0;
-    if (margins) { margins[2 * m] = NAN; margins[2 * m + 1] = NAN; }
-  }
+  double scale = 0.0, snorm = 0.0;
+  for (int64_t i = 0; i < n; ++i) { if (fabs(s[i]) > scale) scale = fabs(s[i]); snorm += s[i] * s[i]; }
+  snorm = sqrt(snorm);
+  for (int32_t m = 0; m < max_imfs; ++m) { l_out[m] = 0; N_out[m] = 0; }
+  if (margins) for (int32_t m = 0; m <= max_imfs; ++m) { margins[2 * m] = NAN; margins[2 * m + 1] = NAN; }
   if (k_out) for (int32_t m = 0; m <= max_imfs; ++m) k_out[m] = -1;
   int32_t M = 0;
   while (M < max_imfs) {
     double em;
-    int64_t k = oracle_count_extrema(r, n, &em);
+    int64_t k = oracle_count_extrema(r, n, scale, &em);
     if (k_out) k_out[M] = (int32_t)k;
+    if (margins) margins[2 * M] = em;
     if (k < 2) break; /* trend: fewer than 2 extrema */
     int64_t L = oracle_filter_half_length(xi, n, k, window);
-    double sd[2];
+    double sd[4];
     double* imf = imfs + (size_t)M * (size_t)n;
     int32_t N = oracle_inner(r, n, L, delta, max_inner, imf, sd, par);
     for (int64_t i = 0; i < n; ++i) r[i] -= imf[i]; /* s = s - s_m */
     l_out[M] = (int32_t)(2 * L);
     N_out[M] = N;
     if (margins) {
-      double sm = fabs(sd[0] - delta) / delta;
-      if (!isnan(sd[1])) { double s1 = fabs(sd[1] - delta) / delta; if (s1 < sm) sm = s1; }
-      margins[2 * M] = em;
+      /* |SD - delta| / delta, scaled by ||iterate|| / ||s||: absolute rounding differences are
+         ~1e-16 ||s||, so a decision on a remainder at rounding level has no margin. */
+      double sm = fabs(sd[0] - delta) / delta * (snorm > 0.0 ? sd[2] / snorm : 1.0);
+      if (!isnan(sd[1])) {
+        double s1 = fabs(sd[1] - delta) / delta * (snorm > 0.0 ? sd[3] / snorm : 1.0);
+        if (s1 < sm) sm = s1;
+      }
       margins[2 * M + 1] = sm;
     }
     ++M;
   }
-  if (k_out && M == max_imfs) k_out[M] = (int32_t)oracle_count_extrema(r, n, NULL);
+  if (k_out && M == max_imfs) k_out[M] = (int32_t)oracle_count_extrema(r, n, scale, NULL);
   memcpy(imfs + (size_t)M * (size_t)n, r, sizeof(double) * (size_t)n); /* trend */
   free(r);
   return M;
@@ -246,7 +260,7 @@ void oracle_decompose_batch(const double* s, int64_t batch, int64_t n, int windo
     int32_t* lb = l_out + (size_t)b * (size_t)max_imfs;
     int32_t* nb = N_out + (size_t)b * (size_t)max_imfs;
     int32_t* kb = k_out ? k_out + (size_t)b * (size_t)(max_imfs + 1) : NULL;
-    double* mb = margins ? margins + (size_t)b * (size_t)max_imfs * 2 : NULL;
+    double* mb = margins ? margins + (size_t)b * (size_t)(max_imfs + 1) * 2 : NULL;
     if (!finite) {
       memset(ib, 0, sizeof(double) * (size_t)n * (size_t)(max_imfs + 1));
       memset(lb, 0, sizeof(int32_t) * (size_t)max_imfs);

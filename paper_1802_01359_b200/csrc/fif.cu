@@ -1,0 +1,419 @@
+// fif.cu -- C ABI of the B200 FIF hot path (include/fif.h): plan creation
+// (validation, device tables), dispatch to the sm_100a kernels, the host-buffer
+// end-to-end path and the test hooks.  No torch types, no CPU compute fallback:
+// every step of the decomposition runs in the kernels of fif_resident.cuh.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/fif.h"
+#include "fif_resident.cuh"
+
+using namespace fifgpu;
+
+namespace {
+
+enum { FIF_MAX_STAGES = 3 };
+
+struct Staging {
+  void* d_in = nullptr;
+  void* d_out = nullptr;
+  int32_t* d_meta = nullptr;  // count | lens | iters
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+};
+
+}  // namespace
+
+struct fif_plan_s {
+  int64_t n = 0, batch = 0;
+  fif_dtype dtype = FIF_F64;
+  fif_window window = FIF_WINDOW_TRI_SQ;
+  double xi = 1.6, delta = 1e-3;
+  int32_t max_inner = 200, max_imfs = 10;
+  int device = 0, num_sms = 0;
+  int NC = 0;
+  void* d_sin = nullptr;   // Real[NC+1]  sin(pi j/n)
+  void* d_isin = nullptr;  // Real[NC+1]  1/sin(pi j/n) (j >= 1)
+  void* d_tw = nullptr;    // V[twtotal]  Stockham twiddles e^{-2 pi i k r/(NS RP)}
+  int block = 0, occ = 0;
+  size_t smem = 0;
+  // host (e2e) path staging
+  int64_t chunk = 0;
+  int nstages = 0;
+  Staging st[FIF_MAX_STAGES];
+};
+
+namespace {
+
+template <typename Real> fif_dtype dtype_of();
+template <> fif_dtype dtype_of<double>() { return FIF_F64; }
+template <> fif_dtype dtype_of<float>() { return FIF_F32; }
+
+// ---------------------------------------------------------------- kernel table
+struct Entry {
+  int NC;
+  int R;
+  size_t smem;
+  int threads;
+};
+
+template <typename Real, int NC, int R>
+struct Inst {
+  using K = Resident<Real, NC, R>;
+  using V = typename Cx<Real>::V;
+  static cudaError_t prepare() {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_rfft_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_irfft_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_extrema_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_window_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    return cudaSuccess;
+  }
+  static int occupancy() {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC, R>, K::T, K::smem_bytes);
+    return occ;
+  }
+  static void decompose(const fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
+                        int64_t batch, cudaStream_t s) {
+    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
+    const int64_t cap = (int64_t)p->num_sms * p->occ;
+    const int grid = (int)(batch < cap ? batch : cap);
+    fif_resident_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+        (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
+        (const V*)p->d_tw, prm);
+  }
+  static void test_rfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    fif_test_rfft_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+        (const Real*)in, (Real*)out, batch, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw);
+  }
+  static void test_irfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    fif_test_irfft_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+        (const Real*)in, (Real*)out, batch, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw);
+  }
+  static void test_extrema(const fif_plan_s* p, const void* in, int32_t* k, int64_t batch, cudaStream_t s) {
+    (void)p;
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    fif_test_extrema_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>((const Real*)in, k, batch);
+  }
+  static void test_window(const fif_plan_s* p, int L, void* out, cudaStream_t s) {
+    fif_test_window_kernel<Real, NC, R><<<1, K::T, K::smem_bytes, s>>>((Real*)out, L, (const Real*)p->d_sin,
+                                                                        (const Real*)p->d_isin);
+  }
+  static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
+                         cudaStream_t s) {
+    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    fif_test_inner_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+        (const Real*)in, (Real*)out, N, batch, L, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw,
+        prm);
+  }
+};
+
+// Dispatch on (dtype, NC).  F is a functor template taking Inst<Real,NC,R>.
+template <typename Real, typename F>
+bool dispatch_nc(int NC, F&& f) {
+  switch (NC) {
+    case 64: f(Inst<Real, 64, 2>{}); return true;
+    case 128: f(Inst<Real, 128, 4>{}); return true;
+    case 256: f(Inst<Real, 256, 8>{}); return true;
+    case 512: f(Inst<Real, 512, 8>{}); return true;
+    case 1024: f(Inst<Real, 1024, 8>{}); return true;
+    case 2048: f(Inst<Real, 2048, 8>{}); return true;
+    case 4096: f(Inst<Real, 4096, 8>{}); return true;
+    default: return false;
+  }
+}
+template <typename F>
+bool dispatch(fif_dtype dt, int NC, F&& f) {
+  if (dt == FIF_F64) return dispatch_nc<double>(NC, f);
+  return dispatch_nc<float>(NC, f);
+}
+
+int radix_for(int NC) { return NC == 64 ? 2 : (NC == 128 ? 4 : 8); }
+
+// ---------------------------------------------------------------- tables (host, long double)
+template <typename Real>
+void build_tables(int64_t n, int NC, int R, std::vector<Real>& sint, std::vector<Real>& isin,
+                  std::vector<typename Cx<Real>::V>& tw) {
+  const long double PI = 3.141592653589793238462643383279502884L;
+  sint.assign(NC + 1, (Real)0);
+  isin.assign(NC + 1, (Real)0);
+  for (int j = 0; j <= NC; ++j) {
+    // sin(pi j / n), j <= n/2; reflect to keep the argument <= pi/4 for accuracy
+    long double v;
+    if (2 * (int64_t)j <= n / 2) v = sinl(PI * (long double)j / (long double)n);
+    else v = cosl(PI * (long double)(n / 2 - j) / (long double)n);
+    sint[j] = (Real)v;
+    isin[j] = j ? (Real)(1.0L / v) : (Real)0;
+  }
+  const int P = sched_passes(NC, R);
+  tw.assign(sched_twtotal(NC, R) > 0 ? sched_twtotal(NC, R) : 1, typename Cx<Real>::V{0, 0});
+  for (int p = 1; p < P; ++p) {
+    const int RP = sched_radix(NC, R, p), NS = sched_ns(NC, R, p), off = sched_twoff(NC, R, p);
+    const int64_t den = (int64_t)NS * RP;
+    for (int r = 1; r < RP; ++r)
+      for (int k = 0; k < NS; ++k) {
+        const int64_t m = ((int64_t)k * r) % den;
+        const long double th = 2.0L * PI * (long double)m / (long double)den;
+        tw[off + (r - 1) * NS + k] = typename Cx<Real>::V{(Real)cosl(th), (Real)(-sinl(th))};
+      }
+  }
+}
+
+template <typename Real>
+fif_status upload_tables(fif_plan_s* p) {
+  std::vector<Real> sint, isin;
+  std::vector<typename Cx<Real>::V> tw;
+  const int R = radix_for(p->NC);
+  build_tables<Real>(p->n, p->NC, R, sint, isin, tw);
+  if (cudaMalloc(&p->d_sin, sizeof(Real) * sint.size()) != cudaSuccess) return FIF_ERR_OOM;
+  if (cudaMalloc(&p->d_isin, sizeof(Real) * isin.size()) != cudaSuccess) return FIF_ERR_OOM;
+  if (cudaMalloc(&p->d_tw, sizeof(tw[0]) * tw.size()) != cudaSuccess) return FIF_ERR_OOM;
+  if (cudaMemcpy(p->d_sin, sint.data(), sizeof(Real) * sint.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->d_isin, isin.data(), sizeof(Real) * isin.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->d_tw, tw.data(), sizeof(tw[0]) * tw.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return FIF_ERR_CUDA;
+  return FIF_OK;
+}
+
+size_t elem_size(fif_dtype d) { return d == FIF_F64 ? 8 : 4; }
+
+fif_status launch_status() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "fif: CUDA error: %s\n", cudaGetErrorString(e));
+    return FIF_ERR_CUDA;
+  }
+  return FIF_OK;
+}
+
+void free_plan(fif_plan_s* p) {
+  if (!p) return;
+  cudaFree(p->d_sin);
+  cudaFree(p->d_isin);
+  cudaFree(p->d_tw);
+  for (int i = 0; i < p->nstages; ++i) {
+    cudaFree(p->st[i].d_in);
+    cudaFree(p->st[i].d_out);
+    cudaFree(p->st[i].d_meta);
+    if (p->st[i].stream) cudaStreamDestroy(p->st[i].stream);
+    if (p->st[i].done) cudaEventDestroy(p->st[i].done);
+  }
+  delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fif_status_string(fif_status s) {
+  switch (s) {
+    case FIF_OK: return "FIF_OK";
+    case FIF_ERR_INVALID_ARG: return "FIF_ERR_INVALID_ARG";
+    case FIF_ERR_UNSUPPORTED_N: return "FIF_ERR_UNSUPPORTED_N";
+    case FIF_ERR_OOM: return "FIF_ERR_OOM";
+    case FIF_ERR_CUDA: return "FIF_ERR_CUDA";
+    case FIF_ERR_NCCL: return "FIF_ERR_NCCL";
+  }
+  return "FIF_ERR_UNKNOWN";
+}
+
+fif_status fif_plan_create(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window, double xi,
+                           double delta, int32_t max_inner, int32_t max_imfs) {
+  if (!out) return FIF_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n < 9 || batch < 0 || !(xi > 0.0) || !isfinite(xi) || !(delta > 0.0) || !isfinite(delta) || max_inner < 1 ||
+      max_imfs < 1 || (dtype != FIF_F64 && dtype != FIF_F32) ||
+      (window != FIF_WINDOW_TRI_SQ && window != FIF_WINDOW_TRI_SQ_WIDE))
+    return FIF_ERR_INVALID_ARG;
+  if (n % 2 != 0) return FIF_ERR_UNSUPPORTED_N;
+  const int64_t NC = n / 2;
+  if ((NC & (NC - 1)) != 0 || NC < 64 || NC > 4096) return FIF_ERR_UNSUPPORTED_N;
+  fif_plan_s* p = new fif_plan_s();
+  p->n = n; p->batch = batch; p->dtype = dtype; p->window = window; p->xi = xi; p->delta = delta;
+  p->max_inner = max_inner; p->max_imfs = max_imfs; p->NC = (int)NC;
+  if (cudaGetDevice(&p->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
+    free_plan(p);
+    return FIF_ERR_CUDA;
+  }
+  fif_status st = dtype == FIF_F64 ? upload_tables<double>(p) : upload_tables<float>(p);
+  if (st != FIF_OK) { free_plan(p); return st; }
+  cudaError_t ce = cudaSuccess;
+  dispatch(dtype, p->NC, [&](auto inst) {
+    using I = decltype(inst);
+    ce = I::prepare();
+    p->occ = I::occupancy();
+    p->block = I::K::T;
+    p->smem = I::K::smem_bytes;
+  });
+  if (ce != cudaSuccess || p->occ < 1) {
+    fprintf(stderr, "fif: kernel setup failed: %s (occ %d)\n", cudaGetErrorString(ce), p->occ);
+    free_plan(p);
+    return FIF_ERR_CUDA;
+  }
+  *out = p;
+  return FIF_OK;
+}
+
+fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int32_t* d_imf_count,
+                         int32_t* d_filter_len, int32_t* d_iters, void* stream) {
+  if (!p) return FIF_ERR_INVALID_ARG;
+  if (p->batch == 0) return FIF_OK;
+  if (!d_signals || !d_imfs || !d_imf_count || !d_filter_len || !d_iters) return FIF_ERR_INVALID_ARG;
+  if (((uintptr_t)d_signals | (uintptr_t)d_imfs) & 15) return FIF_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  dispatch(p->dtype, p->NC, [&](auto inst) {
+    using I = decltype(inst);
+    I::decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
+  });
+  return launch_status();
+}
+
+fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs, int32_t* h_imf_count,
+                              int32_t* h_filter_len, int32_t* h_iters, void* stream) {
+  if (!p) return FIF_ERR_INVALID_ARG;
+  if (p->batch == 0) return FIF_OK;
+  if (!h_signals || !h_imfs || !h_imf_count || !h_filter_len || !h_iters) return FIF_ERR_INVALID_ARG;
+  const size_t es = elem_size(p->dtype);
+  const size_t in_sig = (size_t)p->n * es, out_sig = in_sig * (size_t)(p->max_imfs + 1);
+  const size_t meta_sig = (size_t)(1 + 2 * p->max_imfs);
+  if (p->nstages == 0) {
+    // chunks of ~1/8 of the batch (>= one full wave of CTAs when possible), 3 stages in flight
+    int64_t chunk = (p->batch + 7) / 8;
+    const int64_t wave = (int64_t)p->num_sms * p->occ;
+    if (chunk < wave) chunk = wave < p->batch ? wave : p->batch;
+    p->chunk = chunk;
+    p->nstages = (int)((p->batch + chunk - 1) / chunk < FIF_MAX_STAGES ? (p->batch + chunk - 1) / chunk
+                                                                        : FIF_MAX_STAGES);
+    for (int i = 0; i < p->nstages; ++i) {
+      Staging& S = p->st[i];
+      if (cudaMalloc(&S.d_in, in_sig * chunk) != cudaSuccess || cudaMalloc(&S.d_out, out_sig * chunk) != cudaSuccess ||
+          cudaMalloc(&S.d_meta, sizeof(int32_t) * meta_sig * chunk) != cudaSuccess)
+        return FIF_ERR_OOM;
+      if (cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming) != cudaSuccess)
+        return FIF_ERR_CUDA;
+    }
+  }
+  cudaStream_t user = (cudaStream_t)stream;
+  cudaEvent_t start;
+  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  cudaEventRecord(start, user);
+  for (int i = 0; i < p->nstages; ++i) cudaStreamWaitEvent(p->st[i].stream, start, 0);
+  const int64_t nchunks = (p->batch + p->chunk - 1) / p->chunk;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    Staging& S = p->st[c % p->nstages];
+    const int64_t b0 = c * p->chunk, nb = (b0 + p->chunk <= p->batch) ? p->chunk : p->batch - b0;
+    int32_t* d_cnt = S.d_meta;
+    int32_t* d_len = S.d_meta + nb;
+    int32_t* d_it = d_len + nb * p->max_imfs;
+    cudaMemcpyAsync(S.d_in, (const char*)h_signals + b0 * in_sig, nb * in_sig, cudaMemcpyHostToDevice, S.stream);
+    dispatch(p->dtype, p->NC, [&](auto inst) {
+      using I = decltype(inst);
+      I::decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
+    });
+    cudaMemcpyAsync((char*)h_imfs + b0 * out_sig, S.d_out, nb * out_sig, cudaMemcpyDeviceToHost, S.stream);
+    cudaMemcpyAsync(h_imf_count + b0, d_cnt, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, S.stream);
+    cudaMemcpyAsync(h_filter_len + b0 * p->max_imfs, d_len, sizeof(int32_t) * nb * p->max_imfs,
+                    cudaMemcpyDeviceToHost, S.stream);
+    cudaMemcpyAsync(h_iters + b0 * p->max_imfs, d_it, sizeof(int32_t) * nb * p->max_imfs, cudaMemcpyDeviceToHost,
+                    S.stream);
+  }
+  for (int i = 0; i < p->nstages; ++i) {
+    cudaEventRecord(p->st[i].done, p->st[i].stream);
+    cudaStreamWaitEvent(user, p->st[i].done, 0);
+  }
+  cudaEventDestroy(start);
+  fif_status st = launch_status();
+  if (st != FIF_OK) return st;
+  if (cudaStreamSynchronize(user) != cudaSuccess) return FIF_ERR_CUDA;
+  return FIF_OK;
+}
+
+fif_status fif_destroy(fif_plan_t p) {
+  if (!p) return FIF_OK;
+  cudaDeviceSynchronize();
+  free_plan(p);
+  return FIF_OK;
+}
+
+int32_t fif_plan_kernels_per_call(fif_plan_t p) { return (p && p->batch > 0) ? 1 : 0; }
+
+const char* fif_plan_regime(fif_plan_t p) { return p ? "resident" : "none"; }
+
+fif_status fif_plan_launch_config(fif_plan_t p, int32_t* grid, int32_t* block, int32_t* smem_bytes) {
+  if (!p) return FIF_ERR_INVALID_ARG;
+  const int64_t cap = (int64_t)p->num_sms * p->occ;
+  if (grid) *grid = (int32_t)(p->batch < cap ? p->batch : cap);
+  if (block) *block = p->block;
+  if (smem_bytes) *smem_bytes = (int32_t)p->smem;
+  return FIF_OK;
+}
+
+// ---------------------------------------------------------------- test hooks
+#define HOOK_SYNC(s)                                       \
+  do {                                                     \
+    fif_status st_ = launch_status();                      \
+    if (st_ != FIF_OK) return st_;                         \
+    if (cudaStreamSynchronize(s) != cudaSuccess) return FIF_ERR_CUDA; \
+    return FIF_OK;                                         \
+  } while (0)
+
+fif_status fif_test_rfft(fif_plan_t p, int64_t batch, const void* d_in, void* d_out, void* stream) {
+  if (!p || batch < 0 || (batch && (!d_in || !d_out))) return FIF_ERR_INVALID_ARG;
+  if (!batch) return FIF_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_rfft(p, d_in, d_out, batch, s); });
+  HOOK_SYNC(s);
+}
+
+fif_status fif_test_irfft(fif_plan_t p, int64_t batch, const void* d_in, void* d_out, void* stream) {
+  if (!p || batch < 0 || (batch && (!d_in || !d_out))) return FIF_ERR_INVALID_ARG;
+  if (!batch) return FIF_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_irfft(p, d_in, d_out, batch, s); });
+  HOOK_SYNC(s);
+}
+
+fif_status fif_test_extrema(fif_plan_t p, int64_t batch, const void* d_in, int32_t* d_k, void* stream) {
+  if (!p || batch < 0 || (batch && (!d_in || !d_k))) return FIF_ERR_INVALID_ARG;
+  if (!batch) return FIF_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_extrema(p, d_in, d_k, batch, s); });
+  HOOK_SYNC(s);
+}
+
+fif_status fif_test_window_spectrum(fif_plan_t p, int32_t L, void* d_out, void* stream) {
+  if (!p || L < 1 || !d_out) return FIF_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_window(p, L, d_out, s); });
+  HOOK_SYNC(s);
+}
+
+fif_status fif_test_inner(fif_plan_t p, int64_t batch, int32_t L, const void* d_in, void* d_imf, int32_t* d_N,
+                          void* stream) {
+  if (!p || batch < 0 || L < 1 || (batch && (!d_in || !d_imf || !d_N))) return FIF_ERR_INVALID_ARG;
+  if (!batch) return FIF_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_inner(p, L, d_in, d_imf, d_N, batch, s); });
+  HOOK_SYNC(s);
+}
+
+}  // extern "C"
