@@ -51,9 +51,9 @@ typedef enum {
 } fif_status;
 
 /* Create a plan for `batch` independent signals of length n.
- *   n          : samples per signal.  This build supports even n with n/2 a power
- *                of two, 128 <= n <= 8192 (f64) / 16384 (f32) -- the on-chip
- *                resident regime; other n -> FIF_ERR_UNSUPPORTED_N.
+ *   n          : samples per signal.  This build supports powers of two
+ *                512 <= n <= 8192 (f64 and f32) -- the on-chip resident regime;
+ *                other n -> FIF_ERR_UNSUPPORTED_N.
  *   batch      : number of signals, >= 0 (0 is a valid no-op plan).
  *   dtype      : element type of signals and IMFs.  f32 computes the FFTs in fp32 and
  *                accumulates the stopping sums and takes the floor in fp64 (reading A14).

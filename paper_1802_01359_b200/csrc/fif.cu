@@ -62,29 +62,29 @@ struct Entry {
   int threads;
 };
 
-template <typename Real, int NC, int R>
+template <typename Real, int NC>
 struct Inst {
-  using K = Resident<Real, NC, R>;
+  using K = Resident<Real, NC>;
   using V = typename Cx<Real>::V;
   static cudaError_t prepare() {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_test_rfft_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_test_rfft_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_test_irfft_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_test_irfft_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_test_extrema_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_test_extrema_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_test_window_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_test_window_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     return cudaSuccess;
   }
   static int occupancy() {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC, R>, K::T, K::smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC>, K::T, K::smem_bytes);
     return occ;
   }
   static void decompose(const fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
@@ -92,34 +92,34 @@ struct Inst {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
     const int64_t cap = (int64_t)p->num_sms * p->occ;
     const int grid = (int)(batch < cap ? batch : cap);
-    fif_resident_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+    fif_resident_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
         (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
         (const V*)p->d_tw, prm);
   }
   static void test_rfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
     const int grid = (int)(batch < 4096 ? batch : 4096);
-    fif_test_rfft_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+    fif_test_rfft_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
         (const Real*)in, (Real*)out, batch, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw);
   }
   static void test_irfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
     const int grid = (int)(batch < 4096 ? batch : 4096);
-    fif_test_irfft_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+    fif_test_irfft_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
         (const Real*)in, (Real*)out, batch, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw);
   }
   static void test_extrema(const fif_plan_s* p, const void* in, int32_t* k, int64_t batch, cudaStream_t s) {
     (void)p;
     const int grid = (int)(batch < 4096 ? batch : 4096);
-    fif_test_extrema_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>((const Real*)in, k, batch);
+    fif_test_extrema_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>((const Real*)in, k, batch);
   }
   static void test_window(const fif_plan_s* p, int L, void* out, cudaStream_t s) {
-    fif_test_window_kernel<Real, NC, R><<<1, K::T, K::smem_bytes, s>>>((Real*)out, L, (const Real*)p->d_sin,
+    fif_test_window_kernel<Real, NC><<<1, K::T, K::smem_bytes, s>>>((Real*)out, L, (const Real*)p->d_sin,
                                                                         (const Real*)p->d_isin);
   }
   static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
                          cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
     const int grid = (int)(batch < 4096 ? batch : 4096);
-    fif_test_inner_kernel<Real, NC, R><<<grid, K::T, K::smem_bytes, s>>>(
+    fif_test_inner_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
         (const Real*)in, (Real*)out, N, batch, L, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw,
         prm);
   }
@@ -129,13 +129,11 @@ struct Inst {
 template <typename Real, typename F>
 bool dispatch_nc(int NC, F&& f) {
   switch (NC) {
-    case 64: f(Inst<Real, 64, 2>{}); return true;
-    case 128: f(Inst<Real, 128, 4>{}); return true;
-    case 256: f(Inst<Real, 256, 8>{}); return true;
-    case 512: f(Inst<Real, 512, 8>{}); return true;
-    case 1024: f(Inst<Real, 1024, 8>{}); return true;
-    case 2048: f(Inst<Real, 2048, 8>{}); return true;
-    case 4096: f(Inst<Real, 4096, 8>{}); return true;
+    case 256: f(Inst<Real, 256>{}); return true;
+    case 512: f(Inst<Real, 512>{}); return true;
+    case 1024: f(Inst<Real, 1024>{}); return true;
+    case 2048: f(Inst<Real, 2048>{}); return true;
+    case 4096: f(Inst<Real, 4096>{}); return true;
     default: return false;
   }
 }
@@ -145,11 +143,9 @@ bool dispatch(fif_dtype dt, int NC, F&& f) {
   return dispatch_nc<float>(NC, f);
 }
 
-int radix_for(int NC) { return NC == 64 ? 2 : (NC == 128 ? 4 : 8); }
-
 // ---------------------------------------------------------------- tables (host, long double)
 template <typename Real>
-void build_tables(int64_t n, int NC, int R, std::vector<Real>& sint, std::vector<Real>& isin,
+void build_tables(int64_t n, int NC, std::vector<Real>& sint, std::vector<Real>& isin,
                   std::vector<typename Cx<Real>::V>& tw) {
   const long double PI = 3.141592653589793238462643383279502884L;
   sint.assign(NC + 1, (Real)0);
@@ -162,10 +158,10 @@ void build_tables(int64_t n, int NC, int R, std::vector<Real>& sint, std::vector
     sint[j] = (Real)v;
     isin[j] = j ? (Real)(1.0L / v) : (Real)0;
   }
-  const int P = sched_passes(NC, R);
-  tw.assign(sched_twtotal(NC, R) > 0 ? sched_twtotal(NC, R) : 1, typename Cx<Real>::V{0, 0});
+  const int P = sched_passes(NC);
+  tw.assign(sched_twtotal(NC) > 0 ? sched_twtotal(NC) : 1, typename Cx<Real>::V{0, 0});
   for (int p = 1; p < P; ++p) {
-    const int RP = sched_radix(NC, R, p), NS = sched_ns(NC, R, p), off = sched_twoff(NC, R, p);
+    const int RP = sched_radix(NC, p), NS = sched_ns(NC, p), off = sched_twoff(NC, p);
     const int64_t den = (int64_t)NS * RP;
     for (int r = 1; r < RP; ++r)
       for (int k = 0; k < NS; ++k) {
@@ -180,8 +176,7 @@ template <typename Real>
 fif_status upload_tables(fif_plan_s* p) {
   std::vector<Real> sint, isin;
   std::vector<typename Cx<Real>::V> tw;
-  const int R = radix_for(p->NC);
-  build_tables<Real>(p->n, p->NC, R, sint, isin, tw);
+  build_tables<Real>(p->n, p->NC, sint, isin, tw);
   if (cudaMalloc(&p->d_sin, sizeof(Real) * sint.size()) != cudaSuccess) return FIF_ERR_OOM;
   if (cudaMalloc(&p->d_isin, sizeof(Real) * isin.size()) != cudaSuccess) return FIF_ERR_OOM;
   if (cudaMalloc(&p->d_tw, sizeof(tw[0]) * tw.size()) != cudaSuccess) return FIF_ERR_OOM;
@@ -244,7 +239,7 @@ fif_status fif_plan_create(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype 
     return FIF_ERR_INVALID_ARG;
   if (n % 2 != 0) return FIF_ERR_UNSUPPORTED_N;
   const int64_t NC = n / 2;
-  if ((NC & (NC - 1)) != 0 || NC < 64 || NC > 4096) return FIF_ERR_UNSUPPORTED_N;
+  if ((NC & (NC - 1)) != 0 || NC < 256 || NC > 4096) return FIF_ERR_UNSUPPORTED_N;
   fif_plan_s* p = new fif_plan_s();
   p->n = n; p->batch = batch; p->dtype = dtype; p->window = window; p->xi = xi; p->delta = delta;
   p->max_inner = max_inner; p->max_imfs = max_imfs; p->NC = (int)NC;

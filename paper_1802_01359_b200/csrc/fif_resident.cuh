@@ -2,7 +2,7 @@
 //
 // One CTA decomposes one signal at a time (persistent over the batch): the
 // remainder r (time domain) and its spectrum r_hat stay in REGISTERS for all
-// IMFs; shared memory holds only the FFT exchange buffers and the sin table.
+// IMFs; shared memory holds only the FFT exchange buffers and the sin tables.
 // HBM traffic per signal is the compulsory one: read s once, write every IMF
 // and the trend once.
 //
@@ -20,10 +20,16 @@
 //   a7  outer loop control, trend, zero fill
 //
 // FFT: n real points = NC = n/2 complex points (z_m = x_2m + i x_2m+1), Stockham
-// auto-sort passes (radix 8, plus one radix-2/4 first pass), each thread owning
-// R = 8 complex values at positions j + T*q.  The first forward pass reads from
-// registers and the last pass of either direction ends in registers, so the
-// time-domain data never round-trips through shared memory at the ends.
+// auto-sort passes: one radix-4 pass then radix 8 (one radix-2/4 pass first
+// when NC/4 is not a power of 8).  T = NC/8 threads, each owning 8 complex
+// values.  Register layouts:
+//   time domain   : pairs (x_2m, x_2m+1) at m = j + T q, q = 0..7 (coalesced IMF stores)
+//   spectrum      : "group layout" -- thread j owns the two radix-4 groups
+//                   g1 = j and g2 = NC/4 - j (g2 = NC/8 for j = 0), bins g + r NC/4,
+//                   r = 0..3.  Each group set is closed under k <-> NC - k, so the
+//                   real-IFFT pre-processing (which pairs X_k with X_{NC-k}) and the
+//                   first inverse radix-4 pass run in registers with no shared-
+//                   memory round trip.  Thread 0 also owns X_{NC} (Nyquist).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -49,31 +55,32 @@ struct Params {
 };
 
 // ------------------------------------------------------------------ radix schedule (compile time)
-__host__ __device__ constexpr int sched_r0(int NC, int R) {
-  int m = NC;
-  while (m % R == 0 && m > 1) m /= R;
-  return m;  // leftover factor (1, 2 or 4 for power-of-two NC and R = 8)
+// pass 0: radix 4; then the radix-8 factorisation of NC/4 with the leftover (2 or 4) first.
+constexpr int kR = 8;  // complex values per thread
+__host__ __device__ constexpr int sched_left(int m) {
+  while (m % 8 == 0 && m > 1) m /= 8;
+  return m;
 }
-__host__ __device__ constexpr int sched_passes(int NC, int R) {
-  int m = NC, p = 0;
-  while (m % R == 0 && m > 1) { m /= R; ++p; }
-  return p + (m > 1 ? 1 : 0);
+__host__ __device__ constexpr int sched_passes(int NC) {
+  int m = NC / 4, p = 0;
+  while (m % 8 == 0 && m > 1) { m /= 8; ++p; }
+  return 1 + p + (m > 1 ? 1 : 0);
 }
-__host__ __device__ constexpr int sched_radix(int NC, int R, int p) {
-  return (sched_r0(NC, R) > 1 && p == 0) ? sched_r0(NC, R) : R;
+__host__ __device__ constexpr int sched_radix(int NC, int p) {
+  return p == 0 ? 4 : ((sched_left(NC / 4) > 1 && p == 1) ? sched_left(NC / 4) : 8);
 }
-__host__ __device__ constexpr int sched_ns(int NC, int R, int p) {
+__host__ __device__ constexpr int sched_ns(int NC, int p) {
   int ns = 1;
-  for (int i = 0; i < p; ++i) ns *= sched_radix(NC, R, i);
+  for (int i = 0; i < p; ++i) ns *= sched_radix(NC, i);
   return ns;
 }
 // offset (in complex elements) of pass p's twiddle block tw[(r-1)*NS + k], r = 1..RP-1, k < NS
-__host__ __device__ constexpr int sched_twoff(int NC, int R, int p) {
+__host__ __device__ constexpr int sched_twoff(int NC, int p) {
   int off = 0;
-  for (int i = 1; i < p; ++i) off += (sched_radix(NC, R, i) - 1) * sched_ns(NC, R, i);
+  for (int i = 1; i < p; ++i) off += (sched_radix(NC, i) - 1) * sched_ns(NC, i);
   return off;
 }
-__host__ __device__ constexpr int sched_twtotal(int NC, int R) { return sched_twoff(NC, R, sched_passes(NC, R)); }
+__host__ __device__ constexpr int sched_twtotal(int NC) { return sched_twoff(NC, sched_passes(NC)); }
 
 // ------------------------------------------------------------------ complex helpers
 template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return V{a.x + b.x, a.y + b.y}; }
@@ -82,6 +89,7 @@ template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
   return V{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
 }
 template <typename V> __device__ __forceinline__ V cconj(V a) { return V{a.x, -a.y}; }
+template <typename V, typename S> __device__ __forceinline__ V cscale(V a, S s) { return V{a.x * s, a.y * s}; }
 // multiply by DIR * i
 template <int DIR, typename V> __device__ __forceinline__ V mul_i(V a) {
   return DIR > 0 ? V{-a.y, a.x} : V{a.y, -a.x};
@@ -101,7 +109,7 @@ template <int DIR, typename V> __device__ __forceinline__ void dft8(V* v) {
   // t_j *= w^j, w = e^{DIR i pi/4}
   t1 = V{c * (t1.x - (S)DIR * t1.y), c * ((S)DIR * t1.x + t1.y)};
   t2 = mul_i<DIR>(t2);
-  t3 = V{c * (-t3.x - (S)DIR * t3.y), c * ((S)DIR * t3.x - t3.y)};
+  t3 = V{-c * (t3.x + (S)DIR * t3.y), c * ((S)DIR * t3.x - t3.y)};
   dft4<DIR>(u0, u1, u2, u3);
   dft4<DIR>(t0, t1, t2, t3);
   v[0] = u0; v[1] = t0; v[2] = u1; v[3] = t1; v[4] = u2; v[5] = t2; v[6] = u3; v[7] = t3;
@@ -120,24 +128,23 @@ template <int DIR, typename V> struct Dft<8, DIR, V> {
 
 // shared-memory padding: one pad element per 128 bytes of data (bank-conflict-free
 // strided Stockham stores)
-template <typename V> __device__ __forceinline__ int pad(int i) {
+template <typename V> __host__ __device__ constexpr int pad(int i) {
   return sizeof(V) == 16 ? i + (i >> 3) : i + (i >> 4);
 }
-template <typename V> __host__ __device__ constexpr int padded_len(int n) {
-  return sizeof(V) == 16 ? n + (n >> 3) + 1 : n + (n >> 4) + 1;
-}
+template <typename V> __host__ __device__ constexpr int padded_len(int n) { return pad<V>(n) + 1; }
 
 // ------------------------------------------------------------------ one Stockham pass
 // Virtual threads vt in [0, NC/RP): inputs x[vt + r NC/RP], twiddle e^{DIR 2 pi i k r/(NS RP)}
 // with k = vt mod NS, radix-RP DFT, outputs y[(vt/NS) NS RP + k + r NS].
-// Real thread j runs virtual threads vt = j + T u, u < R/RP; its register q = u + r (R/RP)
+// Real thread j runs virtual threads vt = j + T u, u < 8/RP; its register q = u + r (8/RP)
 // holds position j + T q, which is exactly vt + r NC/RP.
-template <typename V, int NC, int R, int RP, int NS, int DIR, bool FROM_REGS, bool TO_REGS>
-__device__ __forceinline__ void stockham_pass(V (&v)[R], const V* src, V* dst, const V* __restrict__ tw, int j) {
-  constexpr int T = NC / R, VP = R / RP;
+template <typename V, int NC, int RP, int NS, int DIR, bool FROM_REGS, bool TO_REGS>
+__device__ __forceinline__ void stockham_pass(V (&v)[kR], const V* src, V* dst, const V* __restrict__ tw, int j) {
+  constexpr int T = NC / kR, VP = kR / RP;
   if (!FROM_REGS) {
+    const V* s0 = src + pad<V>(j);
 #pragma unroll
-    for (int q = 0; q < R; ++q) v[q] = src[pad<V>(j + T * q)];
+    for (int q = 0; q < kR; ++q) v[q] = s0[pad<V>(T * q)];  // T multiple of 8: pad is additive
   }
 #pragma unroll
   for (int u = 0; u < VP; ++u) {
@@ -168,15 +175,15 @@ __device__ __forceinline__ void stockham_pass(V (&v)[R], const V* src, V* dst, c
 
 // Runs passes p..P-1.  `rd` is read by pass p (unless FROM_REGS), `wr` written.  Returns the
 // buffer written last (so the caller's next write phase goes to the other one).
-template <typename V, int NC, int R, int DIR, int p, bool FROM_REGS>
-__device__ __forceinline__ V* fft_passes(V (&v)[R], V* rd, V* wr, const V* __restrict__ tw, int j, V* last) {
-  constexpr int P = sched_passes(NC, R);
-  constexpr int RP = sched_radix(NC, R, p), NS = sched_ns(NC, R, p);
+template <typename V, int NC, int DIR, int p, bool FROM_REGS>
+__device__ __forceinline__ V* fft_passes(V (&v)[kR], V* rd, V* wr, const V* __restrict__ tw, int j, V* last) {
+  constexpr int P = sched_passes(NC);
+  constexpr int RP = sched_radix(NC, p), NS = sched_ns(NC, p);
   constexpr bool LAST = (p == P - 1);
-  stockham_pass<V, NC, R, RP, NS, DIR, FROM_REGS, LAST>(v, rd, wr, tw + sched_twoff(NC, R, p), j);
+  stockham_pass<V, NC, RP, NS, DIR, FROM_REGS, LAST>(v, rd, wr, tw + sched_twoff(NC, p), j);
   if constexpr (!LAST) {
     __syncthreads();
-    return fft_passes<V, NC, R, DIR, p + 1, false>(v, wr, rd, tw, j, wr);
+    return fft_passes<V, NC, DIR, p + 1, false>(v, wr, rd, tw, j, wr);
   } else {
     return last;
   }
@@ -198,13 +205,15 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red /*[
 }
 
 // ------------------------------------------------------------------ the kernel body
-template <typename Real, int NC, int R>
+template <typename Real, int NC>
 struct Resident {
   using V = typename Cx<Real>::V;
   static constexpr int n = 2 * NC;
-  static constexpr int T = NC / R;
+  static constexpr int R = kR;
+  static constexpr int T = NC / kR;
+  static constexpr int G = NC / 4;  // radix-4 group stride
   static constexpr int NW = T / 32;
-  static constexpr int P = sched_passes(NC, R);
+  static constexpr int P = sched_passes(NC);
   static constexpr int PADN = padded_len<V>(NC);
   static_assert(T >= 32 && T % 32 == 0, "need at least one full warp");
   static_assert((NC & (NC - 1)) == 0, "power-of-two NC");
@@ -214,14 +223,18 @@ struct Resident {
   static constexpr size_t off_bufB = off_bufA + sizeof(V) * PADN;
   static constexpr size_t off_sin = off_bufB + sizeof(V) * PADN;
   static constexpr size_t off_isin = off_sin + sizeof(Real) * ((NC + 2) & ~1);
-  static constexpr size_t off_red = off_isin + sizeof(Real) * ((NC + 2) & ~1);   // 2 slots x 2*NW doubles
-  static constexpr size_t off_nbr = off_red + sizeof(double) * 4 * NW;          // NW*R V
-  static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;               // NW + 8 ints
+  static constexpr size_t off_red = off_isin + sizeof(Real) * ((NC + 2) & ~1);  // 2 slots x 2*NW doubles
+  static constexpr size_t off_nbr = off_red + sizeof(double) * 4 * NW;         // NW*R V
+  static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // NW + 8 ints
   static constexpr size_t smem_bytes = off_int + sizeof(int) * (NW + 8);
 
   struct Smem {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
   };
+
+  // group layout: bin index of spectrum register q for thread j
+  __device__ static int g2_of(int j) { return j == 0 ? NC / 8 : G - j; }
+  __device__ static int bin_of(int j, int q) { return (q < 4 ? j : g2_of(j)) + (q & 3) * G; }
 
   // -------------------------------------------------------------- a2 extrema count
   // Fast path: with no zero difference, k = #{p : sign(D_p) != sign(D_p+1)} -- a plain
@@ -251,14 +264,15 @@ struct Resident {
     bool zero = false;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const int m = j + T * q;
       const Real d0 = rt[q].y - rt[q].x;  // D_{2m}
-      zero |= (d0 == (Real)0);
-      if (m < NC - 1) {
-        const Real d1 = nb[q].x - rt[q].y;  // D_{2m+1}
-        const Real d2 = nb[q].y - nb[q].x;  // D_{2m+2} (checked for zero by pair m+1)
-        zero |= (d1 == (Real)0);
-        cnt += ((d0 > (Real)0) != (d1 > (Real)0)) + ((d1 > (Real)0) != (d2 > (Real)0));
+      const Real d1 = nb[q].x - rt[q].y;  // D_{2m+1}
+      const Real d2 = nb[q].y - nb[q].x;  // D_{2m+2} (checked for zero by pair m+1)
+      const bool s0 = d0 > (Real)0, s1 = d1 > (Real)0, s2 = d2 > (Real)0;
+      if (q < R - 1 || j < T - 1) {  // pair m = NC-1 has no successor
+        zero |= (d0 == (Real)0) | (d1 == (Real)0);
+        cnt += (s0 != s1) + (s1 != s2);
+      } else {
+        zero |= (d0 == (Real)0);
       }
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -295,7 +309,7 @@ struct Resident {
         if (lastsg != 0 && sg != lastsg) ++c;
         lastsg = sg;
       }
-      // ordered fold over lanes 0..31 (lane 0 accumulates)
+      // ordered fold over lanes 0..31
       int F = __shfl_sync(0xffffffffu, first, 0), Ls = __shfl_sync(0xffffffffu, lastsg, 0),
           C = __shfl_sync(0xffffffffu, c, 0);
       for (int l = 1; l < 32; ++l) {
@@ -324,10 +338,10 @@ struct Resident {
   }
 
   // -------------------------------------------------------------- a4 window spectrum
-  // w_hat_k = [sin(pi r/n) / (L sin(pi k/n))]^4, r = min(Lk mod n, n - Lk mod n), k in [0, n/2].
+  // w_hat_k = [sin(pi r/n) / (L sin(pi k/n))]^4, r = min(Lk mod n, n - Lk mod n), 1 <= k <= n/2.
+  // (Lk mod n computed in 32-bit: exact for power-of-two n even on wrap-around.)  k = 0 -> caller.
   __device__ static Real what(const Smem& sm, int L, Real invL, int k) {
-    if (k == 0) return (Real)1;
-    const int m = (int)(((long long)L * k) & (n - 1));
+    const int m = (int)(((unsigned)L * (unsigned)k) & (unsigned)(n - 1));
     const int r = min(m, n - m);
     const Real s = sm.sint[r] * sm.isin[k] * invL;
     const Real s2 = s * s;
@@ -335,102 +349,120 @@ struct Resident {
   }
 
   // -------------------------------------------------------------- a5 stopping search (one probe)
-  // P(N) = sum c_k a_k^{2(N-1)} |X_k|^2, Q(N) = sum c_k w_k^2 a_k^{2(N-1)} |X_k|^2 (fp64 accumulation)
-  // Also returns d_k = a_k^N for the thread's bins (used when N = the probe).  The thread's R+1 bins
-  // are processed together (powers by squaring over the bits of the uniform exponent N-1) for ILP.
-  static constexpr int NB = R + 1;  // R/2 bins k, R/2 mirrors NC-k, + the middle bin (thread 0 only)
-  __device__ static void probe(const V (&Xa)[R / 2], const V (&Xb)[R / 2], const V& Xm, const Smem& sm, int L,
-                               Real invL, int N, double& P, double& Q, Real (&dA)[R / 2], Real (&dB)[R / 2],
-                               Real& dM, double* red, int j) {
-    double a[NB], e[NB], wv[NB], pk[NB];
+  // P(N) = sum c_k a_k^{2(N-1)} |X_k|^2, Q(N) = sum c_k w_k^2 a_k^{2(N-1)} |X_k|^2 (fp64 accumulation),
+  // c_k = 1 for k in {0, NC}, 2 otherwise.  a_k = 1 - w_k (w_k in [0, 1]; a value ~1e-16 below 0
+  // from rounding only ever enters as a tiny power).  Also returns d_k = a_k^N.
+  __device__ static void probe(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N, double& P,
+                               double& Q, Real (&d)[R], Real& dn, double* red, int j) {
+    double P2 = 0.0, Q2 = 0.0;  // sums with c = 1, doubled at the end
+    const int ex = N - 1;
+    const int nbits = ex ? 32 - __clz(ex) : 0;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      int kk;
-      V X;
-      if (i < R / 2) { kk = j + T * i; X = Xa[i]; }
-      else if (i < R) { kk = NC - (j + T * (i - R / 2)); X = Xb[i - R / 2]; }
-      else { kk = NC / 2; X = Xm; }
-      const Real w = what(sm, L, invL, kk);
-      const Real av = fminf_t(fmaxf_t((Real)1 - w, (Real)0), (Real)1);
-      a[i] = (double)av;
-      wv[i] = (double)w;
-      const double c = (kk == 0 || kk == NC) ? 1.0 : 2.0;
-      pk[i] = (i < R || j == 0) ? c * ((double)X.x * (double)X.x + (double)X.y * (double)X.y) : 0.0;
-      e[i] = 1.0;
-    }
-    // e = a^(N-1) by squaring (exponent uniform across the block: no divergence)
-    {
-      double b[NB];
+    for (int g = 0; g < R; g += 4) {
+      double a[4], e[4], b[4], w[4];
 #pragma unroll
-      for (int i = 0; i < NB; ++i) b[i] = a[i];
-      int ex = N - 1;
-      while (ex) {
-        if (ex & 1) {
+      for (int i = 0; i < 4; ++i) {
+        const int kk = bin_of(j, g + i);
+        Real wv = what(sm, L, invL, kk);
+        if (g + i == 0 && j == 0) wv = (Real)1;  // bin 0: w_hat_0 = 1 (row sums to 1)
+        w[i] = (double)wv;
+        a[i] = 1.0 - w[i];
+        b[i] = a[i];
+        e[i] = 1.0;
+      }
+      for (int bit = 0; bit < nbits; ++bit) {  // e = a^(N-1), uniform exponent
+        if ((ex >> bit) & 1) {
 #pragma unroll
-          for (int i = 0; i < NB; ++i) e[i] *= b[i];
+          for (int i = 0; i < 4; ++i) e[i] *= b[i];
         }
-        ex >>= 1;
-        if (ex) {
 #pragma unroll
-          for (int i = 0; i < NB; ++i) b[i] *= b[i];
-        }
+        for (int i = 0; i < 4; ++i) b[i] *= b[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const V x = X[g + i];
+        double pk = (double)x.x * (double)x.x + (double)x.y * (double)x.y;
+        if (g + i == 0 && j == 0) pk *= 0.5;  // bin 0 has weight 1
+        const double px = pk * (e[i] * e[i]);
+        P2 += px;
+        Q2 += px * (w[i] * w[i]);
+        d[g + i] = (Real)(e[i] * a[i]);
       }
     }
-    P = 0.0; Q = 0.0;
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      const double x = e[i] * e[i];
-      const double px = pk[i] * x;
-      P += px;
-      Q += px * (wv[i] * wv[i]);
-      const Real d = (Real)(e[i] * a[i]);
-      if (i < R / 2) dA[i]= d; else if (i < R) dB[i - R / 2] = d; else dM = d;
+    if (j == 0) {  // Nyquist bin k = NC, weight 1
+      const double wv = (double)what(sm, L, invL, NC);
+      const double a = 1.0 - wv;
+      double e = 1.0, b = a;
+      for (int bit = 0; bit < nbits; ++bit) {
+        if ((ex >> bit) & 1) e *= b;
+        b *= b;
+      }
+      const double pk = 0.5 * ((double)Xn.x * (double)Xn.x + (double)Xn.y * (double)Xn.y);
+      const double px = pk * (e * e);
+      P2 += px;
+      Q2 += px * (wv * wv);
+      dn = (Real)(e * a);
     }
+    P = 2.0 * P2;
+    Q = 2.0 * Q2;
     block_sum2<NW>(P, Q, red, j);
   }
 
-  __device__ static Real fminf_t(Real a, Real b) { return a < b ? a : b; }
-  __device__ static Real fmaxf_t(Real a, Real b) { return a > b ? a : b; }
+  // d_k = a_k^N only (no reduction): after a bisection that did not end on its last probe
+  __device__ static void damping_only(const Smem& sm, int L, Real invL, int N, Real (&d)[R], Real& dn, int j) {
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      Real wv = what(sm, L, invL, bin_of(j, q));
+      if (q == 0 && j == 0) wv = (Real)1;
+      const double a = 1.0 - (double)wv;
+      double e = 1.0, b = a;
+      for (int x = N; x; x >>= 1) {
+        if (x & 1) e *= b;
+        b *= b;
+      }
+      d[q] = (Real)e;
+    }
+    if (j == 0) {
+      const double a = 1.0 - (double)what(sm, L, invL, NC);
+      double e = 1.0, b = a;
+      for (int x = N; x; x >>= 1) {
+        if (x & 1) e *= b;
+        b *= b;
+      }
+      dn = (Real)e;
+    }
+  }
 
-  __device__ static int search(const V (&Xa)[R / 2], const V (&Xb)[R / 2], const V& Xm, const Smem& sm, int L,
-                               const Params& p, Real (&dA)[R / 2], Real (&dB)[R / 2], Real& dM, int& slot, int j) {
+  __device__ static int search(const V (&X)[R], const V& Xn, const Smem& sm, int L, const Params& p, Real (&d)[R],
+                               Real& dn, int& slot, int j) {
     const Real invL = (Real)1 / (Real)L;
     double Pv, Qv;
     const int cap = p.max_inner;
-    probe(Xa, Xb, Xm, sm, L, invL, cap, Pv, Qv, dA, dB, dM, sm.red + slot * 2 * NW, j);
+    probe(X, Xn, sm, L, invL, cap, Pv, Qv, d, dn, sm.red + slot * 2 * NW, j);
     slot ^= 1;
     if (!(Qv <= p.delta2 * Pv)) return cap;
     int lo = 0, hi = cap, lastN = cap;  // invariant: pass(hi), !pass(lo) (lo = 0 is virtual)
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      probe(Xa, Xb, Xm, sm, L, invL, mid, Pv, Qv, dA, dB, dM, sm.red + slot * 2 * NW, j);
+      probe(X, Xn, sm, L, invL, mid, Pv, Qv, d, dn, sm.red + slot * 2 * NW, j);
       slot ^= 1;
       lastN = mid;
       if (Qv <= p.delta2 * Pv) hi = mid; else lo = mid;
     }
-    if (lastN != hi) {  // recompute d_k = a_k^hi (dA/dB hold the last probe's N)
-      double Pd, Qd;
-      probe(Xa, Xb, Xm, sm, L, invL, hi, Pd, Qd, dA, dB, dM, sm.red + slot * 2 * NW, j);
-      slot ^= 1;
-    }
+    if (lastN != hi) damping_only(sm, L, invL, hi, d, dn, j);
     return hi;
   }
 
   // -------------------------------------------------------------- real-FFT pre/post processing
-  // w_k = e^{+2 pi i k/n} = (sin(pi (n/2 - 2k)/n), sin(pi 2k/n)), k <= n/4
+  // w(k) = e^{+2 pi i k/n} = (sin(pi (n/2 - 2k)/n), sin(pi 2k/n)), 0 <= k <= n/4
   __device__ static V wk(const Smem& sm, int k) { return V{sm.sint[NC - 2 * k], sm.sint[2 * k]}; }
-
-  // forward: from Z (NC-point FFT of z) to X_k, X_{NC-k}
-  __device__ static void post_forward(V P, V Q, V w, V& Xk, V& Xmk) {
-    const Real h = (Real)0.5;
-    const V E = V{h * (P.x + Q.x), h * (P.y - Q.y)};       // (P + Q*)/2
-    const V D = V{h * (P.x - Q.x), h * (P.y + Q.y)};       // (P - Q*)/2
-    const V O = V{D.y, -D.x};                              // D / i
-    const V wO = cmul(cconj(w), O);                         // e^{-2 pi i k/n} O
-    Xk = cadd(E, wO);
-    Xmk = cconj(csub(E, wO));
+  // e^{-2 pi i k/n} for 0 <= k < NC
+  __device__ static V wfwd(const Smem& sm, int k) {
+    if (2 * k <= NC) return V{sm.sint[NC - 2 * k], -sm.sint[2 * k]};
+    const int kk = NC - k;
+    return V{-sm.sint[NC - 2 * kk], -sm.sint[2 * kk]};
   }
-  // inverse: from A = D_k, B = D_{NC-k} (already scaled by 1/n) to Z_k, Z_{NC-k}
+  // inverse: from A = D_k, B = D_{NC-k} (pre-scaled by 1/n), w = e^{2 pi i k/n} -> Z_k, Z_{NC-k}
   __device__ static void pre_inverse(V A, V B, V w, V& Zk, V& Zmk) {
     const V S = V{A.x + B.x, A.y - B.y};    // A + B*
     const V D = V{A.x - B.x, A.y + B.y};    // A - B*
@@ -439,50 +471,80 @@ struct Resident {
     Zmk = cconj(csub(S, Tm));
   }
 
-  // forward rfft of the registers rt (pairs at m = j + T q) -> spectrum in pair layout
-  __device__ static void rfft(const V (&rt)[R], V (&Xa)[R / 2], V (&Xb)[R / 2], V& Xm, const Smem& sm,
-                              const V* __restrict__ tw, V*& last, int j) {
+  // forward rfft of the registers rt (pairs at m = j + T q) -> spectrum in group layout
+  __device__ static void rfft(const V (&rt)[R], V (&X)[R], V& Xn, const Smem& sm, const V* __restrict__ tw,
+                              V*& last, int j) {
     V v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = rt[q];
     V* wr = (last == sm.bufA) ? sm.bufB : sm.bufA;
     V* rd = (wr == sm.bufA) ? sm.bufB : sm.bufA;
-    V* lw = fft_passes<V, NC, R, -1, 0, true>(v, rd, wr, tw, j, wr);
-    // Z -> the buffer not written last
-    V* zb = (lw == sm.bufA) ? sm.bufB : sm.bufA;
+    V* lw = fft_passes<V, NC, -1, 0, true>(v, rd, wr, tw, j, wr);
+    V* zb = (lw == sm.bufA) ? sm.bufB : sm.bufA;  // Z -> the buffer not written last
 #pragma unroll
     for (int q = 0; q < R; ++q) zb[pad<V>(j + T * q)] = v[q];
     last = zb;
     __syncthreads();
+    const Real h = (Real)0.5;
 #pragma unroll
-    for (int q = 0; q < R / 2; ++q) {
-      const int k = j + T * q;
-      const V P = zb[pad<V>(k)];
-      const V Q = zb[pad<V>((NC - k) & (NC - 1))];
-      post_forward(P, Q, wk(sm, k), Xa[q], Xb[q]);
+    for (int q = 0; q < R; ++q) {
+      const int k = bin_of(j, q);
+      const V Pz = zb[pad<V>(k)];
+      const V Qz = zb[pad<V>((NC - k) & (NC - 1))];
+      const V E = V{h * (Pz.x + Qz.x), h * (Pz.y - Qz.y)};  // (P + Q*)/2
+      const V D = V{h * (Pz.x - Qz.x), h * (Pz.y + Qz.y)};  // (P - Q*)/2
+      const V O = V{D.y, -D.x};                             // D / i
+      X[q] = cadd(E, cmul(wfwd(sm, k), O));
     }
     if (j == 0) {
-      const V P = zb[pad<V>(NC / 2)];
-      Xm = cconj(P);
+      const V Z0 = zb[pad<V>(0)];
+      Xn = V{Z0.x - Z0.y, (Real)0};
+      X[0] = V{Z0.x + Z0.y, (Real)0};
     }
   }
 
-  // inverse: spectrum D (pair layout, pre-scaled by 1/n) -> time-domain pairs in v (m = j + T q)
-  __device__ static void irfft(const V (&Da)[R / 2], const V (&Db)[R / 2], const V& Dm, V (&v)[R], const Smem& sm,
-                               const V* __restrict__ tw, V*& last, int j) {
-    V* zb = (last == sm.bufA) ? sm.bufB : sm.bufA;
+  // inverse: spectrum D (group layout, pre-scaled by 1/n; Dn = D_NC on thread 0) -> time-domain
+  // pairs in v (m = j + T q).  Pre-processing and the first radix-4 pass run in registers.
+  __device__ static void irfft(const V (&D)[R], const V& Dn, V (&v)[R], const Smem& sm, const V* __restrict__ tw,
+                               V*& last, int j) {
+    if (j != 0) {
+      // pairs (g1 r, g2 3-r) = (q, 7-q); bins k = j + r G (r = 0, 1) are <= n/4: use them as "k",
+      // for r = 2, 3 the mirror NC - k = g2 + (3-r) G is the one <= n/4.
 #pragma unroll
-    for (int q = 0; q < R / 2; ++q) {
-      const int k = j + T * q;
-      V Zk, Zmk;
-      pre_inverse(Da[q], Db[q], wk(sm, k), Zk, Zmk);
-      zb[pad<V>(k)] = Zk;
-      if (k != 0) zb[pad<V>(NC - k)] = Zmk;
+      for (int r = 0; r < 2; ++r) {
+        const int k = j + r * G;
+        pre_inverse(D[r], D[7 - r], wk(sm, k), v[r], v[7 - r]);
+      }
+      const int g2 = G - j;
+#pragma unroll
+      for (int r = 2; r < 4; ++r) {
+        const int k = g2 + (3 - r) * G;  // bin of register 7 - r
+        pre_inverse(D[7 - r], D[r], wk(sm, k), v[7 - r], v[r]);
+      }
+    } else {
+      // thread 0: g1 = {0, G, 2G, 3G}, g2 = {G/2, 3G/2, 5G/2, 7G/2}
+      V dummy;
+      pre_inverse(D[0], Dn, V{(Real)1, (Real)0}, v[0], dummy);          // k = 0 with X_NC
+      pre_inverse(D[1], D[3], wk(sm, G), v[1], v[3]);                   // k = NC/4
+      v[2] = V{(Real)2 * D[2].x, -(Real)2 * D[2].y};                    // k = NC/2: 2 conj(D)
+      pre_inverse(D[4], D[7], wk(sm, G / 2), v[4], v[7]);               // k = NC/8
+      pre_inverse(D[5], D[6], wk(sm, 3 * G / 2), v[5], v[6]);           // k = 3NC/8
     }
-    if (j == 0) zb[pad<V>(NC / 2)] = V{(Real)2 * Dm.x, -(Real)2 * Dm.y};  // 2 conj(D_mid)
-    __syncthreads();
+    // first inverse pass: radix 4, NS = 1 (no twiddles), groups g1, g2 -> y[4 g + r]
+    dft4<1>(v[0], v[1], v[2], v[3]);
+    dft4<1>(v[4], v[5], v[6], v[7]);
+    V* zb = (last == sm.bufA) ? sm.bufB : sm.bufA;
     V* other = (zb == sm.bufA) ? sm.bufB : sm.bufA;
-    last = fft_passes<V, NC, R, 1, 0, false>(v, zb, other, tw, j, zb);
+    {
+      const int b1 = 4 * j, b2 = 4 * g2_of(j);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        zb[pad<V>(b1 + r)] = v[r];
+        zb[pad<V>(b2 + r)] = v[4 + r];
+      }
+    }
+    __syncthreads();
+    last = fft_passes<V, NC, 1, 1, false>(v, zb, other, tw, j, zb);
   }
 
   // -------------------------------------------------------------- one signal, all IMFs
@@ -505,33 +567,28 @@ struct Resident {
       if (j == 0) *count = -1;
       return;
     }
-    V Xa[R / 2], Xb[R / 2], Xm{0, 0};
-    rfft(rt, Xa, Xb, Xm, sm, tw, last, j);
+    V X[R], Xn{0, 0};
+    rfft(rt, X, Xn, sm, tw, last, j);
     int k = extrema(rt, sm, last, j);
     int M = 0;
     const Real invn = (Real)1 / (Real)n;
     while (M < p.max_imfs && k >= 2) {
       const int L = filter_half_length(p, k);
-      Real dA[R / 2], dB[R / 2], dM = 0;
-      const int N = search(Xa, Xb, Xm, sm, L, p, dA, dB, dM, slot, j);
+      Real d[R], dn = 0;
+      const int N = search(X, Xn, sm, L, p, d, dn, slot, j);
       // damping: D = d X / n (IMF spectrum), X <- (1 - d) X
-      V Da[R / 2], Db[R / 2], Dmv{0, 0};
+      V D[R], Dn{0, 0};
 #pragma unroll
-      for (int q = 0; q < R / 2; ++q) {
-        const Real sa = dA[q] * invn, sb = dB[q] * invn;
-        Da[q] = V{Xa[q].x * sa, Xa[q].y * sa};
-        Db[q] = V{Xb[q].x * sb, Xb[q].y * sb};
-        const Real ra = (Real)1 - dA[q], rb = (Real)1 - dB[q];
-        Xa[q] = V{Xa[q].x * ra, Xa[q].y * ra};
-        Xb[q] = V{Xb[q].x * rb, Xb[q].y * rb};
+      for (int q = 0; q < R; ++q) {
+        D[q] = cscale(X[q], d[q] * invn);
+        X[q] = cscale(X[q], (Real)1 - d[q]);
       }
       if (j == 0) {
-        const Real sm_ = dM * invn, rm = (Real)1 - dM;
-        Dmv = V{Xm.x * sm_, Xm.y * sm_};
-        Xm = V{Xm.x * rm, Xm.y * rm};
+        Dn = cscale(Xn, dn * invn);
+        Xn = cscale(Xn, (Real)1 - dn);
       }
       V v[R];
-      irfft(Da, Db, Dmv, v, sm, tw, last, j);
+      irfft(D, Dn, v, sm, tw, last, j);
       Real* o = out + (size_t)M * slot_stride;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
@@ -572,12 +629,12 @@ struct Resident {
 };
 
 // ------------------------------------------------------------------ kernels
-template <typename Real, int NC, int R>
-__global__ void __launch_bounds__(NC / R, (NC / R) <= 256 ? FIF_MINB : 1)
+template <typename Real, int NC>
+__global__ void __launch_bounds__(NC / kR, (NC / kR) <= 256 ? FIF_MINB : 1)
 fif_resident_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32_t* __restrict__ count,
                     int32_t* __restrict__ lens, int32_t* __restrict__ iters, const Real* __restrict__ sintab,
                     const Real* __restrict__ isintab, const typename Cx<Real>::V* __restrict__ tw, Params p) {
-  using K = Resident<Real, NC, R>;
+  using K = Resident<Real, NC>;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
   const int j = threadIdx.x;
@@ -591,12 +648,12 @@ fif_resident_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32
 }
 
 // test hook kernels (same device code) --------------------------------------------------------
-template <typename Real, int NC, int R>
-__global__ void __launch_bounds__(NC / R) fif_test_rfft_kernel(const Real* __restrict__ in, Real* __restrict__ out,
-                                                             int64_t batch, const Real* __restrict__ sintab,
-                                                             const Real* __restrict__ isintab,
-                                                             const typename Cx<Real>::V* __restrict__ tw) {
-  using K = Resident<Real, NC, R>;
+template <typename Real, int NC>
+__global__ void __launch_bounds__(NC / kR) fif_test_rfft_kernel(const Real* __restrict__ in, Real* __restrict__ out,
+                                                              int64_t batch, const Real* __restrict__ sintab,
+                                                              const Real* __restrict__ isintab,
+                                                              const typename Cx<Real>::V* __restrict__ tw) {
+  using K = Resident<Real, NC>;
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
@@ -604,26 +661,22 @@ __global__ void __launch_bounds__(NC / R) fif_test_rfft_kernel(const Real* __res
   K::load_tables(sm, sintab, isintab, j);
   V* last = sm.bufA;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    V rt[R], Xa[R / 2], Xb[R / 2], Xm{0, 0};
-    for (int q = 0; q < R; ++q) rt[q] = reinterpret_cast<const V*>(in + b * K::n)[j + K::T * q];
-    K::rfft(rt, Xa, Xb, Xm, sm, tw, last, j);
+    V rt[kR], X[kR], Xn{0, 0};
+    for (int q = 0; q < kR; ++q) rt[q] = reinterpret_cast<const V*>(in + b * K::n)[j + K::T * q];
+    K::rfft(rt, X, Xn, sm, tw, last, j);
     V* o = reinterpret_cast<V*>(out + b * (K::n + 2));
-    for (int q = 0; q < R / 2; ++q) {
-      const int k = j + K::T * q;
-      o[k] = Xa[q];
-      o[NC - k] = Xb[q];
-    }
-    if (j == 0) o[NC / 2] = Xm;
+    for (int q = 0; q < kR; ++q) o[K::bin_of(j, q)] = X[q];
+    if (j == 0) o[NC] = Xn;
     __syncthreads();
   }
 }
 
-template <typename Real, int NC, int R>
-__global__ void __launch_bounds__(NC / R) fif_test_irfft_kernel(const Real* __restrict__ in, Real* __restrict__ out,
-                                                              int64_t batch, const Real* __restrict__ sintab,
-                                                              const Real* __restrict__ isintab,
-                                                              const typename Cx<Real>::V* __restrict__ tw) {
-  using K = Resident<Real, NC, R>;
+template <typename Real, int NC>
+__global__ void __launch_bounds__(NC / kR) fif_test_irfft_kernel(const Real* __restrict__ in, Real* __restrict__ out,
+                                                               int64_t batch, const Real* __restrict__ sintab,
+                                                               const Real* __restrict__ isintab,
+                                                               const typename Cx<Real>::V* __restrict__ tw) {
+  using K = Resident<Real, NC>;
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
@@ -633,57 +686,53 @@ __global__ void __launch_bounds__(NC / R) fif_test_irfft_kernel(const Real* __re
   const Real invn = (Real)1 / (Real)K::n;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     const V* x = reinterpret_cast<const V*>(in + b * (K::n + 2));
-    V Da[R / 2], Db[R / 2], Dm{0, 0}, v[R];
-    for (int q = 0; q < R / 2; ++q) {
-      const int k = j + K::T * q;
-      Da[q] = V{x[k].x * invn, x[k].y * invn};
-      Db[q] = V{x[NC - k].x * invn, x[NC - k].y * invn};
-    }
-    if (j == 0) Dm = V{x[NC / 2].x * invn, x[NC / 2].y * invn};
-    K::irfft(Da, Db, Dm, v, sm, tw, last, j);
-    for (int q = 0; q < R; ++q) reinterpret_cast<V*>(out + b * K::n)[j + K::T * q] = v[q];
+    V D[kR], Dn{0, 0}, v[kR];
+    for (int q = 0; q < kR; ++q) D[q] = cscale(x[K::bin_of(j, q)], invn);
+    if (j == 0) Dn = cscale(x[NC], invn);
+    K::irfft(D, Dn, v, sm, tw, last, j);
+    for (int q = 0; q < kR; ++q) reinterpret_cast<V*>(out + b * K::n)[j + K::T * q] = v[q];
     __syncthreads();
   }
 }
 
-template <typename Real, int NC, int R>
-__global__ void __launch_bounds__(NC / R) fif_test_extrema_kernel(const Real* __restrict__ in, int32_t* __restrict__ kout,
-                                                                int64_t batch) {
-  using K = Resident<Real, NC, R>;
+template <typename Real, int NC>
+__global__ void __launch_bounds__(NC / kR) fif_test_extrema_kernel(const Real* __restrict__ in,
+                                                                 int32_t* __restrict__ kout, int64_t batch) {
+  using K = Resident<Real, NC>;
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
   const int j = threadIdx.x;
   V* last = sm.bufA;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    V rt[R];
-    for (int q = 0; q < R; ++q) rt[q] = reinterpret_cast<const V*>(in + b * K::n)[j + K::T * q];
+    V rt[kR];
+    for (int q = 0; q < kR; ++q) rt[q] = reinterpret_cast<const V*>(in + b * K::n)[j + K::T * q];
     const int k = K::extrema(rt, sm, last, j);
     if (j == 0) kout[b] = k;
     __syncthreads();
   }
 }
 
-template <typename Real, int NC, int R>
-__global__ void __launch_bounds__(NC / R) fif_test_window_kernel(Real* __restrict__ out, int L,
-                                                               const Real* __restrict__ sintab,
-                                                               const Real* __restrict__ isintab) {
-  using K = Resident<Real, NC, R>;
+template <typename Real, int NC>
+__global__ void __launch_bounds__(NC / kR) fif_test_window_kernel(Real* __restrict__ out, int L,
+                                                                const Real* __restrict__ sintab,
+                                                                const Real* __restrict__ isintab) {
+  using K = Resident<Real, NC>;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
   const int j = threadIdx.x;
   K::load_tables(sm, sintab, isintab, j);
   const Real invL = (Real)1 / (Real)L;
-  for (int k = j; k <= NC; k += K::T) out[k] = K::what(sm, L, invL, k);
+  for (int k = j; k <= NC; k += K::T) out[k] = k == 0 ? (Real)1 : K::what(sm, L, invL, k);
 }
 
-template <typename Real, int NC, int R>
-__global__ void __launch_bounds__(NC / R) fif_test_inner_kernel(const Real* __restrict__ in, Real* __restrict__ out,
-                                                              int32_t* __restrict__ Nout, int64_t batch, int L,
-                                                              const Real* __restrict__ sintab,
-                                                              const Real* __restrict__ isintab,
-                                                              const typename Cx<Real>::V* __restrict__ tw, Params p) {
-  using K = Resident<Real, NC, R>;
+template <typename Real, int NC>
+__global__ void __launch_bounds__(NC / kR) fif_test_inner_kernel(const Real* __restrict__ in, Real* __restrict__ out,
+                                                               int32_t* __restrict__ Nout, int64_t batch, int L,
+                                                               const Real* __restrict__ sintab,
+                                                               const Real* __restrict__ isintab,
+                                                               const typename Cx<Real>::V* __restrict__ tw, Params p) {
+  using K = Resident<Real, NC>;
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
@@ -693,19 +742,16 @@ __global__ void __launch_bounds__(NC / R) fif_test_inner_kernel(const Real* __re
   int slot = 0;
   const Real invn = (Real)1 / (Real)K::n;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    V rt[R], Xa[R / 2], Xb[R / 2], Xm{0, 0};
-    for (int q = 0; q < R; ++q) rt[q] = reinterpret_cast<const V*>(in + b * K::n)[j + K::T * q];
-    K::rfft(rt, Xa, Xb, Xm, sm, tw, last, j);
-    Real dA[R / 2], dB[R / 2], dM = 0;
-    const int N = K::search(Xa, Xb, Xm, sm, L, p, dA, dB, dM, slot, j);
-    V Da[R / 2], Db[R / 2], Dmv{0, 0}, v[R];
-    for (int q = 0; q < R / 2; ++q) {
-      Da[q] = V{Xa[q].x * dA[q] * invn, Xa[q].y * dA[q] * invn};
-      Db[q] = V{Xb[q].x * dB[q] * invn, Xb[q].y * dB[q] * invn};
-    }
-    if (j == 0) Dmv = V{Xm.x * dM * invn, Xm.y * dM * invn};
-    K::irfft(Da, Db, Dmv, v, sm, tw, last, j);
-    for (int q = 0; q < R; ++q) reinterpret_cast<V*>(out + b * K::n)[j + K::T * q] = v[q];
+    V rt[kR], X[kR], Xn{0, 0};
+    for (int q = 0; q < kR; ++q) rt[q] = reinterpret_cast<const V*>(in + b * K::n)[j + K::T * q];
+    K::rfft(rt, X, Xn, sm, tw, last, j);
+    Real d[kR], dn = 0;
+    const int N = K::search(X, Xn, sm, L, p, d, dn, slot, j);
+    V D[kR], Dn{0, 0}, v[kR];
+    for (int q = 0; q < kR; ++q) D[q] = cscale(X[q], d[q] * invn);
+    if (j == 0) Dn = cscale(Xn, dn * invn);
+    K::irfft(D, Dn, v, sm, tw, last, j);
+    for (int q = 0; q < kR; ++q) reinterpret_cast<V*>(out + b * K::n)[j + K::T * q] = v[q];
     if (j == 0) Nout[b] = N;
     __syncthreads();
   }

@@ -57,6 +57,7 @@ def test_unsupported_n_reported():
 
     h = ctypes.c_void_p()
     assert fif.lib().fif_plan_create(ctypes.byref(h), 3 * 1024, 1, 0, 0, 1.6, 1e-3, 200, 10) == 2
+    assert fif.lib().fif_plan_create(ctypes.byref(h), 256, 1, 0, 0, 1.6, 1e-3, 200, 10) == 2
     assert fif.lib().fif_plan_create(ctypes.byref(h), 1 << 20, 1, 0, 0, 1.6, 1e-3, 200, 10) == 2
 
 
