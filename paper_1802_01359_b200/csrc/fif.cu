@@ -50,9 +50,6 @@ struct fif_plan_s {
 
 namespace {
 
-template <typename Real> fif_dtype dtype_of();
-template <> fif_dtype dtype_of<double>() { return FIF_F64; }
-template <> fif_dtype dtype_of<float>() { return FIF_F32; }
 
 // ---------------------------------------------------------------- kernel table
 struct Entry {

@@ -190,18 +190,54 @@ __device__ __forceinline__ V* fft_passes(V (&v)[kR], V* rd, V* wr, const V* __re
 }
 
 // ------------------------------------------------------------------ block reductions
-template <int NW>
-__device__ __forceinline__ void block_sum2(double& a, double& b, double* red /*[2*NW]*/, int j) {
+// Sum M values over the block; every thread gets the same (deterministically ordered) totals.
+// red: NW*M doubles of scratch, not reused until after the next __syncthreads of the caller.
+template <int NW, int M, typename S>
+__device__ __forceinline__ void block_sum(S (&v)[M], S* red, int j) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  if ((j & 31) == 0) { red[j >> 5] = a; red[NW + (j >> 5)] = b; }
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  const int lane = j & 31;
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < M; ++i) red[(j >> 5) * M + i] = v[i];
   __syncthreads();
-  a = 0.0; b = 0.0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) { a += red[w]; b += red[NW + w]; }
+  for (int i = 0; i < M; ++i) v[i] = lane < NW ? red[lane * M + i] : (S)0;
+#pragma unroll
+  for (int o = NW / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+#pragma unroll
+  for (int i = 0; i < M; ++i) v[i] = __shfl_sync(0xffffffffu, v[i], 0);
+}
+
+// e_i = a_i^ex by squaring; ex is uniform across the block (no divergence); unrolled for ex < 256.
+template <int M, typename S>
+__device__ __forceinline__ void upow(S (&e)[M], const S (&a)[M], int ex) {
+  S b[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) { b[i] = a[i]; e[i] = (S)1; }
+  if (ex < 256) {
+#pragma unroll
+    for (int bit = 0; bit < 8; ++bit) {
+      if ((ex >> bit) & 1)
+#pragma unroll
+        for (int i = 0; i < M; ++i) e[i] *= b[i];
+      if ((ex >> (bit + 1)) != 0)
+#pragma unroll
+        for (int i = 0; i < M; ++i) b[i] *= b[i];
+    }
+  } else {
+    for (int x = ex; x; x >>= 1) {
+      if (x & 1)
+#pragma unroll
+        for (int i = 0; i < M; ++i) e[i] *= b[i];
+#pragma unroll
+      for (int i = 0; i < M; ++i) b[i] *= b[i];
+    }
+  }
 }
 
 // ------------------------------------------------------------------ the kernel body
@@ -223,8 +259,8 @@ struct Resident {
   static constexpr size_t off_bufB = off_bufA + sizeof(V) * PADN;
   static constexpr size_t off_sin = off_bufB + sizeof(V) * PADN;
   static constexpr size_t off_isin = off_sin + sizeof(Real) * ((NC + 2) & ~1);
-  static constexpr size_t off_red = off_isin + sizeof(Real) * ((NC + 2) & ~1);  // 2 slots x 2*NW doubles
-  static constexpr size_t off_nbr = off_red + sizeof(double) * 4 * NW;         // NW*R V
+  static constexpr size_t off_red = off_isin + sizeof(Real) * ((NC + 2) & ~1);  // 2 slots x 4*NW doubles
+  static constexpr size_t off_nbr = off_red + sizeof(double) * 8 * NW;         // NW*R V
   static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // NW + 8 ints
   static constexpr size_t smem_bytes = off_int + sizeof(int) * (NW + 8);
 
@@ -348,109 +384,164 @@ struct Resident {
     return s2 * s2;
   }
 
-  // -------------------------------------------------------------- a5 stopping search (one probe)
+  // -------------------------------------------------------------- a5 stopping search
   // P(N) = sum c_k a_k^{2(N-1)} |X_k|^2, Q(N) = sum c_k w_k^2 a_k^{2(N-1)} |X_k|^2 (fp64 accumulation),
-  // c_k = 1 for k in {0, NC}, 2 otherwise.  a_k = 1 - w_k (w_k in [0, 1]; a value ~1e-16 below 0
-  // from rounding only ever enters as a tiny power).  Also returns d_k = a_k^N.
-  __device__ static void probe(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N, double& P,
-                               double& Q, Real (&d)[R], Real& dn, double* red, int j) {
-    double P2 = 0.0, Q2 = 0.0;  // sums with c = 1, doubled at the end
-    const int ex = N - 1;
-    const int nbits = ex ? 32 - __clz(ex) : 0;
-#pragma unroll
-    for (int g = 0; g < R; g += 4) {
-      double a[4], e[4], b[4], w[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int kk = bin_of(j, g + i);
-        Real wv = what(sm, L, invL, kk);
-        if (g + i == 0 && j == 0) wv = (Real)1;  // bin 0: w_hat_0 = 1 (row sums to 1)
-        w[i] = (double)wv;
-        a[i] = 1.0 - w[i];
-        b[i] = a[i];
-        e[i] = 1.0;
-      }
-      for (int bit = 0; bit < nbits; ++bit) {  // e = a^(N-1), uniform exponent
-        if ((ex >> bit) & 1) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) e[i] *= b[i];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) b[i] *= b[i];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const V x = X[g + i];
-        double pk = (double)x.x * (double)x.x + (double)x.y * (double)x.y;
-        if (g + i == 0 && j == 0) pk *= 0.5;  // bin 0 has weight 1
-        const double px = pk * (e[i] * e[i]);
-        P2 += px;
-        Q2 += px * (w[i] * w[i]);
-        d[g + i] = (Real)(e[i] * a[i]);
-      }
-    }
-    if (j == 0) {  // Nyquist bin k = NC, weight 1
-      const double wv = (double)what(sm, L, invL, NC);
-      const double a = 1.0 - wv;
-      double e = 1.0, b = a;
-      for (int bit = 0; bit < nbits; ++bit) {
-        if ((ex >> bit) & 1) e *= b;
-        b *= b;
-      }
-      const double pk = 0.5 * ((double)Xn.x * (double)Xn.x + (double)Xn.y * (double)Xn.y);
-      const double px = pk * (e * e);
-      P2 += px;
-      Q2 += px * (wv * wv);
-      dn = (Real)(e * a);
-    }
-    P = 2.0 * P2;
-    Q = 2.0 * Q2;
-    block_sum2<NW>(P, Q, red, j);
+  // c_k = 1 for k in {0, NC}, 2 otherwise; pass(N) <=> Q(N) <= delta^2 P(N) (SD_N <= delta).
+  // a_k = 1 - w_k (w_k in [0, 1]; a value ~1e-16 below 0 from rounding only ever enters as a
+  // tiny power).  The thread's bins: X[q] (group layout) + X_NC on thread 0 (handled as the
+  // 9th bin with a zero amplitude elsewhere).
+  static constexpr int NB = R + 1;
+  // bins of group g (two groups of <= 5 bins keep register pressure low): q in [lo(g), hi(g))
+  __device__ static constexpr int glo(int g) { return g == 0 ? 0 : 4; }
+  __device__ static constexpr int ghi(int g) { return g == 0 ? 4 : NB; }
+  __device__ static double bin_w1(const Smem& sm, int L, Real invL, int j, int q) {
+    if (q == R) return (double)what(sm, L, invL, NC);
+    if (q == 0 && j == 0) return 1.0;  // bin 0: w_hat_0 = 1 (rows sum to 1)
+    return (double)what(sm, L, invL, bin_of(j, q));
+  }
+  __device__ static double bin_p1(const V (&X)[R], const V& Xn, int j, int q) {
+    if (q == R) return (j == 0) ? 0.5 * ((double)Xn.x * (double)Xn.x) : 0.0;  // X_NC real, weight 1
+    const double p = (double)X[q].x * (double)X[q].x + (double)X[q].y * (double)X[q].y;
+    return (q == 0 && j == 0) ? 0.5 * p : p;                                   // X_0 weight 1
   }
 
-  // d_k = a_k^N only (no reduction): after a bisection that did not end on its last probe
-  __device__ static void damping_only(const Smem& sm, int L, Real invL, int N, Real (&d)[R], Real& dn, int j) {
+  // One fp64 probe at N: (P, Q) block totals and d_k = a_k^N.
+  __device__ static void probe(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N, double& P,
+                               double& Q, double (&d)[NB], double* red, int j) {
+    double v[2] = {0.0, 0.0};
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      Real wv = what(sm, L, invL, bin_of(j, q));
-      if (q == 0 && j == 0) wv = (Real)1;
-      const double a = 1.0 - (double)wv;
-      double e = 1.0, b = a;
-      for (int x = N; x; x >>= 1) {
-        if (x & 1) e *= b;
-        b *= b;
+    for (int g = 0; g < 2; ++g) {
+      constexpr int M = 5;
+      double w[M], a[M], e[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const int q = glo(g) + i;
+        w[i] = q < ghi(g) ? bin_w1(sm, L, invL, j, q) : 1.0;
+        a[i] = 1.0 - w[i];
       }
-      d[q] = (Real)e;
-    }
-    if (j == 0) {
-      const double a = 1.0 - (double)what(sm, L, invL, NC);
-      double e = 1.0, b = a;
-      for (int x = N; x; x >>= 1) {
-        if (x & 1) e *= b;
-        b *= b;
+      upow<M>(e, a, N - 1);
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const int q = glo(g) + i;
+        if (q < ghi(g)) {
+          const double px = bin_p1(X, Xn, j, q) * (e[i] * e[i]);
+          v[0] += px;
+          v[1] += px * (w[i] * w[i]);
+          d[q] = e[i] * a[i];
+        }
       }
-      dn = (Real)e;
     }
+    v[0] *= 2.0; v[1] *= 2.0;
+    block_sum<NW, 2>(v, red, j);
+    P = v[0]; Q = v[1];
+  }
+
+  // fp32 hint for the minimal passing N in [1, hi] (bisection on fp32 sums); only a hint:
+  // the caller verifies it in fp64.
+  __device__ static int hint_fp32(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int hi,
+                                  float delta2, float* red, int j) {
+    float a[NB], pk[NB], pw[NB];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const double w = bin_w1(sm, L, invL, j, q), p64 = bin_p1(X, Xn, j, q);
+      a[q] = (float)(1.0 - w);
+      pk[q] = (float)p64;
+      pw[q] = (float)(p64 * w * w);
+    }
+    int lo = 0;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      float e[NB];
+      upow<NB>(e, a, mid - 1);
+      float v[2] = {0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const float x = e[i] * e[i];
+        v[0] += pk[i] * x;
+        v[1] += pw[i] * x;
+      }
+      block_sum<NW, 2>(v, red, j);
+      if (v[1] <= delta2 * v[0]) hi = mid; else lo = mid;
+    }
+    return hi;
+  }
+
+  // fp64 check of pass(N-1) (N > 1) and pass(N) in one pass; d_k = a_k^N.
+  __device__ static void verify(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N,
+                                double delta2, bool& pass_lo, bool& pass_hi, double (&d)[NB], double* red, int j) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      constexpr int M = 5;
+      double w[M], a[M], e[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const int q = glo(g) + i;
+        w[i] = q < ghi(g) ? bin_w1(sm, L, invL, j, q) : 1.0;
+        a[i] = 1.0 - w[i];
+      }
+      upow<M>(e, a, N > 1 ? N - 2 : 0);  // a^(N-2)
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const int q = glo(g) + i;
+        if (q < ghi(g)) {
+          const double pk = bin_p1(X, Xn, j, q);
+          const double w2 = w[i] * w[i];
+          const double e1 = N > 1 ? e[i] * a[i] : e[i];  // a^(N-1)
+          const double x0 = pk * (e[i] * e[i]), x1 = pk * (e1 * e1);
+          v[0] += x0;
+          v[1] += x0 * w2;
+          v[2] += x1;
+          v[3] += x1 * w2;
+          d[q] = e1 * a[i];
+        }
+      }
+    }
+    block_sum<NW, 4>(v, red, j);
+    pass_lo = (N > 1) && (v[1] <= delta2 * v[0]);
+    pass_hi = v[3] <= delta2 * v[2];
   }
 
   __device__ static int search(const V (&X)[R], const V& Xn, const Smem& sm, int L, const Params& p, Real (&d)[R],
                                Real& dn, int& slot, int j) {
     const Real invL = (Real)1 / (Real)L;
-    double Pv, Qv;
-    const int cap = p.max_inner;
-    probe(X, Xn, sm, L, invL, cap, Pv, Qv, d, dn, sm.red + slot * 2 * NW, j);
+    double* red = sm.red + slot * 4 * NW;
     slot ^= 1;
-    if (!(Qv <= p.delta2 * Pv)) return cap;
-    int lo = 0, hi = cap, lastN = cap;  // invariant: pass(hi), !pass(lo) (lo = 0 is virtual)
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      probe(X, Xn, sm, L, invL, mid, Pv, Qv, d, dn, sm.red + slot * 2 * NW, j);
+    double Pv, Qv, dd[NB];
+    const int cap = p.max_inner;
+    probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+    int N = cap;
+    if (Qv <= p.delta2 * Pv) {
+      // the minimal passing N lies in [1, cap]: fp32 hint, fp64 verification (+ fp64 bisection fallback)
+      red = sm.red + slot * 4 * NW;
       slot ^= 1;
-      lastN = mid;
-      if (Qv <= p.delta2 * Pv) hi = mid; else lo = mid;
+      const int Nh = hint_fp32(X, Xn, sm, L, invL, cap, (float)p.delta2, reinterpret_cast<float*>(red), j);
+      red = sm.red + slot * 4 * NW;
+      slot ^= 1;
+      bool plo, phi;
+      verify(X, Xn, sm, L, invL, Nh, p.delta2, plo, phi, dd, red, j);
+      if (phi && !plo) {
+        N = Nh;
+      } else {
+        int lo = phi ? 0 : Nh, hi = phi ? Nh - 1 : cap;  // pass(hi) known, !pass(lo) (lo = 0 virtual)
+        if (phi && hi == 0) hi = 1;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          red = sm.red + slot * 4 * NW;
+          slot ^= 1;
+          probe(X, Xn, sm, L, invL, mid, Pv, Qv, dd, red, j);
+          if (Qv <= p.delta2 * Pv) hi = mid; else lo = mid;
+        }
+        N = hi;
+        red = sm.red + slot * 4 * NW;
+        slot ^= 1;
+        probe(X, Xn, sm, L, invL, N, Pv, Qv, dd, red, j);  // d = a^N
+      }
     }
-    if (lastN != hi) damping_only(sm, L, invL, hi, d, dn, j);
-    return hi;
+#pragma unroll
+    for (int q = 0; q < R; ++q) d[q] = (Real)dd[q];
+    dn = (Real)dd[R];
+    return N;
   }
 
   // -------------------------------------------------------------- real-FFT pre/post processing
@@ -505,30 +596,30 @@ struct Resident {
 
   // inverse: spectrum D (group layout, pre-scaled by 1/n; Dn = D_NC on thread 0) -> time-domain
   // pairs in v (m = j + T q).  Pre-processing and the first radix-4 pass run in registers.
-  __device__ static void irfft(const V (&D)[R], const V& Dn, V (&v)[R], const Smem& sm, const V* __restrict__ tw,
-                               V*& last, int j) {
+  __device__ static void irfft(V (&v)[R], const V& Dn, const Smem& sm, const V* __restrict__ tw, V*& last, int j) {
+    // in place: v holds D on entry (group layout), time-domain pairs on exit
     if (j != 0) {
       // pairs (g1 r, g2 3-r) = (q, 7-q); bins k = j + r G (r = 0, 1) are <= n/4: use them as "k",
       // for r = 2, 3 the mirror NC - k = g2 + (3-r) G is the one <= n/4.
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int k = j + r * G;
-        pre_inverse(D[r], D[7 - r], wk(sm, k), v[r], v[7 - r]);
+        pre_inverse(v[r], v[7 - r], wk(sm, k), v[r], v[7 - r]);
       }
       const int g2 = G - j;
 #pragma unroll
       for (int r = 2; r < 4; ++r) {
         const int k = g2 + (3 - r) * G;  // bin of register 7 - r
-        pre_inverse(D[7 - r], D[r], wk(sm, k), v[7 - r], v[r]);
+        pre_inverse(v[7 - r], v[r], wk(sm, k), v[7 - r], v[r]);
       }
     } else {
       // thread 0: g1 = {0, G, 2G, 3G}, g2 = {G/2, 3G/2, 5G/2, 7G/2}
       V dummy;
-      pre_inverse(D[0], Dn, V{(Real)1, (Real)0}, v[0], dummy);          // k = 0 with X_NC
-      pre_inverse(D[1], D[3], wk(sm, G), v[1], v[3]);                   // k = NC/4
-      v[2] = V{(Real)2 * D[2].x, -(Real)2 * D[2].y};                    // k = NC/2: 2 conj(D)
-      pre_inverse(D[4], D[7], wk(sm, G / 2), v[4], v[7]);               // k = NC/8
-      pre_inverse(D[5], D[6], wk(sm, 3 * G / 2), v[5], v[6]);           // k = 3NC/8
+      pre_inverse(v[0], Dn, V{(Real)1, (Real)0}, v[0], dummy);          // k = 0 with X_NC
+      pre_inverse(v[1], v[3], wk(sm, G), v[1], v[3]);                   // k = NC/4
+      v[2] = V{(Real)2 * v[2].x, -(Real)2 * v[2].y};                    // k = NC/2: 2 conj(D)
+      pre_inverse(v[4], v[7], wk(sm, G / 2), v[4], v[7]);               // k = NC/8
+      pre_inverse(v[5], v[6], wk(sm, 3 * G / 2), v[5], v[6]);           // k = 3NC/8
     }
     // first inverse pass: radix 4, NS = 1 (no twiddles), groups g1, g2 -> y[4 g + r]
     dft4<1>(v[0], v[1], v[2], v[3]);
@@ -577,18 +668,17 @@ struct Resident {
       Real d[R], dn = 0;
       const int N = search(X, Xn, sm, L, p, d, dn, slot, j);
       // damping: D = d X / n (IMF spectrum), X <- (1 - d) X
-      V D[R], Dn{0, 0};
+      V v[R], Dn{0, 0};
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        D[q] = cscale(X[q], d[q] * invn);
+        v[q] = cscale(X[q], d[q] * invn);
         X[q] = cscale(X[q], (Real)1 - d[q]);
       }
       if (j == 0) {
         Dn = cscale(Xn, dn * invn);
         Xn = cscale(Xn, (Real)1 - dn);
       }
-      V v[R];
-      irfft(D, Dn, v, sm, tw, last, j);
+      irfft(v, Dn, sm, tw, last, j);
       Real* o = out + (size_t)M * slot_stride;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
@@ -686,10 +776,10 @@ __global__ void __launch_bounds__(NC / kR) fif_test_irfft_kernel(const Real* __r
   const Real invn = (Real)1 / (Real)K::n;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     const V* x = reinterpret_cast<const V*>(in + b * (K::n + 2));
-    V D[kR], Dn{0, 0}, v[kR];
-    for (int q = 0; q < kR; ++q) D[q] = cscale(x[K::bin_of(j, q)], invn);
+    V Dn{0, 0}, v[kR];
+    for (int q = 0; q < kR; ++q) v[q] = cscale(x[K::bin_of(j, q)], invn);
     if (j == 0) Dn = cscale(x[NC], invn);
-    K::irfft(D, Dn, v, sm, tw, last, j);
+    K::irfft(v, Dn, sm, tw, last, j);
     for (int q = 0; q < kR; ++q) reinterpret_cast<V*>(out + b * K::n)[j + K::T * q] = v[q];
     __syncthreads();
   }
@@ -747,10 +837,10 @@ __global__ void __launch_bounds__(NC / kR) fif_test_inner_kernel(const Real* __r
     K::rfft(rt, X, Xn, sm, tw, last, j);
     Real d[kR], dn = 0;
     const int N = K::search(X, Xn, sm, L, p, d, dn, slot, j);
-    V D[kR], Dn{0, 0}, v[kR];
-    for (int q = 0; q < kR; ++q) D[q] = cscale(X[q], d[q] * invn);
+    V Dn{0, 0}, v[kR];
+    for (int q = 0; q < kR; ++q) v[q] = cscale(X[q], d[q] * invn);
     if (j == 0) Dn = cscale(Xn, dn * invn);
-    K::irfft(D, Dn, v, sm, tw, last, j);
+    K::irfft(v, Dn, sm, tw, last, j);
     for (int q = 0; q < kR; ++q) reinterpret_cast<V*>(out + b * K::n)[j + K::T * q] = v[q];
     if (j == 0) Nout[b] = N;
     __syncthreads();
