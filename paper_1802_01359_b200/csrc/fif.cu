@@ -18,6 +18,9 @@ using namespace fifgpu;
 namespace {
 
 enum { FIF_MAX_STAGES = 3 };
+// max_inner value with a compile-time-specialised kernel (the paper's/BASELINE's cap of 200,
+// PAPER.md:433 "limit on the maximal number of iterations"); any other value uses the generic kernel
+constexpr int kFastCap = 200;
 
 struct Staging {
   void* d_in = nullptr;
@@ -65,8 +68,13 @@ struct Inst {
   using V = typename Cx<Real>::V;
   static cudaError_t prepare() {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, kFastCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, kFastCap>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem_bytes)) != cudaSuccess)
+      return e;
     if ((e = cudaFuncSetAttribute(fif_test_rfft_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(fif_test_irfft_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -75,13 +83,13 @@ struct Inst {
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(fif_test_window_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     return cudaSuccess;
   }
   static int occupancy() {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC>, K::T, K::smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC, kFastCap>, K::T, K::smem_bytes);
     return occ;
   }
   static void decompose(const fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
@@ -89,9 +97,14 @@ struct Inst {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
     const int64_t cap = (int64_t)p->num_sms * p->occ;
     const int grid = (int)(batch < cap ? batch : cap);
-    fif_resident_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
-        (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
-        (const V*)p->d_tw, prm);
+    if (p->max_inner == kFastCap)
+      fif_resident_kernel<Real, NC, kFastCap><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
+    else
+      fif_resident_kernel<Real, NC, 0><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
   }
   static void test_rfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
     const int grid = (int)(batch < 4096 ? batch : 4096);
@@ -116,9 +129,14 @@ struct Inst {
                          cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
     const int grid = (int)(batch < 4096 ? batch : 4096);
-    fif_test_inner_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
-        (const Real*)in, (Real*)out, N, batch, L, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw,
-        prm);
+    if (p->max_inner == kFastCap)
+      fif_test_inner_kernel<Real, NC, kFastCap><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)in, (Real*)out, N, batch, L, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
+    else
+      fif_test_inner_kernel<Real, NC, 0><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)in, (Real*)out, N, batch, L, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
   }
 };
 

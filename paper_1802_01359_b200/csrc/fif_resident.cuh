@@ -167,8 +167,14 @@ __device__ __forceinline__ void stockham_pass(V (&v)[kR], const V* src, V* dst, 
       for (int r = 0; r < RP; ++r) v[u + r * VP] = w[r];
     } else {
       const int idxD = (vt / NS) * NS * RP + k;
+      if constexpr (NS % 8 == 0) {  // pad is additive over r NS: one base address
+        V* d0 = dst + pad<V>(idxD);
 #pragma unroll
-      for (int r = 0; r < RP; ++r) dst[pad<V>(idxD + r * NS)] = w[r];
+        for (int r = 0; r < RP; ++r) d0[pad<V>(r * NS)] = w[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < RP; ++r) dst[pad<V>(idxD + r * NS)] = w[r];
+      }
     }
   }
 }
@@ -213,6 +219,27 @@ __device__ __forceinline__ void block_sum(S (&v)[M], S* red, int j) {
   for (int i = 0; i < M; ++i) v[i] = __shfl_sync(0xffffffffu, v[i], 0);
 }
 
+// e_i = a_i^E, E a compile-time constant: the addition chain is fixed at compile time.
+template <int E, int M, typename S>
+__device__ __forceinline__ void upow_ct(S (&e)[M], const S (&a)[M]) {
+  S b[M];
+  bool first = true;
+#pragma unroll
+  for (int i = 0; i < M; ++i) { b[i] = a[i]; e[i] = (S)1; }
+#pragma unroll
+  for (int bit = 0; bit < 16; ++bit) {
+    if ((E >> bit) & 1) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) e[i] = first ? b[i] : e[i] * b[i];
+      first = false;
+    }
+    if ((E >> (bit + 1)) != 0) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) b[i] *= b[i];
+    }
+  }
+}
+
 // e_i = a_i^ex by squaring; ex is uniform across the block (no divergence); unrolled for ex < 256.
 template <int M, typename S>
 __device__ __forceinline__ void upow(S (&e)[M], const S (&a)[M], int ex) {
@@ -241,7 +268,9 @@ __device__ __forceinline__ void upow(S (&e)[M], const S (&a)[M], int ex) {
 }
 
 // ------------------------------------------------------------------ the kernel body
-template <typename Real, int NC>
+// CAP > 0: a compile-time max_inner (the first probe's power chain is fixed at compile time);
+// CAP = 0: runtime max_inner.
+template <typename Real, int NC, int CAP = 0>
 struct Resident {
   using V = typename Cx<Real>::V;
   static constexpr int n = 2 * NC;
@@ -261,8 +290,8 @@ struct Resident {
   static constexpr size_t off_isin = off_sin + sizeof(Real) * ((NC + 2) & ~1);
   static constexpr size_t off_red = off_isin + sizeof(Real) * ((NC + 2) & ~1);  // 2 slots x 4*NW doubles
   static constexpr size_t off_nbr = off_red + sizeof(double) * 8 * NW;         // NW*R V
-  static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // NW + 8 ints
-  static constexpr size_t smem_bytes = off_int + sizeof(int) * (NW + 8);
+  static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // 2 NW + 8 ints
+  static constexpr size_t smem_bytes = off_int + sizeof(int) * (2 * NW + 8);
 
   struct Smem {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
@@ -274,43 +303,56 @@ struct Resident {
 
   // -------------------------------------------------------------- a2 extrema count
   // Fast path: with no zero difference, k = #{p : sign(D_p) != sign(D_p+1)} -- a plain
-  // sum.  Any zero difference -> exact sequential rule (zeros dropped) in one warp.
+  // sum of sign-bit XORs over 8-bit masks (q = register index).  Any zero difference ->
+  // exact sequential rule (zeros dropped) in one warp.  Sign / zero tests are integer ops
+  // on the IEEE bit pattern (no FP64-pipe compares).
+  __device__ static unsigned sgn_bit(double d) { return (unsigned)__double2hiint(d) >> 31; }
+  __device__ static unsigned sgn_bit(float d) { return (unsigned)__float_as_int(d) >> 31; }
+  __device__ static bool is_zero(double d) {
+    return (((unsigned)__double2hiint(d) & 0x7fffffffu) | (unsigned)__double2loint(d)) == 0u;
+  }
+  __device__ static bool is_zero(float d) { return ((unsigned)__float_as_int(d) & 0x7fffffffu) == 0u; }
+
   __device__ static int extrema(const V (&rt)[R], const Smem& sm, V*& last, int j) {
     const int lane = j & 31, w = j >> 5;
-    V nb[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      nb[q].x = __shfl_down_sync(0xffffffffu, rt[q].x, 1);
-      nb[q].y = __shfl_down_sync(0xffffffffu, rt[q].y, 1);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < R; ++q) sm.nbr[w * R + q] = rt[q];
-    }
-    __syncthreads();
-    if (lane == 31) {
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        int w2 = w + 1, q2 = q;
-        if (w2 == NW) { w2 = 0; q2 = q + 1; }
-        if (q2 < R) nb[q] = sm.nbr[w2 * R + q2];
-      }
-    }
-    int cnt = 0;
+    unsigned S0 = 0, S1 = 0;   // sign bits of D_{2m} and D_{2m+1}, bit q
     bool zero = false;
+    Real xn[R];                // x_{2m+2}: first sample of the next pair
+#pragma unroll
+    for (int q = 0; q < R; ++q) xn[q] = __shfl_down_sync(0xffffffffu, rt[q].x, 1);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const Real d0 = rt[q].y - rt[q].x;  // D_{2m}
-      const Real d1 = nb[q].x - rt[q].y;  // D_{2m+1}
-      const Real d2 = nb[q].y - nb[q].x;  // D_{2m+2} (checked for zero by pair m+1)
-      const bool s0 = d0 > (Real)0, s1 = d1 > (Real)0, s2 = d2 > (Real)0;
-      if (q < R - 1 || j < T - 1) {  // pair m = NC-1 has no successor
-        zero |= (d0 == (Real)0) | (d1 == (Real)0);
-        cnt += (s0 != s1) + (s1 != s2);
-      } else {
-        zero |= (d0 == (Real)0);
+      S0 |= sgn_bit(d0) << q;
+      zero |= is_zero(d0);
+    }
+    unsigned S2 = __shfl_down_sync(0xffffffffu, S0, 1);  // sign bits of D_{2m+2} (next pair's D_{2m})
+    int* nmask = sm.ired + NW + 1;                      // [NW] masks of lane 0 of each warp
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) sm.nbr[w * R + q].x = rt[q].x;
+      nmask[w] = (int)S0;
+    }
+    __syncthreads();
+    if (lane == 31) {
+      if (w + 1 < NW) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) xn[q] = sm.nbr[(w + 1) * R + q].x;
+        S2 = (unsigned)nmask[w + 1];
+      } else {  // thread T-1: pair m = T-1 + T q is followed by pair T (q+1) of thread 0
+#pragma unroll
+        for (int q = 0; q < R - 1; ++q) xn[q] = sm.nbr[q + 1].x;
+        S2 = (unsigned)nmask[0] >> 1;
       }
     }
+    const unsigned valid = (j == T - 1) ? ((1u << (R - 1)) - 1u) : ((1u << R) - 1u);  // pair NC-1 has no successor
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const Real d1 = xn[q] - rt[q].y;  // D_{2m+1}
+      S1 |= sgn_bit(d1) << q;
+      zero |= ((valid >> q) & 1u) && is_zero(d1);
+    }
+    int cnt = __popc((S0 ^ S1) & valid) + __popc((S1 ^ S2) & valid);
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if (lane == 0) sm.ired[w] = cnt;
     const int anyzero = __syncthreads_or(zero);
@@ -405,7 +447,8 @@ struct Resident {
     return (q == 0 && j == 0) ? 0.5 * p : p;                                   // X_0 weight 1
   }
 
-  // One fp64 probe at N: (P, Q) block totals and d_k = a_k^N.
+  // One fp64 probe at N: (P, Q) block totals and d_k = a_k^N.  ECT >= 0: N - 1 == ECT at compile time.
+  template <int ECT = -1>
   __device__ static void probe(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N, double& P,
                                double& Q, double (&d)[NB], double* red, int j) {
     double v[2] = {0.0, 0.0};
@@ -419,7 +462,7 @@ struct Resident {
         w[i] = q < ghi(g) ? bin_w1(sm, L, invL, j, q) : 1.0;
         a[i] = 1.0 - w[i];
       }
-      upow<M>(e, a, N - 1);
+      if constexpr (ECT >= 0) upow_ct<ECT>(e, a); else upow<M>(e, a, N - 1);
 #pragma unroll
       for (int i = 0; i < M; ++i) {
         const int q = glo(g) + i;
@@ -436,27 +479,28 @@ struct Resident {
     P = v[0]; Q = v[1];
   }
 
-  // fp32 hint for the minimal passing N in [1, hi] (bisection on fp32 sums); only a hint:
-  // the caller verifies it in fp64.
+  // fp32 hint for the minimal passing N in [1, hi] (bisection on fp32 sums, powers through the SFU:
+  // a^(2(N-1)) = ex2(2(N-1) lg2 a)); only a hint: the caller verifies it in fp64.
+  __device__ static float lg2f(float x) { float y; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+  __device__ static float ex2f(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
   __device__ static int hint_fp32(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int hi,
                                   float delta2, float* red, int j) {
-    float a[NB], pk[NB], pw[NB];
+    float l2[NB], pk[NB], pw[NB];
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
       const double w = bin_w1(sm, L, invL, j, q), p64 = bin_p1(X, Xn, j, q);
-      a[q] = (float)(1.0 - w);
+      l2[q] = fmaxf(2.0f * lg2f(fmaxf((float)(1.0 - w), 0.0f)), -1e30f);  // finite: 0 * l2 = 0 at N = 1
       pk[q] = (float)p64;
       pw[q] = (float)(p64 * w * w);
     }
     int lo = 0;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      float e[NB];
-      upow<NB>(e, a, mid - 1);
+      const float t = (float)(mid - 1);
       float v[2] = {0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        const float x = e[i] * e[i];
+        const float x = ex2f(t * l2[i]);
         v[0] += pk[i] * x;
         v[1] += pw[i] * x;
       }
@@ -509,7 +553,8 @@ struct Resident {
     slot ^= 1;
     double Pv, Qv, dd[NB];
     const int cap = p.max_inner;
-    probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+    if constexpr (CAP > 0) probe<CAP - 1>(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+    else probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
     int N = cap;
     if (Qv <= p.delta2 * Pv) {
       // the minimal passing N lies in [1, cap]: fp32 hint, fp64 verification (+ fp64 bisection fallback)
@@ -719,12 +764,12 @@ struct Resident {
 };
 
 // ------------------------------------------------------------------ kernels
-template <typename Real, int NC>
+template <typename Real, int NC, int CAP>
 __global__ void __launch_bounds__(NC / kR, (NC / kR) <= 256 ? FIF_MINB : 1)
 fif_resident_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32_t* __restrict__ count,
                     int32_t* __restrict__ lens, int32_t* __restrict__ iters, const Real* __restrict__ sintab,
                     const Real* __restrict__ isintab, const typename Cx<Real>::V* __restrict__ tw, Params p) {
-  using K = Resident<Real, NC>;
+  using K = Resident<Real, NC, CAP>;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
   const int j = threadIdx.x;
@@ -816,13 +861,13 @@ __global__ void __launch_bounds__(NC / kR) fif_test_window_kernel(Real* __restri
   for (int k = j; k <= NC; k += K::T) out[k] = k == 0 ? (Real)1 : K::what(sm, L, invL, k);
 }
 
-template <typename Real, int NC>
+template <typename Real, int NC, int CAP>
 __global__ void __launch_bounds__(NC / kR) fif_test_inner_kernel(const Real* __restrict__ in, Real* __restrict__ out,
                                                                int32_t* __restrict__ Nout, int64_t batch, int L,
                                                                const Real* __restrict__ sintab,
                                                                const Real* __restrict__ isintab,
                                                                const typename Cx<Real>::V* __restrict__ tw, Params p) {
-  using K = Resident<Real, NC>;
+  using K = Resident<Real, NC, CAP>;
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
