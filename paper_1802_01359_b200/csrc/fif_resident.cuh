@@ -37,6 +37,12 @@
 #ifndef FIF_MINB
 #define FIF_MINB 2
 #endif
+#ifndef FIF_EXT1
+#define FIF_EXT1 0
+#endif
+#ifndef FIF_SPEC
+#define FIF_SPEC 0
+#endif
 
 namespace fifgpu {
 
@@ -126,25 +132,40 @@ template <int DIR, typename V> struct Dft<8, DIR, V> {
   __device__ __forceinline__ static void run(V* v) { dft8<DIR>(v); }
 };
 
-// shared-memory padding: one pad element per 128 bytes of data (bank-conflict-free
-// strided Stockham stores)
-template <typename V> __host__ __device__ constexpr int pad(int i) {
-  return sizeof(V) == 16 ? i + (i >> 3) : i + (i >> 4);
+// shared-memory XOR swizzle of the FFT exchange buffers: element i of a row of ROW = 128 B /
+// sizeof(V) elements is stored at i ^ (row index mod ROW).  Every access pattern of the passes
+// (consecutive, stride-4 radix-4 stores, the mirrored group stores) then hits ROW distinct
+// 16-/8-byte bank groups per quarter-/half-warp phase, with no padding.
+template <typename V> __host__ __device__ constexpr int swz_row() { return 128 / (int)sizeof(V); }
+// MODE 0: XOR with (row mod ROW); MODE 1: XOR with (row mod 4) -- used for the buffer written by
+// the radix-4 pass 0 (its mirrored group stores are conflict-free only under a period-4 swizzle).
+template <typename V, int MODE = 0> __host__ __device__ constexpr int sw(int i) {
+  return i ^ ((i / swz_row<V>()) & (MODE == 0 ? swz_row<V>() - 1 : 3));
 }
-template <typename V> __host__ __device__ constexpr int padded_len(int n) { return pad<V>(n) + 1; }
+// sw(i + off) == sw(i) + off whenever off is a multiple of ROW^2
+template <typename V> __host__ __device__ constexpr bool sw_additive(int off) {
+  return off % (swz_row<V>() * swz_row<V>()) == 0;
+}
+// swizzle mode of the buffer written by pass p (read by pass p+1)
+__host__ __device__ constexpr int sw_mode_out(int p) { return p == 0 ? 1 : 0; }
 
 // ------------------------------------------------------------------ one Stockham pass
 // Virtual threads vt in [0, NC/RP): inputs x[vt + r NC/RP], twiddle e^{DIR 2 pi i k r/(NS RP)}
 // with k = vt mod NS, radix-RP DFT, outputs y[(vt/NS) NS RP + k + r NS].
 // Real thread j runs virtual threads vt = j + T u, u < 8/RP; its register q = u + r (8/RP)
 // holds position j + T q, which is exactly vt + r NC/RP.
-template <typename V, int NC, int RP, int NS, int DIR, bool FROM_REGS, bool TO_REGS>
+template <typename V, int NC, int RP, int NS, int DIR, bool FROM_REGS, bool TO_REGS, int MIN, int MOUT>
 __device__ __forceinline__ void stockham_pass(V (&v)[kR], const V* src, V* dst, const V* __restrict__ tw, int j) {
   constexpr int T = NC / kR, VP = kR / RP;
   if (!FROM_REGS) {
-    const V* s0 = src + pad<V>(j);
+    if constexpr (sw_additive<V>(T)) {
+      const V* s0 = src + sw<V, MIN>(j);
 #pragma unroll
-    for (int q = 0; q < kR; ++q) v[q] = s0[pad<V>(T * q)];  // T multiple of 8: pad is additive
+      for (int q = 0; q < kR; ++q) v[q] = s0[T * q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < kR; ++q) v[q] = src[sw<V, MIN>(j + T * q)];
+    }
   }
 #pragma unroll
   for (int u = 0; u < VP; ++u) {
@@ -153,12 +174,24 @@ __device__ __forceinline__ void stockham_pass(V (&v)[kR], const V* src, V* dst, 
     V w[RP];
 #pragma unroll
     for (int r = 0; r < RP; ++r) w[r] = v[u + r * VP];
-    if (NS > 1) {
+    if constexpr (NS > 1 && NS < 32) {  // few distinct twiddles per warp: table loads are broadcasts
 #pragma unroll
       for (int r = 1; r < RP; ++r) {
         V t = __ldg(tw + (r - 1) * NS + k);
         if (DIR > 0) t.y = -t.y;
         w[r] = cmul(w[r], t);
+      }
+    } else if constexpr (NS >= 32) {  // 32 distinct per warp: load t^1, t^2, t^4 and multiply out the rest
+      V t[RP];
+      t[1] = __ldg(tw + k);
+      if constexpr (RP > 2) t[2] = __ldg(tw + NS + k);
+      if constexpr (RP > 4) t[4] = __ldg(tw + 3 * NS + k);
+      if constexpr (RP > 2) t[3] = cmul(t[1], t[2]);
+      if constexpr (RP > 4) { t[5] = cmul(t[1], t[4]); t[6] = cmul(t[2], t[4]); t[7] = cmul(t[3], t[4]); }
+#pragma unroll
+      for (int r = 1; r < RP; ++r) {
+        if (DIR > 0) t[r].y = -t[r].y;
+        w[r] = cmul(w[r], t[r]);
       }
     }
     Dft<RP, DIR, V>::run(w);
@@ -167,13 +200,13 @@ __device__ __forceinline__ void stockham_pass(V (&v)[kR], const V* src, V* dst, 
       for (int r = 0; r < RP; ++r) v[u + r * VP] = w[r];
     } else {
       const int idxD = (vt / NS) * NS * RP + k;
-      if constexpr (NS % 8 == 0) {  // pad is additive over r NS: one base address
-        V* d0 = dst + pad<V>(idxD);
+      if constexpr (sw_additive<V>(NS)) {  // one base address
+        V* d0 = dst + sw<V, MOUT>(idxD);
 #pragma unroll
-        for (int r = 0; r < RP; ++r) d0[pad<V>(r * NS)] = w[r];
+        for (int r = 0; r < RP; ++r) d0[r * NS] = w[r];
       } else {
 #pragma unroll
-        for (int r = 0; r < RP; ++r) dst[pad<V>(idxD + r * NS)] = w[r];
+        for (int r = 0; r < RP; ++r) dst[sw<V, MOUT>(idxD + r * NS)] = w[r];
       }
     }
   }
@@ -186,7 +219,8 @@ __device__ __forceinline__ V* fft_passes(V (&v)[kR], V* rd, V* wr, const V* __re
   constexpr int P = sched_passes(NC);
   constexpr int RP = sched_radix(NC, p), NS = sched_ns(NC, p);
   constexpr bool LAST = (p == P - 1);
-  stockham_pass<V, NC, RP, NS, DIR, FROM_REGS, LAST>(v, rd, wr, tw + sched_twoff(NC, p), j);
+  stockham_pass<V, NC, RP, NS, DIR, FROM_REGS, LAST, (p > 0 ? sw_mode_out(p - 1) : 0), sw_mode_out(p)>(
+      v, rd, wr, tw + sched_twoff(NC, p), j);
   if constexpr (!LAST) {
     __syncthreads();
     return fft_passes<V, NC, DIR, p + 1, false>(v, wr, rd, tw, j, wr);
@@ -209,6 +243,31 @@ __device__ __forceinline__ void block_sum(S (&v)[M], S* red, int j) {
 #pragma unroll
     for (int i = 0; i < M; ++i) red[(j >> 5) * M + i] = v[i];
   __syncthreads();
+#pragma unroll
+  for (int i = 0; i < M; ++i) v[i] = lane < NW ? red[lane * M + i] : (S)0;
+#pragma unroll
+  for (int o = NW / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+#pragma unroll
+  for (int i = 0; i < M; ++i) v[i] = __shfl_sync(0xffffffffu, v[i], 0);
+}
+
+// The same reduction split in two halves around a barrier the caller already has:
+// warp_sum (all lanes get the warp total; lane 0 publishes it) ... __syncthreads() ... block_collect.
+template <int M, typename S>
+__device__ __forceinline__ void warp_publish(S (&v)[M], S* red, int j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  if ((j & 31) == 0)
+#pragma unroll
+    for (int i = 0; i < M; ++i) red[(j >> 5) * M + i] = v[i];
+}
+template <int NW, int M, typename S>
+__device__ __forceinline__ void block_collect(S (&v)[M], const S* red, int j) {
+  const int lane = j & 31;
 #pragma unroll
   for (int i = 0; i < M; ++i) v[i] = lane < NW ? red[lane * M + i] : (S)0;
 #pragma unroll
@@ -279,7 +338,7 @@ struct Resident {
   static constexpr int G = NC / 4;  // radix-4 group stride
   static constexpr int NW = T / 32;
   static constexpr int P = sched_passes(NC);
-  static constexpr int PADN = padded_len<V>(NC);
+  static constexpr int PADN = NC;  // exchange buffer length (swizzled, no padding)
   static_assert(T >= 32 && T % 32 == 0, "need at least one full warp");
   static_assert((NC & (NC - 1)) == 0, "power-of-two NC");
 
@@ -291,7 +350,7 @@ struct Resident {
   static constexpr size_t off_red = off_isin + sizeof(Real) * ((NC + 2) & ~1);  // 2 slots x 4*NW doubles
   static constexpr size_t off_nbr = off_red + sizeof(double) * 8 * NW;         // NW*R V
   static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // 2 NW + 8 ints
-  static constexpr size_t smem_bytes = off_int + sizeof(int) * (2 * NW + 8);
+  static constexpr size_t smem_bytes = off_int + sizeof(int) * (4 * NW + 8);
 
   struct Smem {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
@@ -313,21 +372,97 @@ struct Resident {
   }
   __device__ static bool is_zero(float d) { return ((unsigned)__float_as_int(d) & 0x7fffffffu) == 0u; }
 
+  // One barrier: warp-interior tests are counted before it; the 8 NW boundary tests between
+  // lane 31 of warp b and the next pair (lane 0 of warp b+1, or thread 0 / q+1 after the last
+  // warp) are recomputed identically by every warp after it from values published in smem.
   __device__ static int extrema(const V (&rt)[R], const Smem& sm, V*& last, int j) {
+#if FIF_EXT1 == 0
+    return extrema2(rt, sm, last, j);
+#endif
     const int lane = j & 31, w = j >> 5;
     unsigned S0 = 0, S1 = 0;   // sign bits of D_{2m} and D_{2m+1}, bit q
     bool zero = false;
-    Real xn[R];                // x_{2m+2}: first sample of the next pair
-#pragma unroll
-    for (int q = 0; q < R; ++q) xn[q] = __shfl_down_sync(0xffffffffu, rt[q].x, 1);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const Real d0 = rt[q].y - rt[q].x;  // D_{2m}
       S0 |= sgn_bit(d0) << q;
       zero |= is_zero(d0);
     }
-    unsigned S2 = __shfl_down_sync(0xffffffffu, S0, 1);  // sign bits of D_{2m+2} (next pair's D_{2m})
-    int* nmask = sm.ired + NW + 1;                      // [NW] masks of lane 0 of each warp
+    const unsigned S2 = __shfl_down_sync(0xffffffffu, S0, 1);  // sign bits of D_{2m+2}
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const Real xn = __shfl_down_sync(0xffffffffu, rt[q].x, 1);  // x_{2m+2}
+      const Real d1 = xn - rt[q].y;                              // D_{2m+1} (lanes 0..30)
+      S1 |= sgn_bit(d1) << q;
+      zero |= (lane < 31) && is_zero(d1);
+    }
+    int cnt = (lane < 31) ? __popc(S0 ^ S1) + __popc(S1 ^ S2) : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    int* wcnt = sm.ired + NW + 1;     // [NW] warp-interior counts
+    int* m0 = wcnt + NW;              // [NW] S0 of lane 0
+    int* m31 = m0 + NW;               // [NW] S0 of lane 31
+    if (lane == 0) {
+      wcnt[w] = cnt;
+      m0[w] = (int)S0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) sm.nbr[w * R + q].x = rt[q].x;   // x_{2m} of lane 0
+    }
+    if (lane == 31) {
+      m31[w] = (int)S0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) sm.nbr[w * R + q].y = rt[q].y;   // x_{2m+1} of lane 31
+    }
+    const int anyzero0 = __syncthreads_or(zero);
+    // boundary tests t = b*R + q, b = warp, handled 2 per lane (NW*R <= 64 for T <= 256; loop otherwise)
+    int bcnt = 0;
+    bool bzero = false;
+    for (int t = lane; t < NW * R; t += 32) {
+      const int b = t / R, q = t % R;
+      Real xnext;
+      unsigned s2;
+      bool has = true;
+      if (b + 1 < NW) {
+        xnext = sm.nbr[(b + 1) * R + q].x;
+        s2 = ((unsigned)m0[b + 1] >> q) & 1u;
+      } else if (q + 1 < R) {
+        xnext = sm.nbr[q + 1].x;
+        s2 = ((unsigned)m0[0] >> (q + 1)) & 1u;
+      } else {
+        has = false;  // pair NC-1: no successor
+        xnext = (Real)0;
+        s2 = 0;
+      }
+      if (has) {
+        const Real d1 = xnext - sm.nbr[b * R + q].y;
+        const unsigned s1 = sgn_bit(d1), s0 = ((unsigned)m31[b] >> q) & 1u;
+        bcnt += (int)(s0 != s1) + (int)(s1 != s2);
+        bzero |= is_zero(d1);
+      }
+    }
+    bcnt = __reduce_add_sync(0xffffffffu, bcnt);
+    const bool anyzero = anyzero0 || __any_sync(0xffffffffu, bzero);
+    int total = bcnt;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) total += wcnt[ww];
+    if (anyzero) total = extrema_exact(rt, sm, last, j);
+    return total;
+  }
+
+  __device__ static int extrema2(const V (&rt)[R], const Smem& sm, V*& last, int j) {
+    const int lane = j & 31, w = j >> 5;
+    unsigned S0 = 0, S1 = 0;
+    bool zero = false;
+    Real xn[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) xn[q] = __shfl_down_sync(0xffffffffu, rt[q].x, 1);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const Real d0 = rt[q].y - rt[q].x;
+      S0 |= sgn_bit(d0) << q;
+      zero |= is_zero(d0);
+    }
+    unsigned S2 = __shfl_down_sync(0xffffffffu, S0, 1);
+    int* nmask = sm.ired + NW + 1;
     if (lane == 0) {
 #pragma unroll
       for (int q = 0; q < R; ++q) sm.nbr[w * R + q].x = rt[q].x;
@@ -339,16 +474,16 @@ struct Resident {
 #pragma unroll
         for (int q = 0; q < R; ++q) xn[q] = sm.nbr[(w + 1) * R + q].x;
         S2 = (unsigned)nmask[w + 1];
-      } else {  // thread T-1: pair m = T-1 + T q is followed by pair T (q+1) of thread 0
+      } else {
 #pragma unroll
         for (int q = 0; q < R - 1; ++q) xn[q] = sm.nbr[q + 1].x;
         S2 = (unsigned)nmask[0] >> 1;
       }
     }
-    const unsigned valid = (j == T - 1) ? ((1u << (R - 1)) - 1u) : ((1u << R) - 1u);  // pair NC-1 has no successor
+    const unsigned valid = (j == T - 1) ? ((1u << (R - 1)) - 1u) : ((1u << R) - 1u);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const Real d1 = xn[q] - rt[q].y;  // D_{2m+1}
+      const Real d1 = xn[q] - rt[q].y;
       S1 |= sgn_bit(d1) << q;
       zero |= ((valid >> q) & 1u) && is_zero(d1);
     }
@@ -368,16 +503,16 @@ struct Resident {
   __device__ static int extrema_exact(const V (&rt)[R], const Smem& sm, V*& last, int j) {
     V* buf = (last == sm.bufA) ? sm.bufB : sm.bufA;
 #pragma unroll
-    for (int q = 0; q < R; ++q) buf[pad<V>(j + T * q)] = rt[q];
+    for (int q = 0; q < R; ++q) buf[sw<V>(j + T * q)] = rt[q];
     last = buf;
     __syncthreads();
     if (j < 32) {
       constexpr int CH = NC / 32;  // pairs per lane
       int first = 0, lastsg = 0, c = 0;
       const int m0 = j * CH;
-      Real prev = buf[pad<V>(m0)].x;
+      Real prev = buf[sw<V>(m0)].x;
       for (int p = 2 * m0 + 1; p <= 2 * (m0 + CH) && p < n; ++p) {
-        const V pr = buf[pad<V>(p >> 1)];
+        const V pr = buf[sw<V>(p >> 1)];
         const Real x = (p & 1) ? pr.y : pr.x;
         const Real d = x - prev;
         prev = x;
@@ -441,6 +576,49 @@ struct Resident {
     if (q == 0 && j == 0) return 1.0;  // bin 0: w_hat_0 = 1 (rows sum to 1)
     return (double)what(sm, L, invL, bin_of(j, q));
   }
+  // signed sin(pi m / n), cos(pi m / n) for any integer m (table holds sin(pi r/n), 0 <= r <= n/2)
+  __device__ static Real ssin(const Smem& sm, unsigned m) {
+    m &= (unsigned)(2 * n - 1);
+    const bool neg = m >= (unsigned)n;
+    if (neg) m -= (unsigned)n;
+    const unsigned r = min(m, (unsigned)n - m);
+    const Real v = sm.sint[r];
+    return neg ? -v : v;
+  }
+  __device__ static Real scos(const Smem& sm, unsigned m) { return ssin(sm, m + (unsigned)(n / 2)); }
+  // w_hat for all NB bins of the thread (group layout + Nyquist).  The numerators
+  // sin(pi L k/n) of the 8 group bins k = g + q n/8 share one angle A = pi L g/n and the
+  // block-uniform step B = pi L/8: sin(A + qB) = sA cos qB + cA sin qB (group 1) and
+  // sin((q+1)B - A) (group 2, g2 = n/8 - j), so only (sA, cA) are per-thread table gathers.
+  __device__ static void bin_w_all(const Smem& sm, int L, Real invL, int j, double (&w)[NB]) {
+    Real cq[5], sq[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {  // qB = pi (qL mod 16) (n/8) / n: uniform addresses (broadcasts)
+      const unsigned m = ((unsigned)(q * L) & 15u) * (unsigned)(n / 8);
+      sq[q] = ssin(sm, m);
+      cq[q] = scos(sm, m);
+    }
+    const unsigned mA = (unsigned)L * (unsigned)j;
+    const Real sA = ssin(sm, mA), cA = scos(sm, mA);
+    Real sA2 = sA, cA2 = cA;
+    if (j == 0) {  // g2 = n/16: angle (q + 1/2) B = (q+1)B - B/2
+      const unsigned mh = ((unsigned)L & 31u) * (unsigned)(n / 16);
+      sA2 = ssin(sm, mh);
+      cA2 = scos(sm, mh);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const Real n1 = sA * cq[q] + cA * sq[q];              // sin(A + qB)
+      const Real n2 = sq[q + 1] * cA2 - cq[q + 1] * sA2;    // sin((q+1)B - A2)
+      const Real s1 = n1 * sm.isin[bin_of(j, q)] * invL;
+      const Real s2 = n2 * sm.isin[bin_of(j, q + 4)] * invL;
+      const Real t1 = s1 * s1, t2 = s2 * s2;
+      w[q] = (double)(t1 * t1);
+      w[q + 4] = (double)(t2 * t2);
+    }
+    if (j == 0) w[0] = 1.0;  // bin 0: w_hat_0 = 1 (rows sum to 1)
+    w[R] = (double)what(sm, L, invL, NC);
+  }
   __device__ static double bin_p1(const V (&X)[R], const V& Xn, int j, int q) {
     if (q == R) return (j == 0) ? 0.5 * ((double)Xn.x * (double)Xn.x) : 0.0;  // X_NC real, weight 1
     const double p = (double)X[q].x * (double)X[q].x + (double)X[q].y * (double)X[q].y;
@@ -451,7 +629,18 @@ struct Resident {
   template <int ECT = -1>
   __device__ static void probe(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N, double& P,
                                double& Q, double (&d)[NB], double* red, int j) {
-    double v[2] = {0.0, 0.0};
+    double v[2];
+    probe_part<ECT>(X, Xn, sm, L, invL, N, v, d, j);
+    block_sum<NW, 2>(v, red, j);
+    P = v[0]; Q = v[1];
+  }
+  // the thread's share of (P, Q) (not reduced) and d_k = a_k^N
+  template <int ECT = -1>
+  __device__ static void probe_part(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N,
+                                    double (&v)[2], double (&d)[NB], int j) {
+    v[0] = 0.0; v[1] = 0.0;
+    double wall[NB];
+    bin_w_all(sm, L, invL, j, wall);
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
       constexpr int M = 5;
@@ -459,7 +648,7 @@ struct Resident {
 #pragma unroll
       for (int i = 0; i < M; ++i) {
         const int q = glo(g) + i;
-        w[i] = q < ghi(g) ? bin_w1(sm, L, invL, j, q) : 1.0;
+        w[i] = q < ghi(g) ? wall[q] : 1.0;
         a[i] = 1.0 - w[i];
       }
       if constexpr (ECT >= 0) upow_ct<ECT>(e, a); else upow<M>(e, a, N - 1);
@@ -475,8 +664,6 @@ struct Resident {
       }
     }
     v[0] *= 2.0; v[1] *= 2.0;
-    block_sum<NW, 2>(v, red, j);
-    P = v[0]; Q = v[1];
   }
 
   // fp32 hint for the minimal passing N in [1, hi] (bisection on fp32 sums, powers through the SFU:
@@ -486,9 +673,11 @@ struct Resident {
   __device__ static int hint_fp32(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int hi,
                                   float delta2, float* red, int j) {
     float l2[NB], pk[NB], pw[NB];
+    double wall[NB];
+    bin_w_all(sm, L, invL, j, wall);
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
-      const double w = bin_w1(sm, L, invL, j, q), p64 = bin_p1(X, Xn, j, q);
+      const double w = wall[q], p64 = bin_p1(X, Xn, j, q);
       l2[q] = fmaxf(2.0f * lg2f(fmaxf((float)(1.0 - w), 0.0f)), -1e30f);  // finite: 0 * l2 = 0 at N = 1
       pk[q] = (float)p64;
       pw[q] = (float)(p64 * w * w);
@@ -514,6 +703,8 @@ struct Resident {
   __device__ static void verify(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N,
                                 double delta2, bool& pass_lo, bool& pass_hi, double (&d)[NB], double* red, int j) {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
+    double wall[NB];
+    bin_w_all(sm, L, invL, j, wall);
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
       constexpr int M = 5;
@@ -521,7 +712,7 @@ struct Resident {
 #pragma unroll
       for (int i = 0; i < M; ++i) {
         const int q = glo(g) + i;
-        w[i] = q < ghi(g) ? bin_w1(sm, L, invL, j, q) : 1.0;
+        w[i] = q < ghi(g) ? wall[q] : 1.0;
         a[i] = 1.0 - w[i];
       }
       upow<M>(e, a, N > 1 ? N - 2 : 0);  // a^(N-2)
@@ -546,6 +737,36 @@ struct Resident {
     pass_hi = v[3] <= delta2 * v[2];
   }
 
+  // Minimal passing N in [1, cap - 1] when pass(cap) is known: fp32 hint, fp64 verification
+  // (+ fp64 bisection fallback).  Returns N and d_k = a_k^N.
+  __device__ static int search_below_cap(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL,
+                                         const Params& p, double (&dd)[NB], int& slot, int j) {
+    const int cap = p.max_inner;
+    double* red = sm.red + slot * 4 * NW;
+    slot ^= 1;
+    const int Nh = hint_fp32(X, Xn, sm, L, invL, cap, (float)p.delta2, reinterpret_cast<float*>(red), j);
+    red = sm.red + slot * 4 * NW;
+    slot ^= 1;
+    bool plo, phi;
+    verify(X, Xn, sm, L, invL, Nh, p.delta2, plo, phi, dd, red, j);
+    if (phi && !plo) return Nh;
+    int lo = phi ? 0 : Nh, hi = phi ? Nh - 1 : cap;  // pass(hi) known, !pass(lo) (lo = 0 virtual)
+    double Pv, Qv;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      red = sm.red + slot * 4 * NW;
+      slot ^= 1;
+      probe(X, Xn, sm, L, invL, mid, Pv, Qv, dd, red, j);
+      if (Qv <= p.delta2 * Pv) hi = mid; else lo = mid;
+    }
+    red = sm.red + slot * 4 * NW;
+    slot ^= 1;
+    probe(X, Xn, sm, L, invL, hi, Pv, Qv, dd, red, j);  // d = a^N
+    return hi;
+  }
+
+  // Full search (cap probe first); used by the test hook.  The decomposition loop inlines the cap
+  // probe speculatively (decompose_one).
   __device__ static int search(const V (&X)[R], const V& Xn, const Smem& sm, int L, const Params& p, Real (&d)[R],
                                Real& dn, int& slot, int j) {
     const Real invL = (Real)1 / (Real)L;
@@ -556,33 +777,7 @@ struct Resident {
     if constexpr (CAP > 0) probe<CAP - 1>(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
     else probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
     int N = cap;
-    if (Qv <= p.delta2 * Pv) {
-      // the minimal passing N lies in [1, cap]: fp32 hint, fp64 verification (+ fp64 bisection fallback)
-      red = sm.red + slot * 4 * NW;
-      slot ^= 1;
-      const int Nh = hint_fp32(X, Xn, sm, L, invL, cap, (float)p.delta2, reinterpret_cast<float*>(red), j);
-      red = sm.red + slot * 4 * NW;
-      slot ^= 1;
-      bool plo, phi;
-      verify(X, Xn, sm, L, invL, Nh, p.delta2, plo, phi, dd, red, j);
-      if (phi && !plo) {
-        N = Nh;
-      } else {
-        int lo = phi ? 0 : Nh, hi = phi ? Nh - 1 : cap;  // pass(hi) known, !pass(lo) (lo = 0 virtual)
-        if (phi && hi == 0) hi = 1;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          red = sm.red + slot * 4 * NW;
-          slot ^= 1;
-          probe(X, Xn, sm, L, invL, mid, Pv, Qv, dd, red, j);
-          if (Qv <= p.delta2 * Pv) hi = mid; else lo = mid;
-        }
-        N = hi;
-        red = sm.red + slot * 4 * NW;
-        slot ^= 1;
-        probe(X, Xn, sm, L, invL, N, Pv, Qv, dd, red, j);  // d = a^N
-      }
-    }
+    if (Qv <= p.delta2 * Pv) N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
 #pragma unroll
     for (int q = 0; q < R; ++q) d[q] = (Real)dd[q];
     dn = (Real)dd[R];
@@ -618,22 +813,22 @@ struct Resident {
     V* lw = fft_passes<V, NC, -1, 0, true>(v, rd, wr, tw, j, wr);
     V* zb = (lw == sm.bufA) ? sm.bufB : sm.bufA;  // Z -> the buffer not written last
 #pragma unroll
-    for (int q = 0; q < R; ++q) zb[pad<V>(j + T * q)] = v[q];
+    for (int q = 0; q < R; ++q) zb[sw<V>(j + T * q)] = v[q];
     last = zb;
     __syncthreads();
     const Real h = (Real)0.5;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int k = bin_of(j, q);
-      const V Pz = zb[pad<V>(k)];
-      const V Qz = zb[pad<V>((NC - k) & (NC - 1))];
+      const V Pz = zb[sw<V>(k)];
+      const V Qz = zb[sw<V>((NC - k) & (NC - 1))];
       const V E = V{h * (Pz.x + Qz.x), h * (Pz.y - Qz.y)};  // (P + Q*)/2
       const V D = V{h * (Pz.x - Qz.x), h * (Pz.y + Qz.y)};  // (P - Q*)/2
       const V O = V{D.y, -D.x};                             // D / i
       X[q] = cadd(E, cmul(wfwd(sm, k), O));
     }
     if (j == 0) {
-      const V Z0 = zb[pad<V>(0)];
+      const V Z0 = zb[sw<V>(0)];
       Xn = V{Z0.x - Z0.y, (Real)0};
       X[0] = V{Z0.x + Z0.y, (Real)0};
     }
@@ -643,6 +838,18 @@ struct Resident {
   // pairs in v (m = j + T q).  Pre-processing and the first radix-4 pass run in registers.
   __device__ static void irfft(V (&v)[R], const V& Dn, const Smem& sm, const V* __restrict__ tw, V*& last, int j) {
     // in place: v holds D on entry (group layout), time-domain pairs on exit
+    V* zb = (last == sm.bufA) ? sm.bufB : sm.bufA;
+    irfft_p0(v, Dn, sm, zb, j);
+    __syncthreads();
+    last = irfft_rest(v, sm, tw, zb, j);
+  }
+  // passes 1.. of the inverse (pass 0 output in zb, visible to all threads); returns the buffer written last
+  __device__ static V* irfft_rest(V (&v)[R], const Smem& sm, const V* __restrict__ tw, V* zb, int j) {
+    V* other = (zb == sm.bufA) ? sm.bufB : sm.bufA;
+    return fft_passes<V, NC, 1, 1, false>(v, zb, other, tw, j, zb);
+  }
+  // pre-processing (Hermitian pairs -> Z) and the first inverse radix-4 pass, in registers; stores to zb
+  __device__ static void irfft_p0(V (&v)[R], const V& Dn, const Smem& sm, V* zb, int j) {
     if (j != 0) {
       // pairs (g1 r, g2 3-r) = (q, 7-q); bins k = j + r G (r = 0, 1) are <= n/4: use them as "k",
       // for r = 2, 3 the mirror NC - k = g2 + (3-r) G is the one <= n/4.
@@ -669,18 +876,12 @@ struct Resident {
     // first inverse pass: radix 4, NS = 1 (no twiddles), groups g1, g2 -> y[4 g + r]
     dft4<1>(v[0], v[1], v[2], v[3]);
     dft4<1>(v[4], v[5], v[6], v[7]);
-    V* zb = (last == sm.bufA) ? sm.bufB : sm.bufA;
-    V* other = (zb == sm.bufA) ? sm.bufB : sm.bufA;
-    {
-      const int b1 = 4 * j, b2 = 4 * g2_of(j);
+    const int b1 = 4 * j, b2 = 4 * g2_of(j);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        zb[pad<V>(b1 + r)] = v[r];
-        zb[pad<V>(b2 + r)] = v[4 + r];
-      }
+    for (int r = 0; r < 4; ++r) {
+      zb[sw<V, sw_mode_out(0)>(b1 + r)] = v[r];
+      zb[sw<V, sw_mode_out(0)>(b2 + r)] = v[4 + r];
     }
-    __syncthreads();
-    last = fft_passes<V, NC, 1, 1, false>(v, zb, other, tw, j, zb);
   }
 
   // -------------------------------------------------------------- one signal, all IMFs
@@ -710,20 +911,75 @@ struct Resident {
     const Real invn = (Real)1 / (Real)n;
     while (M < p.max_imfs && k >= 2) {
       const int L = filter_half_length(p, k);
-      Real d[R], dn = 0;
-      const int N = search(X, Xn, sm, L, p, d, dn, slot, j);
-      // damping: D = d X / n (IMF spectrum), X <- (1 - d) X
+      const Real invL = (Real)1 / (Real)L;
+#if FIF_SPEC == 0
+      V v[R], Dn{0, 0};
+      int N;
+      {
+        Real d[R], dn = 0;
+        N = search(X, Xn, sm, L, p, d, dn, slot, j);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          v[q] = cscale(X[q], d[q] * invn);
+          X[q] = cscale(X[q], (Real)1 - d[q]);
+        }
+        if (j == 0) {
+          Dn = cscale(Xn, dn * invn);
+          Xn = cscale(Xn, (Real)1 - dn);
+        }
+        irfft(v, Dn, sm, tw, last, j);
+      }
+#else
+      // a5, speculative: the cap probe's block reduction is completed at the barrier that
+      // follows the first inverse pass, which already assumes N = cap (the common case); if
+      // SD(cap) <= delta the speculative work is dropped and X restored.
+      double part[2], dd[NB];
+      if constexpr (CAP > 0) probe_part<CAP - 1>(X, Xn, sm, L, invL, p.max_inner, part, dd, j);
+      else probe_part(X, Xn, sm, L, invL, p.max_inner, part, dd, j);
+      double* red = sm.red + slot * 4 * NW;
+      slot ^= 1;
+      warp_publish<2>(part, red, j);
+      V* stash = last;  // not read by anyone until the next write phase: holds X_old
+#pragma unroll
+      for (int q = 0; q < R; ++q) stash[j + T * q] = X[q];
+      const V Xn_old = Xn;
+      // a6 damping: D = d X / n (IMF spectrum), X <- (1 - d) X
       V v[R], Dn{0, 0};
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        v[q] = cscale(X[q], d[q] * invn);
-        X[q] = cscale(X[q], (Real)1 - d[q]);
+        v[q] = cscale(X[q], (Real)dd[q] * invn);
+        X[q] = cscale(X[q], (Real)1 - (Real)dd[q]);
       }
       if (j == 0) {
-        Dn = cscale(Xn, dn * invn);
-        Xn = cscale(Xn, (Real)1 - dn);
+        Dn = cscale(Xn, (Real)dd[R] * invn);
+        Xn = cscale(Xn, (Real)1 - (Real)dd[R]);
       }
-      irfft(v, Dn, sm, tw, last, j);
+      V* zb = (last == sm.bufA) ? sm.bufB : sm.bufA;
+      irfft_p0(v, Dn, sm, zb, j);
+      __syncthreads();
+      block_collect<NW, 2>(part, red, j);
+      int N = p.max_inner;
+      if (part[1] <= p.delta2 * part[0]) {
+        // rare: the minimal passing N is below the cap
+#pragma unroll
+        for (int q = 0; q < R; ++q) X[q] = stash[j + T * q];
+        Xn = Xn_old;
+        N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          v[q] = cscale(X[q], (Real)dd[q] * invn);
+          X[q] = cscale(X[q], (Real)1 - (Real)dd[q]);
+        }
+        if (j == 0) {
+          Dn = cscale(Xn, (Real)dd[R] * invn);
+          Xn = cscale(Xn, (Real)1 - (Real)dd[R]);
+        }
+        last = zb;
+        irfft(v, Dn, sm, tw, last, j);
+      } else {
+        last = irfft_rest(v, sm, tw, zb, j);
+      }
+#endif
       Real* o = out + (size_t)M * slot_stride;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
@@ -858,7 +1114,10 @@ __global__ void __launch_bounds__(NC / kR) fif_test_window_kernel(Real* __restri
   const int j = threadIdx.x;
   K::load_tables(sm, sintab, isintab, j);
   const Real invL = (Real)1 / (Real)L;
-  for (int k = j; k <= NC; k += K::T) out[k] = k == 0 ? (Real)1 : K::what(sm, L, invL, k);
+  double w[K::NB];
+  K::bin_w_all(sm, L, invL, j, w);
+  for (int q = 0; q < kR; ++q) out[K::bin_of(j, q)] = (Real)w[q];
+  if (j == 0) out[NC] = (Real)w[kR];
 }
 
 template <typename Real, int NC, int CAP>
