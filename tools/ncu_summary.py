@@ -41,8 +41,8 @@ for r in rows[2:]:
         if unit == "Mbyte": x *= 1e6
         elif unit == "Gbyte": x *= 1e9
         elif unit == "Kbyte": x *= 1e3
-        elif unit == "msecond" and k == "duration_us": x *= 1e3
-        elif unit == "nsecond" and k == "duration_us": x *= 1e-3
+        elif unit in ("msecond", "ms") and k == "duration_us": x *= 1e3
+        elif unit in ("nsecond", "ns") and k == "duration_us": x *= 1e-3
         e[k] = x
     if "dram_read_bytes" in e and "dram_write_bytes" in e:
         e["dram_bytes"] = e["dram_read_bytes"] + e["dram_write_bytes"]
