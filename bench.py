@@ -135,6 +135,23 @@ def cpu_baseline(cfg, n, delta, budget_s=12.0, max_signals=256):
                       f"{t_total:.1f} s on {ncores} host threads"}
 
 
+def rank_start(rank: int, per_rank: int) -> int:
+    """Weak scaling: rank r decomposes signals [r*B, (r+1)*B) of the generator stream (no data-path collective)."""
+    return rank * per_rank
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """Max of a per-rank time over all ranks (the step time of the whole job)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -188,7 +205,7 @@ def main():
     from paper_1802_01359_b200 import fif, signals
 
     n, B, delta = workload(args.config, args.batch)
-    s_host = signals.make_batch(args.config, batch=B, start=rank * B)
+    s_host = signals.make_batch(args.config, batch=B, start=rank_start(rank, B))
     x = torch.from_numpy(s_host).cuda()
     plan = fif.Plan(n, B, "f64", delta=delta)
     imfs, count, lens, iters = plan.alloc_outputs()
@@ -217,10 +234,7 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, "cuda")
 
     # roofline (dominant kernel = the single resident kernel: its launch duration = the step)
     cnt = count.cpu().numpy()
@@ -256,11 +270,7 @@ def main():
             plan.decompose_host(hs, *h_out, stream=stream)
         e3.record(stream)
         torch.cuda.synchronize()
-        ems = e2.elapsed_time(e3) / ksteps
-        if world > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(e2.elapsed_time(e3) / ksteps, world, "cuda")
         h2d = hs.numel() * hs.element_size()
         d2h = sum(t.numel() * t.element_size() for t in h_out)
         e2e = {"value": samples / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
