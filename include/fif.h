@@ -50,10 +50,17 @@ typedef enum {
   FIF_ERR_NCCL = 5           /* reserved for the distributed plan */
 } fif_status;
 
+typedef enum {
+  FIF_REGIME_AUTO = 0,      /* resident when n fits on chip, streamed otherwise */
+  FIF_REGIME_RESIDENT = 1,  /* one CTA per signal, r and r_hat on chip for all IMFs (power-of-two 512 <= n <= 8192) */
+  FIF_REGIME_STREAMED = 2   /* spectrum / work buffers in HBM, four-step FFT, one kernel sequence per IMF */
+} fif_regime;
+
 /* Create a plan for `batch` independent signals of length n.
- *   n          : samples per signal.  This build supports powers of two
- *                512 <= n <= 8192 (f64 and f32) -- the on-chip resident regime;
- *                other n -> FIF_ERR_UNSUPPORTED_N.
+ *   n          : samples per signal, even.  Resident regime: powers of two 512 <= n <= 8192.
+ *                Streamed regime: n/2 = N1 N2 with N1, N2 of the form 2^a 3^b 5^c, N2 <= 2048 (f64) /
+ *                4096 (f32), N1 <= 1024 -- e.g. every 2^a 3^b 5^c up to n = 2^22 (f64) / 2^23 (f32).
+ *                Other n -> FIF_ERR_UNSUPPORTED_N.
  *   batch      : number of signals, >= 0 (0 is a valid no-op plan).
  *   dtype      : element type of signals and IMFs.  f32 computes the FFTs in fp32 and
  *                accumulates the stopping sums and takes the floor in fp64 (reading A14).
@@ -62,9 +69,14 @@ typedef enum {
  *   max_inner  : iteration cap (>= 1).
  *   max_imfs   : cap on the number of IMFs (>= 1).
  * Allocates small device tables (sin table and FFT twiddles, O(n) bytes) on the
- * current device and uploads them synchronously.  On error *out is NULL. */
+ * current device and uploads them synchronously; a streamed plan also allocates its work
+ * buffers (2 batch n/2 complex + O(batch) control).  On error *out is NULL. */
 fif_status fif_plan_create(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window, double xi,
                            double delta, int32_t max_inner, int32_t max_imfs);
+/* Same, forcing a regime (FIF_REGIME_AUTO = fif_plan_create).  Both regimes compute the same
+ * decomposition; forcing the streamed one at small n is used to test it against the oracle. */
+fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window,
+                              double xi, double delta, int32_t max_inner, int32_t max_imfs, fif_regime regime);
 
 /* Decompose the batch (device pointers, caller-owned, current device):
  *   d_signals    [batch][n] dtype, read only.
@@ -96,7 +108,7 @@ fif_status fif_destroy(fif_plan_t plan);
 const char* fif_status_string(fif_status s);
 
 /* Plan introspection: number of kernels one fif_decompose launches, the regime name
- * ("resident"), and the resident kernel's grid / block / dynamic smem. */
+ * ("resident" / "streamed"), and the main kernel's grid / block / dynamic smem. */
 int32_t fif_plan_kernels_per_call(fif_plan_t plan);
 const char* fif_plan_regime(fif_plan_t plan);
 fif_status fif_plan_launch_config(fif_plan_t plan, int32_t* grid, int32_t* block, int32_t* smem_bytes);

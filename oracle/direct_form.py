@@ -91,10 +91,15 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
     r = s.copy()
     imfs = np.zeros((max_imfs + 1, n))
     ls, Ns, ks, sds = [], [], [], []
+    scale, snorm = float(np.abs(s).max()), float(np.linalg.norm(s))
+    margins = np.full((max_imfs + 1, 2), np.nan)  # same definitions as fif_oracle.c
     M = 0
     while M < max_imfs:
         k = count_extrema(r)
         ks.append(k)
+        dd = np.abs(np.diff(r))
+        dd = dd[dd > 0]
+        margins[M, 0] = (dd.min() / scale) if (dd.size and scale > 0) else np.inf
         if k < 2:
             break
         L = filter_half_length(xi, n, k, window)
@@ -109,11 +114,41 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
         ls.append(2 * L)
         Ns.append(N)
         sds.append((curve[N - 1], curve[N - 2] if N > 1 else float("nan")))
+        # iterate norms ||(I-W)^{N-1} r|| (Parseval: sum_k c_k |a^{N-1} r_k|^2 = n ||.||^2)
+        cw = np.full(lam.shape, 2.0)
+        cw[0] = 1.0
+        if n % 2 == 0:
+            cw[-1] = 1.0
+        a = np.clip(1.0 - lam, 0.0, 1.0)
+        def itn(m):
+            return math.sqrt(float(np.sum(cw * np.abs(a ** m * rhat) ** 2)) / n)
+        sm = abs(curve[N - 1] - delta) / delta * (itn(N - 1) / snorm if snorm > 0 else 1.0)
+        if N > 1:
+            sm = min(sm, abs(curve[N - 2] - delta) / delta * (itn(N - 2) / snorm if snorm > 0 else 1.0))
+        margins[M, 1] = sm
         M += 1
     if M == max_imfs:
         ks.append(count_extrema(r))
     imfs[M] = r
-    return {"imfs": imfs, "M": M, "l": ls, "N": Ns, "k": ks, "sd": sds}
+    return {"imfs": imfs, "M": M, "l": ls, "N": Ns, "k": ks, "sd": sds, "margins": margins}
+
+
+def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ):
+    """CPU-DF over a batch, returned in the TD oracle's dict layout (imfs, count, l, N, margins)."""
+    S = np.atleast_2d(np.asarray(signals, dtype=np.float64))
+    B, n = S.shape
+    out = {"imfs": np.zeros((B, max_imfs + 1, n)), "count": np.zeros(B, np.int32),
+           "l": np.zeros((B, max_imfs), np.int32), "N": np.zeros((B, max_imfs), np.int32),
+           "margins": np.full((B, max_imfs + 1, 2), np.nan)}
+    for b in range(B):
+        d = decompose(S[b], xi, delta, max_inner, max_imfs, window)
+        M = d["M"]
+        out["imfs"][b] = d["imfs"]
+        out["count"][b] = M
+        out["l"][b, :M] = d["l"]
+        out["N"][b, :M] = d["N"]
+        out["margins"][b] = d["margins"]
+    return out
 
 
 def damping(lam: np.ndarray, N: int) -> np.ndarray:

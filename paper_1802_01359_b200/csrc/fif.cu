@@ -12,6 +12,7 @@
 
 #include "../../include/fif.h"
 #include "fif_resident.cuh"
+#include "fif_streamed.cuh"
 
 using namespace fifgpu;
 
@@ -45,6 +46,18 @@ struct fif_plan_s {
   void* d_tw = nullptr;    // V[twtotal]  Stockham twiddles e^{-2 pi i k r/(NS RP)}
   int block = 0, occ = 0;
   size_t smem = 0;
+  int regime = 0;  // 0 resident, 1 streamed
+  // streamed regime
+  st::Geo geo{};
+  void* d_tw1 = nullptr;  // V[N1] e^{-2 pi i j/N1}
+  void* d_tw2 = nullptr;  // V[N2]
+  void* d_X = nullptr;    // V[B][NC] spectrum (transposed four-step order)
+  void* d_Xn = nullptr;   // V[B] Nyquist bins
+  void* d_Z = nullptr;    // V[B][NC] FFT work buffer
+  void* d_ctl = nullptr;  // per-signal control arrays + partials
+  st::Ctl ctl{};
+  int st_rounds = 0, st_grid = 0;
+  size_t st_smem_cols = 0, st_smem_rows = 0;
   // host (e2e) path staging
   int64_t chunk = 0;
   int nstages = 0;
@@ -213,11 +226,164 @@ fif_status launch_status() {
   return FIF_OK;
 }
 
+
+// ---------------------------------------------------------------- streamed regime (fif_streamed.cuh)
+bool smooth235(int64_t x) {
+  if (x < 1) return false;
+  for (int f : {2, 3, 5})
+    while (x % f == 0) x /= f;
+  return x == 1;
+}
+// radix schedule: 8s, then the leftover power of two (4 or 2), then 3s and 5s
+int radices(int64_t N, int* rad) {
+  int np = 0, a = 0;
+  while (N % 2 == 0) { N /= 2; ++a; }
+  while (a >= 3) { rad[np++] = 8; a -= 3; }
+  if (a == 2) rad[np++] = 4;
+  if (a == 1) rad[np++] = 2;
+  while (N % 3 == 0) { N /= 3; rad[np++] = 3; }
+  while (N % 5 == 0) { N /= 5; rad[np++] = 5; }
+  return np;
+}
+template <typename Real>
+void host_twiddles(int N, std::vector<typename Cx<Real>::V>& tw) {
+  const long double PI = 3.141592653589793238462643383279502884L;
+  tw.resize(N);
+  for (int j = 0; j < N; ++j) {
+    const long double th = 2.0L * PI * (long double)j / (long double)N;
+    tw[j] = typename Cx<Real>::V{(Real)cosl(th), (Real)(-sinl(th))};
+  }
+}
+// N1 * N2 = NC with both 2^a 3^b 5^c, N2 <= n2max (row FFT in smem), N1 <= n1max (column tiles)
+bool st_factor(int64_t NC, int64_t n2max, int64_t n1max, int& N1, int& N2) {
+  for (int64_t d = n2max; d >= 1; --d) {
+    if (NC % d) continue;
+    const int64_t q = NC / d;
+    if (q > n1max || !smooth235(d) || !smooth235(q)) continue;
+    N2 = (int)d; N1 = (int)q;
+    return true;
+  }
+  return false;
+}
+template <typename Real>
+fif_status st_setup(fif_plan_s* p) {
+  using V = typename Cx<Real>::V;
+  st::Geo& g = p->geo;
+  const int64_t tile = sizeof(Real) == 8 ? 2048 : 4096;  // complex elements per smem buffer
+  g.n = p->n; g.NC = p->n / 2; g.batch = p->batch;
+  if (!st_factor(g.NC, tile, 1024, g.N1, g.N2)) return FIF_ERR_UNSUPPORTED_N;
+  int cmax = (int)(tile / g.N1);
+  if (cmax > g.N2) cmax = g.N2;
+  g.C = 1;
+  for (int c = cmax; c >= 1; --c)
+    if (g.N2 % c == 0) { g.C = c; break; }
+  g.np1 = radices(g.N1, g.rad1);
+  g.np2 = radices(g.N2, g.rad2);
+  g.binch = 8192;
+  g.nbch = (int)((g.NC + g.binch - 1) / g.binch);
+  g.smpch = 16384;
+  g.nsch = (int)((g.n - 1 + g.smpch - 1) / g.smpch);
+  g.max_imfs = p->max_imfs; g.max_inner = p->max_inner; g.window = (int)p->window;
+  g.xi = p->xi; g.delta2 = p->delta * p->delta;
+  // K-ary rounds: the bracket shrinks from cap to ceil(len / (kProbes + 1)) per round
+  p->st_rounds = 0;
+  for (int64_t len = p->max_inner; len > 1; len = (len + st::kProbes) / (st::kProbes + 1)) ++p->st_rounds;
+  p->st_grid = p->num_sms * 8;
+  std::vector<V> t1, t2;
+  host_twiddles<Real>(g.N1, t1);
+  host_twiddles<Real>(g.N2, t2);
+  const int64_t B = p->batch > 0 ? p->batch : 1;
+  if (cudaMalloc(&p->d_tw1, sizeof(V) * t1.size()) != cudaSuccess ||
+      cudaMalloc(&p->d_tw2, sizeof(V) * t2.size()) != cudaSuccess ||
+      cudaMalloc(&p->d_X, sizeof(V) * B * g.NC) != cudaSuccess || cudaMalloc(&p->d_Xn, sizeof(V) * B) != cudaSuccess ||
+      cudaMalloc(&p->d_Z, sizeof(V) * B * g.NC) != cudaSuccess)
+    return FIF_ERR_OOM;
+  const size_t nint = (size_t)B * (9 + 3 * g.nsch);
+  const size_t ctl_bytes = nint * sizeof(int32_t) + 16 + sizeof(double) * (size_t)B * g.nbch * 2 * st::kProbes;
+  if (cudaMalloc(&p->d_ctl, ctl_bytes) != cudaSuccess) return FIF_ERR_OOM;
+  int32_t* ip = (int32_t*)p->d_ctl;
+  st::Ctl& c = p->ctl;
+  c.k = ip; c.L = ip + B; c.N = ip + 2 * B; c.M = ip + 3 * B; c.active = ip + 4 * B; c.search = ip + 5 * B;
+  c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.ext = ip + 9 * B;
+  c.red = (double*)(((uintptr_t)(ip + nint) + 15) & ~(uintptr_t)15);
+  if (cudaMemcpy(p->d_tw1, t1.data(), sizeof(V) * t1.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->d_tw2, t2.data(), sizeof(V) * t2.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return FIF_ERR_CUDA;
+  p->st_smem_cols = 2 * sizeof(V) * (size_t)g.N1 * g.C;
+  p->st_smem_rows = 2 * sizeof(V) * (size_t)g.N2;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(st::k_fwd_cols<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->st_smem_cols)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(st::k_inv_cols<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->st_smem_cols)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(st::k_rows<Real, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->st_smem_rows)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(st::k_rows<Real, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p->st_smem_rows)) != cudaSuccess) {
+    fprintf(stderr, "fif: streamed setup failed: %s\n", cudaGetErrorString(e));
+    return FIF_ERR_CUDA;
+  }
+  p->block = st::kThreads;
+  p->smem = p->st_smem_rows > p->st_smem_cols ? p->st_smem_rows : p->st_smem_cols;
+  p->occ = 1;
+  return FIF_OK;
+}
+
+// the whole decomposition as stream-ordered kernels (no host synchronisation)
+template <typename Real>
+void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its, int64_t batch,
+                  cudaStream_t s) {
+  using V = typename Cx<Real>::V;
+  st::Geo g = p->geo;
+  g.batch = batch;
+  const st::Ctl c = p->ctl;
+  const int G = p->st_grid, TB = st::kThreads;
+  const int64_t sig_stride = (int64_t)(g.max_imfs + 1) * g.n;
+  Real* out = (Real*)imfs;
+  Real* R = out + (int64_t)g.max_imfs * g.n;
+  V* X = (V*)p->d_X;
+  V* Xn = (V*)p->d_Xn;
+  V* Z = (V*)p->d_Z;
+  const V* tw1 = (const V*)p->d_tw1;
+  const V* tw2 = (const V*)p->d_tw2;
+  const int gsig = (int)((batch + TB - 1) / TB);
+  cudaMemsetAsync(c.bad, 0, sizeof(int32_t) * batch, s);
+  st::k_fwd_cols<Real><<<G, TB, p->st_smem_cols, s>>>(g, (const Real*)sig, R, Z, tw1, c, sig_stride);
+  st::k_rows<Real, -1><<<G, TB, p->st_smem_rows, s>>>(g, Z, tw2, c, 0);
+  st::k_fwd_post<Real><<<G, TB, 0, s>>>(g, Z, X, Xn);
+  for (int m = 0; m < g.max_imfs; ++m) {
+    st::k_ext<Real><<<G, TB, 0, s>>>(g, R, sig_stride, c, m == 0);
+    st::k_ctl_ext<<<gsig, TB, 0, s>>>(g, c, m == 0);
+    st::k_probe<Real><<<G, TB, 0, s>>>(g, X, Xn, c, 0);
+    st::k_ctl_probe<<<gsig, TB, 0, s>>>(g, c, 0);
+    for (int r = 0; r < p->st_rounds; ++r) {
+      st::k_probe<Real><<<G, TB, 0, s>>>(g, X, Xn, c, 1);
+      st::k_ctl_probe<<<gsig, TB, 0, s>>>(g, c, 1);
+    }
+    st::k_damp_pre<Real><<<G, TB, 0, s>>>(g, X, Xn, Z, c);
+    st::k_rows<Real, 1><<<G, TB, p->st_smem_rows, s>>>(g, Z, tw2, c, 1);
+    st::k_inv_cols<Real><<<G, TB, p->st_smem_cols, s>>>(g, Z, tw1, out, R, sig_stride, c);
+    st::k_ctl_done<<<gsig, TB, 0, s>>>(g, c, lens, its);
+  }
+  // the loop above exits after max_imfs IMFs; a signal stopped by k < 2 is inactive from then on.
+  // One more extrema pass would only matter for the k_out diagnostics, which the ABI does not export.
+  st::k_final<Real><<<G, TB, 0, s>>>(g, out, sig_stride, c, cnt, lens, its);
+}
+int st_kernels_per_call(const fif_plan_s* p) {
+  return 3 + p->max_imfs * (8 + 2 * p->st_rounds) + 1;
+}
+
 void free_plan(fif_plan_s* p) {
   if (!p) return;
   cudaFree(p->d_sin);
   cudaFree(p->d_isin);
   cudaFree(p->d_tw);
+  cudaFree(p->d_tw1);
+  cudaFree(p->d_tw2);
+  cudaFree(p->d_X);
+  cudaFree(p->d_Xn);
+  cudaFree(p->d_Z);
+  cudaFree(p->d_ctl);
   for (int i = 0; i < p->nstages; ++i) {
     cudaFree(p->st[i].d_in);
     cudaFree(p->st[i].d_out);
@@ -246,22 +412,47 @@ const char* fif_status_string(fif_status s) {
 
 fif_status fif_plan_create(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window, double xi,
                            double delta, int32_t max_inner, int32_t max_imfs) {
+  return fif_plan_create_ex(out, n, batch, dtype, window, xi, delta, max_inner, max_imfs, FIF_REGIME_AUTO);
+}
+
+fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window,
+                              double xi, double delta, int32_t max_inner, int32_t max_imfs, fif_regime regime) {
   if (!out) return FIF_ERR_INVALID_ARG;
   *out = nullptr;
   if (n < 9 || batch < 0 || !(xi > 0.0) || !isfinite(xi) || !(delta > 0.0) || !isfinite(delta) || max_inner < 1 ||
       max_imfs < 1 || (dtype != FIF_F64 && dtype != FIF_F32) ||
-      (window != FIF_WINDOW_TRI_SQ && window != FIF_WINDOW_TRI_SQ_WIDE))
+      (window != FIF_WINDOW_TRI_SQ && window != FIF_WINDOW_TRI_SQ_WIDE) ||
+      (regime != FIF_REGIME_AUTO && regime != FIF_REGIME_RESIDENT && regime != FIF_REGIME_STREAMED))
     return FIF_ERR_INVALID_ARG;
   if (n % 2 != 0) return FIF_ERR_UNSUPPORTED_N;
   const int64_t NC = n / 2;
-  if ((NC & (NC - 1)) != 0 || NC < 256 || NC > 4096) return FIF_ERR_UNSUPPORTED_N;
+  const bool resident_ok = (NC & (NC - 1)) == 0 && NC >= 256 && NC <= 4096;
+  int reg;
+  if (regime == FIF_REGIME_RESIDENT) {
+    if (!resident_ok) return FIF_ERR_UNSUPPORTED_N;
+    reg = 0;
+  } else if (regime == FIF_REGIME_STREAMED) {
+    reg = 1;
+  } else {
+    reg = resident_ok ? 0 : 1;
+  }
+  if (reg == 1) {  // host-side check of the streamed factorisation before any CUDA call
+    int N1, N2;
+    if (!st_factor(NC, dtype == FIF_F64 ? 2048 : 4096, 1024, N1, N2)) return FIF_ERR_UNSUPPORTED_N;
+  }
   fif_plan_s* p = new fif_plan_s();
   p->n = n; p->batch = batch; p->dtype = dtype; p->window = window; p->xi = xi; p->delta = delta;
-  p->max_inner = max_inner; p->max_imfs = max_imfs; p->NC = (int)NC;
+  p->max_inner = max_inner; p->max_imfs = max_imfs; p->NC = (int)(NC < (1 << 30) ? NC : 0); p->regime = reg;
   if (cudaGetDevice(&p->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
     free_plan(p);
     return FIF_ERR_CUDA;
+  }
+  if (reg == 1) {
+    fif_status st = dtype == FIF_F64 ? st_setup<double>(p) : st_setup<float>(p);
+    if (st != FIF_OK) { free_plan(p); return st; }
+    *out = p;
+    return FIF_OK;
   }
   fif_status st = dtype == FIF_F64 ? upload_tables<double>(p) : upload_tables<float>(p);
   if (st != FIF_OK) { free_plan(p); return st; }
@@ -289,6 +480,11 @@ fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int3
   if (!d_signals || !d_imfs || !d_imf_count || !d_filter_len || !d_iters) return FIF_ERR_INVALID_ARG;
   if (((uintptr_t)d_signals | (uintptr_t)d_imfs) & 15) return FIF_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  if (p->regime == 1) {
+    if (p->dtype == FIF_F64) st_decompose<double>(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
+    else st_decompose<float>(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
+    return launch_status();
+  }
   dispatch(p->dtype, p->NC, [&](auto inst) {
     using I = decltype(inst);
     I::decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
@@ -335,10 +531,15 @@ fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs,
     int32_t* d_len = S.d_meta + nb;
     int32_t* d_it = d_len + nb * p->max_imfs;
     cudaMemcpyAsync(S.d_in, (const char*)h_signals + b0 * in_sig, nb * in_sig, cudaMemcpyHostToDevice, S.stream);
-    dispatch(p->dtype, p->NC, [&](auto inst) {
-      using I = decltype(inst);
-      I::decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
-    });
+    if (p->regime == 1) {
+      if (p->dtype == FIF_F64) st_decompose<double>(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
+      else st_decompose<float>(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
+    } else {
+      dispatch(p->dtype, p->NC, [&](auto inst) {
+        using I = decltype(inst);
+        I::decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
+      });
+    }
     cudaMemcpyAsync((char*)h_imfs + b0 * out_sig, S.d_out, nb * out_sig, cudaMemcpyDeviceToHost, S.stream);
     cudaMemcpyAsync(h_imf_count + b0, d_cnt, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, S.stream);
     cudaMemcpyAsync(h_filter_len + b0 * p->max_imfs, d_len, sizeof(int32_t) * nb * p->max_imfs,
@@ -364,14 +565,17 @@ fif_status fif_destroy(fif_plan_t p) {
   return FIF_OK;
 }
 
-int32_t fif_plan_kernels_per_call(fif_plan_t p) { return (p && p->batch > 0) ? 1 : 0; }
+int32_t fif_plan_kernels_per_call(fif_plan_t p) {
+  if (!p || p->batch == 0) return 0;
+  return p->regime == 1 ? st_kernels_per_call(p) : 1;
+}
 
-const char* fif_plan_regime(fif_plan_t p) { return p ? "resident" : "none"; }
+const char* fif_plan_regime(fif_plan_t p) { return p ? (p->regime == 1 ? "streamed" : "resident") : "none"; }
 
 fif_status fif_plan_launch_config(fif_plan_t p, int32_t* grid, int32_t* block, int32_t* smem_bytes) {
   if (!p) return FIF_ERR_INVALID_ARG;
-  const int64_t cap = (int64_t)p->num_sms * p->occ;
-  if (grid) *grid = (int32_t)(p->batch < cap ? p->batch : cap);
+  const int64_t cap = p->regime == 1 ? (int64_t)p->st_grid : (int64_t)p->num_sms * p->occ;
+  if (grid) *grid = (int32_t)(p->batch < cap || p->regime == 1 ? (p->regime == 1 ? cap : p->batch) : cap);
   if (block) *block = p->block;
   if (smem_bytes) *smem_bytes = (int32_t)p->smem;
   return FIF_OK;
@@ -389,6 +593,7 @@ fif_status fif_plan_launch_config(fif_plan_t p, int32_t* grid, int32_t* block, i
 fif_status fif_test_rfft(fif_plan_t p, int64_t batch, const void* d_in, void* d_out, void* stream) {
   if (!p || batch < 0 || (batch && (!d_in || !d_out))) return FIF_ERR_INVALID_ARG;
   if (!batch) return FIF_OK;
+  if (p->regime != 0) return FIF_ERR_UNSUPPORTED_N;  // hooks exercise the resident kernels
   cudaStream_t s = (cudaStream_t)stream;
   dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_rfft(p, d_in, d_out, batch, s); });
   HOOK_SYNC(s);
@@ -397,6 +602,7 @@ fif_status fif_test_rfft(fif_plan_t p, int64_t batch, const void* d_in, void* d_
 fif_status fif_test_irfft(fif_plan_t p, int64_t batch, const void* d_in, void* d_out, void* stream) {
   if (!p || batch < 0 || (batch && (!d_in || !d_out))) return FIF_ERR_INVALID_ARG;
   if (!batch) return FIF_OK;
+  if (p->regime != 0) return FIF_ERR_UNSUPPORTED_N;  // hooks exercise the resident kernels
   cudaStream_t s = (cudaStream_t)stream;
   dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_irfft(p, d_in, d_out, batch, s); });
   HOOK_SYNC(s);
@@ -405,6 +611,7 @@ fif_status fif_test_irfft(fif_plan_t p, int64_t batch, const void* d_in, void* d
 fif_status fif_test_extrema(fif_plan_t p, int64_t batch, const void* d_in, int32_t* d_k, void* stream) {
   if (!p || batch < 0 || (batch && (!d_in || !d_k))) return FIF_ERR_INVALID_ARG;
   if (!batch) return FIF_OK;
+  if (p->regime != 0) return FIF_ERR_UNSUPPORTED_N;  // hooks exercise the resident kernels
   cudaStream_t s = (cudaStream_t)stream;
   dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_extrema(p, d_in, d_k, batch, s); });
   HOOK_SYNC(s);
@@ -412,6 +619,7 @@ fif_status fif_test_extrema(fif_plan_t p, int64_t batch, const void* d_in, int32
 
 fif_status fif_test_window_spectrum(fif_plan_t p, int32_t L, void* d_out, void* stream) {
   if (!p || L < 1 || !d_out) return FIF_ERR_INVALID_ARG;
+  if (p->regime != 0) return FIF_ERR_UNSUPPORTED_N;
   cudaStream_t s = (cudaStream_t)stream;
   dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_window(p, L, d_out, s); });
   HOOK_SYNC(s);
@@ -421,6 +629,7 @@ fif_status fif_test_inner(fif_plan_t p, int64_t batch, int32_t L, const void* d_
                           void* stream) {
   if (!p || batch < 0 || L < 1 || (batch && (!d_in || !d_imf || !d_N))) return FIF_ERR_INVALID_ARG;
   if (!batch) return FIF_OK;
+  if (p->regime != 0) return FIF_ERR_UNSUPPORTED_N;  // hooks exercise the resident kernels
   cudaStream_t s = (cudaStream_t)stream;
   dispatch(p->dtype, p->NC, [&](auto inst) { decltype(inst)::test_inner(p, L, d_in, d_imf, d_N, batch, s); });
   HOOK_SYNC(s);

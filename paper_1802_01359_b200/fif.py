@@ -19,7 +19,8 @@ STATUS = {0: "FIF_OK", 1: "FIF_ERR_INVALID_ARG", 2: "FIF_ERR_UNSUPPORTED_N", 3: 
           5: "FIF_ERR_NCCL"}
 
 # every symbol include/fif.h declares (checked by tests/test_abi.py)
-SYMBOLS = ["fif_plan_create", "fif_decompose", "fif_decompose_host", "fif_destroy", "fif_status_string",
+REGIME_AUTO, REGIME_RESIDENT, REGIME_STREAMED = 0, 1, 2
+SYMBOLS = ["fif_plan_create", "fif_plan_create_ex", "fif_decompose", "fif_decompose_host", "fif_destroy", "fif_status_string",
            "fif_plan_kernels_per_call", "fif_plan_regime", "fif_plan_launch_config", "fif_test_rfft",
            "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner"]
 
@@ -43,6 +44,8 @@ def lib():
         vp, i32p = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)
         i64, i32, d = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
         L.fif_plan_create.argtypes = [ctypes.POINTER(vp), i64, i64, ctypes.c_int, ctypes.c_int, d, d, i32, i32]
+        L.fif_plan_create_ex.argtypes = [ctypes.POINTER(vp), i64, i64, ctypes.c_int, ctypes.c_int, d, d, i32, i32,
+                                         ctypes.c_int]
         L.fif_decompose.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.fif_decompose_host.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.fif_destroy.argtypes = [vp]
@@ -85,13 +88,13 @@ class Plan:
     """fif_plan_create(n, batch, dtype, window, xi, delta, max_inner, max_imfs)."""
 
     def __init__(self, n, batch, dtype="f64", window=WINDOW_TRI_SQ, xi=1.6, delta=1e-3, max_inner=200,
-                 max_imfs=10):
+                 max_imfs=10, regime=REGIME_AUTO):
         self.n, self.batch, self.max_imfs = int(n), int(batch), int(max_imfs)
         self.dtype = dtype
         self._h = ctypes.c_void_p()
-        _check(lib().fif_plan_create(ctypes.byref(self._h), self.n, self.batch, F64 if dtype == "f64" else F32,
-                                     int(window), float(xi), float(delta), int(max_inner), int(max_imfs)),
-               "fif_plan_create")
+        _check(lib().fif_plan_create_ex(ctypes.byref(self._h), self.n, self.batch, F64 if dtype == "f64" else F32,
+                                        int(window), float(xi), float(delta), int(max_inner), int(max_imfs),
+                                        int(regime)), "fif_plan_create_ex")
 
     @property
     def handle(self):
