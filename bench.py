@@ -38,19 +38,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1"])
+    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg4"])
+    ap.add_argument("--n", type=int, default=1 << 14, help="signal length for cfg4 (fp32 sweep)")
     ap.add_argument("--batch", type=int, default=None, help="signals per rank (default: the config's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
-def workload(cfg, batch):
+def workload(cfg, batch, n4=1 << 14):
+    """(n, batch per rank, delta, dtype) of a BASELINE.json config."""
     from paper_1802_01359_b200 import signals
 
+    if cfg == "cfg4":
+        return n4, signals.cfg4_batch(n4) if batch is None else batch, 1e-3, "f32"
     c = signals.CONFIGS[cfg]
     B = c["batch"] if batch is None else batch
-    return c["n"], B, c["delta"]
+    return c["n"], B, c["delta"], c["dtype"]
 
 
 def hbm_peak():
@@ -114,7 +118,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(cfg, n, delta, budget_s=12.0, max_signals=256):
+def cpu_baseline(cfg, n, delta, budget_s=12.0, max_signals=256, n4=None):
     """The oracle as it stands (TD literal iteration, OpenMP over signals) on a bounded sample of the
     same workload: the first S signals of the batch, S grown until >= budget_s of CPU work."""
     import oracle
@@ -124,7 +128,7 @@ def cpu_baseline(cfg, n, delta, budget_s=12.0, max_signals=256):
     done, t_total, start = 0, 0.0, 0
     chunk = max(ncores, 8)
     while t_total < budget_s and done < max_signals:
-        s = signals.make_batch(cfg, batch=chunk, start=start)
+        s = signals.make_batch(cfg, batch=chunk, start=start, n=n4).astype(np.float64)
         t0 = time.perf_counter()
         oracle.decompose(s, delta=delta)
         t_total += time.perf_counter() - t0
@@ -168,13 +172,13 @@ def run_reference(args, world, rank):
     """--impl reference: the oracle (TD literal iteration) on the host cores, bounded sample per step."""
     if rank != 0:
         return
-    n, B, delta = workload(args.config, args.batch)
+    n, B, delta, dt = workload(args.config, args.batch, args.n)
     import oracle
     from paper_1802_01359_b200 import signals
 
     ncores = oracle.num_threads()
-    S = max(ncores, 16)  # signals per step (bounded sample of the batch)
-    s = signals.make_batch(args.config, batch=S)
+    S = max(ncores, 16) if n <= 8192 else ncores  # signals per step (bounded sample of the batch)
+    s = signals.make_batch(args.config, batch=S, n=n if args.config == "cfg4" else None).astype(np.float64)
     for _ in range(args.warmup):
         oracle.decompose(s[: max(1, ncores)], delta=delta)
     t0 = time.perf_counter()
@@ -184,8 +188,8 @@ def run_reference(args, world, rank):
     value = S * n / dt
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {S}-signal sample of the {B}x{n} fp64 batch per step",
+            "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": {"workload": f"{args.config}: {S}-signal sample of the {B}x{n} {dt} batch per step",
                        "n": n, "batch_per_step": S, "xi": 1.6, "delta": delta, "max_inner": 200, "max_imfs": 10},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "oracle",
                              "sample": f"{S} signals of {args.config} per step"},
@@ -204,10 +208,11 @@ def main():
     torch.cuda.set_device(local)
     from paper_1802_01359_b200 import fif, signals
 
-    n, B, delta = workload(args.config, args.batch)
-    s_host = signals.make_batch(args.config, batch=B, start=rank_start(rank, B))
+    n, B, delta, dt = workload(args.config, args.batch, args.n)
+    s_host = signals.make_batch(args.config, batch=B, start=rank_start(rank, B),
+                                n=n if args.config == "cfg4" else None)
     x = torch.from_numpy(s_host).cuda()
-    plan = fif.Plan(n, B, "f64", delta=delta)
+    plan = fif.Plan(n, B, dt, delta=delta)
     imfs, count, lens, iters = plan.alloc_outputs()
     stream = torch.cuda.current_stream()
     cfgl = plan.launch_config()
@@ -239,14 +244,16 @@ def main():
     # roofline (dominant kernel = the single resident kernel: its launch duration = the step)
     cnt = count.cpu().numpy()
     Mtot = int(np.clip(cnt, 0, None).sum())
-    fft_bytes = 2 * n * 8 * (Mtot + B)            # 2 n b per transform, (M+1) transforms per signal
-    comp_bytes = n * 8 * (Mtot + 2 * B)           # read s once + write M IMFs + trend
-    written_bytes = n * 8 * B * (plan.max_imfs + 1) + n * 8 * B  # what the kernel actually moves (all slots)
+    eb = 8 if dt == "f64" else 4
+    passes = 2 if cfgl["regime"] == "resident" else 4  # four-step: two read+write passes per transform
+    fft_bytes = passes * n * eb * (Mtot + B)      # passes*n*b per transform, (M+1) transforms per signal
+    comp_bytes = n * eb * (Mtot + 2 * B)          # read s once + write M IMFs + trend
+    written_bytes = n * eb * B * (plan.max_imfs + 1) + n * eb * B  # output slots + input
     peak, peak_kind = hbm_peak()
     ach = fft_bytes / (ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.config == "cfg1" and args.batch is None:
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
@@ -278,21 +285,23 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, n, delta)
+        cpu = cpu_baseline(args.config, n, delta, n4=n if args.config == "cfg4" else None)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {B} signals x n={n} fp64 per GPU (BASELINE.json configs[1])",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": {"workload": f"{args.config}: {B} signals x n={n} {dt} per GPU (BASELINE.json configs"
+                                   f"[{args.config[-1]}])",
                        "n": n, "batch_per_gpu": B, "xi": 1.6, "delta": delta, "max_inner": 200, "max_imfs": 10,
-                       "window": "tri_sq (R1)", "parallelism": f"batch split x{world}, no collective",
-                       "l2": "inputs+outputs 1.6 GB/step > 126 MB L2 (no flush needed)",
+                       "window": "tri_sq (R1)", "parallelism": f"batch split x{world}, no collective", "regime": cfgl["regime"],
+                       "l2": f"inputs+outputs {written_bytes / 1e9:.2f} GB/step > 126 MB L2 (no flush needed)",
                        "imfs_per_signal_mean": Mtot / B, "launch": cfgl},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "traffic": traffic, "peak_kind": peak_kind,
-                         "model": "FFT-pass bytes 2*n*8*(M+1) per signal (SURVEY.md 8d)",
+                         "model": f"FFT-pass bytes {passes}*n*{eb}*(M+1) per signal (SURVEY.md 8d)",
+                         "scope": "whole step" if cfgl["regime"] != "resident" else "the single resident kernel",
                          "compulsory_frac": comp_bytes / (ms * 1e-3) / 1e9 / peak,
                          "written_bytes_per_launch": written_bytes},
             "cpu_baseline": cpu,
