@@ -1,19 +1,33 @@
-// fif_streamed.cuh -- the "streamed" regime of the FIF hot path for n beyond on-chip capacity
-// (configs 2 and 4: n up to 2^22, radix 2/3/4/5/8).  The spectrum X (transposed four-step order), an
-// FFT work buffer Z and the time-domain remainder R live in HBM; every IMF is a fixed sequence of
-// stream-ordered kernels over the whole batch, with per-signal state (k, L, N, M, done) in device
-// arrays so that no host round trip happens inside fif_decompose.
+// fif_streamed.cuh -- the "streamed" regime of the FIF hot path for n beyond one CTA's on-chip
+// capacity (configs 2, 3 and 4: n up to 2^27, n/2 of the form 2^a 3^b 5^c).
 //
-// Same method and readings as fif_resident.cuh:
-//   a1  forward four-step FFT of z_m = s_2m + i s_2m+1 (columns, then rows; output in transposed
-//       order: position k1 N2 + k2 holds bin k1 + N1 k2) + Hermitian post-processing
-//   a2  extrema monoid per chunk of R, ordered fold per signal (reading A4)
-//   a3  L from k (A1, A3, A8)
-//   a4  w_hat_k = [sin(pi r/n) / (L sin(pi k/n))]^4 with exact integer reduction, sinpi
-//   a5  fp64 cap probe, then K-ary fp64 search passes when SD(cap) <= delta (monotone SD)
-//   a6  damping + pre-processing, inverse four-step (rows, then columns -> natural order),
-//       IMF store and R -= IMF in the last kernel's epilogue
-//   a7  counts, trend in slot M, zero fill
+// The spectrum X (digit-reversed multi-level order, below) and the time-domain remainder R live in
+// HBM (R in the trend slot of d_imfs); the IMF slot being produced doubles as the inverse FFT's work
+// buffer.  Every IMF is a fixed, short sequence of stream-ordered kernels over the whole batch, with
+// per-signal state (k, L, N, M, active) in device arrays, so fif_decompose never synchronises.
+//
+// Multi-level FFT over NC = n/2 complex points z_m = x_2m + i x_2m+1 ("U^T s is the DFT
+// of s ... FFT"): NC = F_0 F_1 ... F_{L-1}; digit i has stride S_i = F_{i+1}...F_{L-1}.  Forward pass
+// i (i = 0..L-1) does, for every block and every lower index s < S_i, a length-F_i DFT over the digit
+// (stride S_i) and multiplies element (k_i, s) by e^{-2 pi i s k_i/(F_i S_i)}; the result sits at
+// position sum k_i S_i and holds bin sum k_i F_0..F_{i-1} ("digit reversed").  The inverse runs the
+// passes backwards (conjugate twiddle first, then the IDFT) and ends in natural order.  The last
+// level (S = 1) is a contiguous row; rows come in Hermitian mirror pairs (bin k of row base+P t pairs
+// with bin NC-k at row P-base, element F-1-t), so the real-FFT post-processing (forward) and the
+// damping + real-IFFT pre-processing (inverse), which couple X_k and X_{NC-k}, fuse into the row pass.
+//
+// Steps (same readings as fif_resident.cuh):
+//   a1  k_col<FWD_FIRST> .. k_rows_fwd: forward FFT + Hermitian post-processing
+//   a2  extrema: per-segment monoid partials written by the level-0 passes, folded by
+//       k_fold (ordered, two levels)                                                   (A4)
+//   a3  L from k in k_fold (A1, A3, A8: floor(fl(fl(xi n)/k)) in IEEE fp64)
+//   a4  w_hat_k = [sin(pi r/n)/(L sin(pi k/n))]^4, sines from a two-level table of
+//       e^{i pi j/n} (exact integer reduction of r = L k mod n)
+//   a5  k_probe: fp64 Parseval sums at N = cap, then K-ary fp64 rounds if SD(cap) <= delta
+//       (SD monotone in N, P7); the last CTA of each signal decides
+//   a6  k_rows_inv: a^N damping, X <- (1-a^N) X, pre-processing, row IDFTs; middle
+//       passes; k_col<INV_LAST>: level-0 IDFT, IMF store, R -= IMF, extrema partials
+//   a7  k_fold bookkeeping (l_m, N_m, M), k_final: trend in slot M, zero fill
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -23,20 +37,54 @@
 namespace fifgpu {
 namespace st {
 
+constexpr int kMaxLev = 4;
 constexpr int kMaxPass = 16;
-constexpr int kProbes = 15;  // K-ary search: probes per pass
+constexpr int kProbes = 15;  // K-ary search: probes per round
 constexpr int kThreads = 256;
+constexpr int kNW = kThreads / 32;
+
+struct Level {
+  int F;          // sub-FFT length of this digit
+  int C;          // columns (consecutive lower indices s) per tile; 2 rows (a mirror pair) for the row level
+  int pitch;      // shared-memory column pitch (complex elements)
+  int np;         // radix passes of the length-F FFT
+  int rad[kMaxPass];
+  int twoff;      // offset of e^{-2 pi i j/F} (j < F) in the Stockham twiddle table
+  int64_t S;      // stride of the digit
+  int64_t A;      // blocks = NC / (F S)
+  int64_t E2;     // 2n / (F S): E-table index step of the inter-level twiddle
+  int64_t tiles;  // tiles per signal = A S / C (column levels)
+};
 
 struct Geo {
   int64_t n, NC, batch;
-  int N1, N2;                      // NC = N1 * N2
-  int C;                           // columns per CTA in the column kernels
-  int rad1[kMaxPass], np1;         // radix schedule of the N1-point FFTs
-  int rad2[kMaxPass], np2;         // radix schedule of the N2-point FFTs
-  int binch, nbch;                 // bins per chunk (reductions), chunks per signal
-  int smpch, nsch;                 // samples per extrema chunk, chunks per signal
+  int L;                 // levels (>= 2)
+  Level lv[kMaxLev];
+  int64_t P;             // rows = NC / F_{L-1}: bin k = base + P t in a row
+  int Frow;              // F_{L-1}
+  int Fd[kMaxLev];       // F_i (copy of lv[i].F for the digit loops)
+  int64_t Pd[kMaxLev];   // bin weight of digit i = F_0 ... F_{i-1}
+  int64_t Sr[kMaxLev];   // row-index weight of digit i = S_i / F_{L-1}  (i < L-1)
+  int64_t units;         // row-pair units = floor(P/2) + 1
+  int64_t nseg;          // extrema segments per signal = NC / C_0 (each 2 C_0 consecutive samples)
+  int64_t grp;           // segments per fold group
+  int64_t ngrp;          // fold groups per signal
+  int64_t rpc;           // probe: rows per chunk
+  int64_t nbch;          // probe chunks per signal
+  int eb;                // E table split: E(j) = Eh[j >> eb] * El[j & (2^eb - 1)]
   int max_imfs, max_inner, window;
   double xi, delta2;
+  int64_t sig_stride;    // reals per signal in d_imfs = (max_imfs + 1) n
+};
+
+template <typename Real>
+struct Tabs {
+  using V = typename Cx<Real>::V;
+  const double2* Eh;  // e^{i pi (h 2^eb)/n}
+  const double2* El;  // e^{i pi l/n}, l < 2^eb
+  const V* Th;        // the same in Real precision (twiddles)
+  const V* Tl;
+  const V* tw;        // per-level Stockham twiddles
 };
 
 // per-signal control block (device)
@@ -44,14 +92,18 @@ struct Ctl {
   int32_t* k;       // extrema count of the current remainder
   int32_t* L;       // half-length of h for the current IMF
   int32_t* N;       // iteration count of the current IMF
-  int32_t* M;       // IMFs done
-  int32_t* active;  // 1 while the current IMF is being extracted
+  int32_t* M;       // IMFs done (-1: non-finite input)
+  int32_t* active;  // 1 while the signal still extracts IMFs
   int32_t* search;  // 1 while the K-ary search runs
   int32_t* lo;      // search bracket: !pass(lo) (lo = 0 virtual), pass(hi)
   int32_t* hi;
-  int32_t* bad;     // non-finite input
-  int32_t* ext;     // [B][nsch][3] extrema partials (first sign, last sign, changes)
-  double* red;      // [B][nbch][2*kProbes] reduction partials
+  int32_t* bad;     // non-finite input seen
+  uint32_t* cnt;    // last-CTA counters
+  uint32_t* segi;   // [B][nseg] packed extrema monoid of a segment's internal differences
+  void* segv;       // [B][nseg][2] Real: first and last sample of the segment
+  uint32_t* gi;     // [B][ngrp] packed monoid of a fold group
+  void* gv;         // [B][ngrp][2] Real
+  double* red;      // [B][nbch][2 kProbes] probe partial sums
 };
 
 // ------------------------------------------------------------------ small DFTs (radix 2, 3, 4, 5, 8)
@@ -83,16 +135,17 @@ __device__ __forceinline__ void dft5(V& x0, V& x1, V& x2, V& x3, V& x4) {
   x3 = csub(t2, u2);
 }
 
-// One Stockham pass of radix p (runtime) over F independent FFTs of length Ns stored contiguously:
-// src[f*Ns + i] -> dst[f*Ns + j].  tw[j] = e^{-2 pi i j/Ns}.
+// One Stockham pass of radix p over `cols` independent length-Ns FFTs, column c at offset c*pitch:
+// src[c, i] -> dst[c, j].  tw[j] = e^{-2 pi i j/Ns}.
 template <int DIR, typename V>
-__device__ void cta_pass(const V* src, V* dst, int Ns, int F, int p, int NS, const V* __restrict__ tw) {
+__device__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int p, int NS,
+                         const V* __restrict__ tw) {
   const int per = Ns / p;
   const int tstride = Ns / (NS * p);
-  for (int idx = threadIdx.x; idx < F * per; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
     const int f = idx / per, vt = idx - f * per;
     const int k = vt % NS;
-    const V* s = src + (size_t)f * Ns + vt;
+    const V* s = src + f * pitch + vt;
     V x[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -101,7 +154,7 @@ __device__ void cta_pass(const V* src, V* dst, int Ns, int F, int p, int NS, con
 #pragma unroll
       for (int r = 1; r < 8; ++r)
         if (r < p) {
-          V t = __ldg(tw + (size_t)k * r * tstride);
+          V t = __ldg(tw + k * r * tstride);
           if (DIR > 0) t.y = -t.y;
           x[r] = cmul(x[r], t);
         }
@@ -113,45 +166,52 @@ __device__ void cta_pass(const V* src, V* dst, int Ns, int F, int p, int NS, con
       case 5: dft5<DIR>(x[0], x[1], x[2], x[3], x[4]); break;
       default: dft8<DIR>(x); break;
     }
-    V* d = dst + (size_t)f * Ns + (vt / NS) * NS * p + k;
+    V* d = dst + f * pitch + (vt / NS) * NS * p + k;
 #pragma unroll
     for (int r = 0; r < 8; ++r)
       if (r < p) d[r * NS] = x[r];
   }
 }
 
-// All passes; a holds the input, returns the buffer holding the output (a or b).
+// All passes of a level; a holds the input, returns the buffer holding the output (a or b).
 template <int DIR, typename V>
-__device__ V* cta_fft(V* a, V* b, int Ns, int F, const int* rad, int np, const V* __restrict__ tw) {
+__device__ V* cta_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
   int NS = 1;
-  for (int ps = 0; ps < np; ++ps) {
+  for (int ps = 0; ps < lv.np; ++ps) {
     __syncthreads();
-    cta_pass<DIR>(a, b, Ns, F, rad[ps], NS, tw);
-    NS *= rad[ps];
+    cta_pass<DIR>(a, b, lv.F, cols, lv.pitch, lv.rad[ps], NS, tw + lv.twoff);
+    NS *= lv.rad[ps];
     V* t = a; a = b; b = t;
   }
   __syncthreads();
   return a;
 }
 
-// e^{s 2 pi i m / Nmod} with exact integer reduction of m (sincospi argument 2 m / Nmod)
-template <typename V>
-__device__ __forceinline__ V cis(int64_t m, int64_t Nmod, int sgn) {
-  m %= Nmod;
-  if (m < 0) m += Nmod;
-  double s, c;
-  sincospi(2.0 * (double)m / (double)Nmod, &s, &c);
-  using S = decltype(V{}.x);
-  return V{(S)c, (S)(sgn * s)};
+// ------------------------------------------------------------------ tables
+// E(j) = e^{i pi j/n}, 0 <= j <= 2n, from the two-level table (one complex product)
+__device__ __forceinline__ double2 E64(const double2* __restrict__ Eh, const double2* __restrict__ El, int eb,
+                                       int64_t j) {
+  return cmul(__ldg(Eh + (j >> eb)), __ldg(El + (j & ((1LL << eb) - 1))));
+}
+// sin(pi j/n) for 0 <= j <= n/2: both table angles lie in the first quadrant, so the imaginary part
+// of the product is a sum of two non-negative terms (relative error ~2 ulp)
+__device__ __forceinline__ double sin_n(const double2* __restrict__ Eh, const double2* __restrict__ El, int eb,
+                                        int64_t j) {
+  const double2 h = __ldg(Eh + (j >> eb)), l = __ldg(El + (j & ((1LL << eb) - 1)));
+  return h.x * l.y + h.y * l.x;
+}
+template <typename Real>
+__device__ __forceinline__ typename Cx<Real>::V Er(const Tabs<Real>& tb, int eb, int64_t j) {
+  return cmul(__ldg(tb.Th + (j >> eb)), __ldg(tb.Tl + (j & ((1LL << eb) - 1))));
 }
 
-// ------------------------------------------------------------------ window spectrum (a4)
-__device__ __forceinline__ double what_st(int64_t n, int L, int64_t k) {
+// a4: w_hat_k for 0 <= k <= n/2: r = min(L k mod n, n - L k mod n)
+template <typename Real>
+__device__ __forceinline__ double what_tab(const Geo& g, const Tabs<Real>& tb, int L, int64_t k) {
   if (k == 0) return 1.0;
-  int64_t m = ((int64_t)L * k) % n;
-  const int64_t r = m < n - m ? m : n - m;
-  const int64_t kk = k < n - k ? k : n - k;
-  const double s = sinpi((double)r / (double)n) / ((double)L * sinpi((double)kk / (double)n));
+  const int64_t m = ((int64_t)L * k) % g.n;
+  const int64_t r = m < g.n - m ? m : g.n - m;
+  const double s = sin_n(tb.Eh, tb.El, g.eb, r) / ((double)L * sin_n(tb.Eh, tb.El, g.eb, k));
   const double s2 = s * s;
   return s2 * s2;
 }
@@ -165,205 +225,426 @@ __device__ __forceinline__ double upow_rt(double a, int e) {
   return r;
 }
 
-// transposed-order position <-> bin
-__device__ __forceinline__ int64_t bin_of_pos(const Geo& g, int64_t p) {
-  const int64_t k1 = p / g.N2, k2 = p - k1 * g.N2;
-  return k1 + (int64_t)g.N1 * k2;
+// row index (position / F_{L-1}) of the row whose bins are base + P t, and back
+__device__ __forceinline__ int64_t row_of_base(const Geo& g, int64_t base) {
+  int64_t r = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxLev - 1; ++i)
+    if (i < g.L - 1) r += ((base / g.Pd[i]) % g.Fd[i]) * g.Sr[i];
+  return r;
 }
-__device__ __forceinline__ int64_t pos_of_bin(const Geo& g, int64_t k) {
-  const int64_t k1 = k % g.N1, k2 = k / g.N1;
-  return k1 * g.N2 + k2;
+__device__ __forceinline__ int64_t base_of_row(const Geo& g, int64_t row) {
+  int64_t b = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxLev - 1; ++i)
+    if (i < g.L - 1) b += ((row / g.Sr[i]) % g.Fd[i]) * g.Pd[i];
+  return b;
 }
 
-// ------------------------------------------------------------------ forward a1: columns
-// z = s viewed as complex [B][NC]; Z[k1 N2 + m2] = twiddle * DFT_N1 over m1 of z[N2 m1 + m2].
-// Also copies s into R and flags non-finite samples.
+// ------------------------------------------------------------------ a2 extrema monoid
+// Over a sequence of differences: f = first nonzero sign, l = last nonzero sign, c = sign changes
+// among the nonzero ones (zero differences dropped: plateau collapse, reading A4).
+struct Mono {
+  int f, l, c;
+};
+__device__ __forceinline__ Mono mcomb(Mono a, Mono b) {
+  return Mono{a.f ? a.f : b.f, b.l ? b.l : a.l, a.c + b.c + ((a.l && b.f && a.l != b.f) ? 1 : 0)};
+}
 template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_fwd_cols(Geo g, const Real* __restrict__ s, Real* __restrict__ R,
-                                                       typename Cx<Real>::V* __restrict__ Z,
-                                                       const typename Cx<Real>::V* __restrict__ tw1, Ctl c,
-                                                       int64_t R_stride) {
-  using V = typename Cx<Real>::V;
-  extern __shared__ __align__(16) char smem_raw[];
-  V* A = reinterpret_cast<V*>(smem_raw);
-  V* Bf = A + (size_t)g.N1 * g.C;
-  const int64_t tiles = g.N2 / g.C;
-  for (int64_t t = blockIdx.x; t < g.batch * tiles; t += gridDim.x) {
-    const int64_t b = t / tiles, c0 = (t - b * tiles) * g.C;
-    const V* zb = reinterpret_cast<const V*>(s + b * g.n);
-    V* Rb = reinterpret_cast<V*>(R + b * R_stride);
-    bool finite = true;
-    // load tile (column-major in smem: column c occupies A[c*N1 .. c*N1+N1))
-    for (int i = threadIdx.x; i < g.N1 * g.C; i += blockDim.x) {
-      const int m1 = i / g.C, cc = i - m1 * g.C;
-      const int64_t gi = (int64_t)g.N2 * m1 + c0 + cc;
-      const V v = zb[gi];
-      finite &= isfinite(v.x) && isfinite(v.y);
-      Rb[gi] = v;
-      A[cc * g.N1 + m1] = v;
-    }
-    if (!finite) atomicOr(c.bad + b, 1);
-    V* out = cta_fft<-1>(A, Bf, g.N1, g.C, g.rad1, g.np1, tw1);
-    V* Zb = Z + b * g.NC;
-    for (int i = threadIdx.x; i < g.N1 * g.C; i += blockDim.x) {
-      const int k1 = i / g.C, cc = i - k1 * g.C;
-      const int64_t m2 = c0 + cc;
-      V v = out[cc * g.N1 + k1];
-      v = cmul(v, cis<V>(m2 * k1, g.NC, -1));
-      Zb[(int64_t)k1 * g.N2 + m2] = v;
-    }
-    __syncthreads();
+__device__ __forceinline__ Mono mdiff(Real d) {
+  const int s = d > (Real)0 ? 1 : (d < (Real)0 ? -1 : 0);
+  return Mono{s, s, 0};
+}
+__device__ __forceinline__ uint32_t mpack(Mono m) {
+  return (uint32_t)(m.f + 1) | ((uint32_t)(m.l + 1) << 2) | ((uint32_t)m.c << 4);
+}
+__device__ __forceinline__ Mono munpack(uint32_t u) {
+  return Mono{(int)(u & 3) - 1, (int)((u >> 2) & 3) - 1, (int)(u >> 4)};
+}
+// ordered warp reduction: lane 0 receives lanes 0..31 combined in lane order
+__device__ __forceinline__ Mono warp_mono(Mono m) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Mono o;
+    o.f = __shfl_down_sync(0xffffffffu, m.f, off);
+    o.l = __shfl_down_sync(0xffffffffu, m.l, off);
+    o.c = __shfl_down_sync(0xffffffffu, m.c, off);
+    if ((lane & (2 * off - 1)) == 0 && lane + off < 32) m = mcomb(m, o);
   }
+  return m;
+}
+// ordered block reduction; the result is valid in thread 0
+__device__ __forceinline__ Mono block_mono(Mono m, Mono* sm) {
+  m = warp_mono(m);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Mono r = sm[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = mcomb(r, sm[w]);
+    m = r;
+  }
+  return m;
 }
 
-// rows: for every row of N2 contiguous elements: DFT (DIR); for DIR = +1 (inverse step B') also
-// multiply by e^{+2 pi i m2 k1/NC}.  Only active signals (if only_active).
-template <typename Real, int DIR>
-__global__ void __launch_bounds__(kThreads) k_rows(Geo g, typename Cx<Real>::V* __restrict__ Z,
-                                                   const typename Cx<Real>::V* __restrict__ tw2, Ctl c,
-                                                   int only_active) {
-  using V = typename Cx<Real>::V;
-  extern __shared__ __align__(16) char smem_raw[];
-  V* A = reinterpret_cast<V*>(smem_raw);
-  V* Bf = A + g.N2;
-  for (int64_t t = blockIdx.x; t < g.batch * g.N1; t += gridDim.x) {
-    const int64_t b = t / g.N1;
-    const int k1 = (int)(t - b * g.N1);
-    if (only_active && !c.active[b]) continue;
-    V* row = Z + b * g.NC + (int64_t)k1 * g.N2;
-    for (int i = threadIdx.x; i < g.N2; i += blockDim.x) A[i] = row[i];
-    V* out = cta_fft<DIR>(A, Bf, g.N2, 1, g.rad2, g.np2, tw2);
-    for (int i = threadIdx.x; i < g.N2; i += blockDim.x) {
-      V v = out[i];
-      if (DIR > 0) v = cmul(v, cis<V>((int64_t)i * k1, g.NC, +1));
-      row[i] = v;
-    }
-    __syncthreads();
-  }
-}
-
-// forward post-processing: X_k = E + e^{-2 pi i k/n} O from Z_k, Z_{NC-k} (transposed positions);
-// Nyquist X_NC = Re Z_0 - Im Z_0 to Xn[b].
+// Segment partials of a level-0 tile held in shared memory as complex pairs: segment f consists of
+// the 2C reals of columns c = 0..C-1 (element (c, f) at buf[c*pitch + f]); one warp per segment.
 template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_fwd_post(Geo g, const typename Cx<Real>::V* __restrict__ Z,
-                                                       typename Cx<Real>::V* __restrict__ X,
-                                                       typename Cx<Real>::V* __restrict__ Xn) {
-  using V = typename Cx<Real>::V;
-  const int64_t tot = g.batch * g.NC;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = i / g.NC, p = i - b * g.NC;
-    const int64_t k = bin_of_pos(g, p);
-    const V* Zb = Z + b * g.NC;
-    const V P = Zb[p];
-    const V Q = Zb[pos_of_bin(g, k == 0 ? 0 : g.NC - k)];
-    const Real h = (Real)0.5;
-    const V E = V{h * (P.x + Q.x), h * (P.y - Q.y)};
-    const V D = V{h * (P.x - Q.x), h * (P.y + Q.y)};
-    const V O = V{D.y, -D.x};
-    V x = cadd(E, cmul(cis<V>(k, g.n, -1), O));
-    if (k == 0) {
-      x = V{P.x + P.y, (Real)0};
-      Xn[b] = V{P.x - P.y, (Real)0};
-    }
-    X[b * g.NC + p] = x;
-  }
-}
-
-// ------------------------------------------------------------------ a2 extrema partials
-// chunk c of signal b covers differences D_i = R[i+1]-R[i] for i in [c*smpch, min((c+1)*smpch, n-1))
-template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_ext(Geo g, const Real* __restrict__ R, int64_t R_stride, Ctl c,
-                                                  int first) {
-  __shared__ int sf[kThreads], sl[kThreads], sc[kThreads];
-  for (int64_t t = blockIdx.x; t < g.batch * g.nsch; t += gridDim.x) {
-    const int64_t b = t / g.nsch;
-    const int ch = (int)(t - b * g.nsch);
-    if (!first && !c.active[b]) continue;
-    const Real* Rb = R + b * R_stride;
-    const int64_t i0 = (int64_t)ch * g.smpch;
-    const int64_t i1 = min((int64_t)(ch + 1) * g.smpch, g.n - 1);
-    // each thread folds a contiguous sub-range
-    const int64_t len = i1 - i0, per = (len + blockDim.x - 1) / blockDim.x;
-    const int64_t a0 = i0 + threadIdx.x * per, a1 = min(a0 + per, i1);
-    int f = 0, l = 0, cnt = 0;
-    if (a0 < a1) {
-      Real prev = Rb[a0];
-      for (int64_t i = a0; i < a1; ++i) {
-        const Real x = Rb[i + 1];
-        const Real d = x - prev;
+__device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, int64_t seg0, int64_t segstep,
+                              uint32_t* __restrict__ segi, Real* __restrict__ segv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nd = 2 * lv.C - 1;  // internal differences
+  const int q = (nd + 31) / 32;
+  for (int f = warp; f < lv.F; f += nw) {
+    Mono m{0, 0, 0};
+    const int d0 = lane * q, d1 = min(d0 + q, nd);
+    if (d0 < d1) {
+      auto x_at = [&](int j) -> Real {
+        const auto v = buf[(j >> 1) * lv.pitch + f];
+        return (j & 1) ? v.y : v.x;
+      };
+      Real prev = x_at(d0);
+      for (int j = d0; j < d1; ++j) {
+        const Real x = x_at(j + 1);
+        m = mcomb(m, mdiff<Real>(x - prev));
         prev = x;
-        if (d == (Real)0) continue;
-        const int sg = d > (Real)0 ? 1 : -1;
-        if (f == 0) f = sg;
-        if (l != 0 && sg != l) ++cnt;
-        l = sg;
       }
     }
-    sf[threadIdx.x] = f; sl[threadIdx.x] = l; sc[threadIdx.x] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int F = 0, Ls = 0, C = 0;
-      for (int u = 0; u < (int)blockDim.x; ++u) {
-        const int f2 = sf[u], l2 = sl[u], c2 = sc[u];
-        C += c2 + ((Ls != 0 && f2 != 0 && Ls != f2) ? 1 : 0);
-        if (F == 0) F = f2;
-        if (l2 != 0) Ls = l2;
+    m = warp_mono(m);
+    if (lane == 0) {
+      const int64_t s = seg0 + (int64_t)f * segstep;
+      segi[s] = mpack(m);
+      segv[2 * s] = buf[f].x;
+      segv[2 * s + 1] = buf[(lv.C - 1) * lv.pitch + f].y;
+    }
+  }
+}
+
+// Ordered fold of items [i0, i1) (monoid + first/last value), boundary differences between
+// consecutive items included (those before i0 are not).  Result in thread 0: monoid, first, last.
+template <typename Real>
+__device__ Mono fold_items(const uint32_t* __restrict__ mi, const Real* __restrict__ mv, int64_t i0, int64_t i1,
+                           Mono* sm) {
+  const int64_t len = i1 - i0, per = (len + blockDim.x - 1) / blockDim.x;
+  const int64_t a0 = i0 + (int64_t)threadIdx.x * per, a1 = min(a0 + per, i1);
+  Mono acc{0, 0, 0};
+  if (a0 < a1) {
+    Real prev = a0 > i0 ? __ldcg(mv + 2 * (a0 - 1) + 1) : (Real)0;
+    for (int64_t s = a0; s < a1; ++s) {
+      const Real first = __ldcg(mv + 2 * s), last = __ldcg(mv + 2 * s + 1);
+      if (s > i0) acc = mcomb(acc, mdiff<Real>(first - prev));
+      acc = mcomb(acc, munpack(__ldcg(mi + s)));
+      prev = last;
+    }
+  }
+  return block_mono(acc, sm);
+}
+
+__device__ __forceinline__ int filter_half_length(const Geo& g, int k) {
+  // PAPER.md:81 l = 2 floor(nu N / k) with reading A1 (h half-support L = floor(xi n/k)), A3 clamp,
+  // A8 IEEE evaluation (no contraction)
+  const double tq = __dmul_rn(g.xi, (double)g.n);
+  const double u = __ddiv_rn(tq, (double)k);
+  long long q = (long long)floor(u);
+  long long L = g.window ? 2 * q : q;
+  const long long Lmax = (g.n - 1) / 4;
+  if (L < 2) L = 2;
+  if (L > Lmax) L = Lmax;
+  return (int)L;
+}
+
+// ------------------------------------------------------------------ init
+__global__ void k_init(Geo g, Ctl c) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < g.batch;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    c.M[b] = 0;
+    c.bad[b] = 0;
+    c.active[b] = 1;
+    c.search[b] = 0;
+    c.cnt[b] = 0;
+  }
+}
+
+// ------------------------------------------------------------------ column passes
+enum { PASS_MID = 0, PASS_FWD_FIRST = 1, PASS_INV_LAST = 2 };
+
+// Tile = C consecutive lower indices s x the F digit values, of block a.  DIR -1: forward (DFT, then
+// twiddle), +1: inverse (conjugate twiddle, then IDFT).  Buffers: forward passes work on X; inverse
+// passes on the IMF slot M of the signal.  FWD_FIRST reads the signal (copying it to R, flagging
+// non-finite samples, writing extrema partials of s); INV_LAST finishes the IMF in natural order,
+// updates R and writes the extrema partials of the new remainder.
+template <typename Real, int DIR, int KIND>
+__global__ void __launch_bounds__(kThreads) k_col(Geo g, Level lv, const Real* __restrict__ sig,
+                                                  Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
+                                                  Tabs<Real> tb, Ctl c) {
+  using V = typename Cx<Real>::V;
+  extern __shared__ __align__(16) char smem_raw[];
+  V* A = reinterpret_cast<V*>(smem_raw);
+  V* Bf = A + (size_t)lv.C * lv.pitch;
+  const int64_t spt = lv.S / lv.C;
+  const int64_t total = g.batch * lv.tiles;
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const int64_t b = t / lv.tiles, tt = t - b * lv.tiles;
+    if (KIND != PASS_FWD_FIRST && !c.active[b]) continue;
+    const int64_t a = tt / spt, s0 = (tt - a * spt) * lv.C;
+    const int64_t base = a * (int64_t)lv.F * lv.S + s0;
+    Real* Rb = imfs + b * g.sig_stride + (int64_t)g.max_imfs * g.n;
+    V* buf;
+    if (DIR < 0) buf = X + b * g.NC;
+    else buf = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
+    const V* src = KIND == PASS_FWD_FIRST ? reinterpret_cast<const V*>(sig + b * g.n) : buf;
+    bool finite = true;
+    for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
+      const int f = i / lv.C, cc = i - f * lv.C;
+      const int64_t gi = base + (int64_t)f * lv.S + cc;
+      V v = src[gi];
+      if (KIND == PASS_FWD_FIRST) {
+        finite &= isfinite(v.x) && isfinite(v.y);
+        reinterpret_cast<V*>(Rb)[gi] = v;
       }
-      int32_t* e = c.ext + (b * g.nsch + ch) * 3;
-      e[0] = F; e[1] = Ls; e[2] = C;
+      if (DIR > 0 && lv.E2 > 0) v = cmul(v, Er(tb, g.eb, lv.E2 * (s0 + cc) * f));
+      A[cc * lv.pitch + f] = v;
+    }
+    if (KIND == PASS_FWD_FIRST) {
+      if (!finite) atomicOr(c.bad + b, 1);
+      __syncthreads();
+      tile_segments<Real>(A, lv, b * g.nseg + s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+    }
+    V* out = cta_fft<DIR>(A, Bf, lv, lv.C, tb.tw);
+    if (KIND == PASS_INV_LAST) {
+      V* stage = out == A ? Bf : A;
+      for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
+        const int f = i / lv.C, cc = i - f * lv.C;
+        const int64_t gi = base + (int64_t)f * lv.S + cc;
+        const V v = out[cc * lv.pitch + f];
+        __stcs(buf + gi, v);
+        V* Rv = reinterpret_cast<V*>(Rb) + gi;
+        const V r = csub(*Rv, v);
+        *Rv = r;
+        stage[cc * lv.pitch + f] = r;
+      }
+      __syncthreads();
+      tile_segments<Real>(stage, lv, b * g.nseg + s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+    } else {
+      for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
+        const int f = i / lv.C, cc = i - f * lv.C;
+        const int64_t gi = base + (int64_t)f * lv.S + cc;
+        V v = out[cc * lv.pitch + f];
+        if (DIR < 0 && lv.E2 > 0) v = cmul(v, cconj(Er(tb, g.eb, lv.E2 * (s0 + cc) * f)));
+        buf[gi] = v;
+      }
     }
     __syncthreads();
   }
 }
 
-// per-signal control: fold extrema partials -> k; decide stop / L
-__global__ void k_ctl_ext(Geo g, Ctl c, int first) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < g.batch; b += (int64_t)gridDim.x * blockDim.x) {
-    if (first) {
-      c.M[b] = 0;
-      c.active[b] = c.bad[b] ? 0 : 1;
-      if (c.bad[b]) c.M[b] = -1;
-    }
+// ------------------------------------------------------------------ a2/a3/a7 fold of extrema partials
+// Groups of segments -> group partials; the last CTA of a signal folds the groups, gets k, and
+// decides.  mode 0: after the forward transform (k of s); mode 1: after IMF M (bookkeeping first).
+template <typename Real>
+__global__ void __launch_bounds__(kThreads) k_fold(Geo g, Ctl c, int mode, int32_t* __restrict__ lens,
+                                                   int32_t* __restrict__ iters) {
+  __shared__ Mono sm[kNW];
+  __shared__ int last;
+  const Real* segv = reinterpret_cast<const Real*>(c.segv);
+  Real* gv = reinterpret_cast<Real*>(c.gv);
+  for (int64_t t = blockIdx.x; t < g.batch * g.ngrp; t += gridDim.x) {
+    const int64_t b = t / g.ngrp, j = t - b * g.ngrp;
     if (!c.active[b]) continue;
-    int F = 0, Ls = 0, C = 0;
-    for (int ch = 0; ch < g.nsch; ++ch) {
-      const int32_t* e = c.ext + (b * g.nsch + ch) * 3;
-      C += e[2] + ((Ls != 0 && e[0] != 0 && Ls != e[0]) ? 1 : 0);
-      if (F == 0) F = e[0];
-      if (e[1] != 0) Ls = e[1];
+    const int64_t s0 = b * g.nseg + j * g.grp, s1 = min(s0 + g.grp, (b + 1) * g.nseg);
+    const Mono m = fold_items<Real>(c.segi, segv, s0, s1, sm);
+    if (threadIdx.x == 0) {
+      c.gi[b * g.ngrp + j] = mpack(m);
+      gv[2 * (b * g.ngrp + j)] = __ldcg(segv + 2 * s0);
+      gv[2 * (b * g.ngrp + j) + 1] = __ldcg(segv + 2 * (s1 - 1) + 1);
+      __threadfence();
+      last = atomicAdd(c.cnt + b, 1u) == (uint32_t)(g.ngrp - 1);
     }
-    c.k[b] = C;
-    if (C < 2 || c.M[b] >= g.max_imfs) {
-      c.active[b] = 0;
-      continue;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      const Mono k = fold_items<Real>(c.gi, gv, b * g.ngrp, (b + 1) * g.ngrp, sm);
+      if (threadIdx.x == 0) {
+        c.cnt[b] = 0;
+        int M = c.M[b];
+        if (mode == 0) {
+          if (c.bad[b]) {
+            c.M[b] = -1;
+            c.active[b] = 0;
+          }
+        } else {
+          lens[b * g.max_imfs + M] = 2 * c.L[b];
+          iters[b * g.max_imfs + M] = c.N[b];
+          c.M[b] = ++M;
+        }
+        if (c.active[b]) {
+          c.k[b] = k.c;
+          if (k.c < 2 || M >= g.max_imfs) c.active[b] = 0;
+          else {
+            c.L[b] = filter_half_length(g, k.c);
+            c.search[b] = 0;
+          }
+        }
+      }
     }
-    const double tq = __dmul_rn(g.xi, (double)g.n);
-    const double u = __ddiv_rn(tq, (double)C);
-    long long q = (long long)floor(u);
-    long long L = g.window ? 2 * q : q;
-    const long long Lmax = (g.n - 1) / 4;
-    if (L < 2) L = 2;
-    if (L > Lmax) L = Lmax;
-    c.L[b] = (int)L;
-    c.search[b] = 0;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ a1 rows (forward) + post-processing
+// Unit u: rows with bases u and (P - u) mod P (one row when they coincide).  After the row DFTs:
+// X_k = E + e^{-2 pi i k/n} O, X_{NC-k} = conj(E - e^{-2 pi i k/n} O), E = (Z_k + conj Z_{NC-k})/2,
+// O = -i (Z_k - conj Z_{NC-k})/2;  X_0 = Re Z_0 + Im Z_0, X_NC = Re Z_0 - Im Z_0 (Nyquist).
+template <typename Real>
+__device__ __forceinline__ void pair_of(const Geo& g, int64_t u, int64_t& ra, int64_t& rb, int64_t& bA, int& two) {
+  bA = u;
+  const int64_t bB = (g.P - u) % g.P;
+  ra = row_of_base(g, bA);
+  rb = row_of_base(g, bB);
+  two = ra != rb;
+}
+// mirror element of t (row a) and whether the pair is processed from t
+__device__ __forceinline__ bool mirror_t(const Geo& g, int64_t bA, int two, int F, int t, int& tm) {
+  if (bA == 0) {
+    tm = t == 0 ? 0 : F - t;
+    return two || t <= tm;
+  }
+  tm = F - 1 - t;
+  return two || t <= tm;
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kThreads) k_rows_fwd(Geo g, Level lv, typename Cx<Real>::V* __restrict__ X,
+                                                       typename Cx<Real>::V* __restrict__ Xn, Tabs<Real> tb,
+                                                       Ctl c) {
+  using V = typename Cx<Real>::V;
+  extern __shared__ __align__(16) char smem_raw[];
+  V* A = reinterpret_cast<V*>(smem_raw);
+  V* Bf = A + 2 * lv.pitch;
+  const int F = lv.F;
+  for (int64_t t = blockIdx.x; t < g.batch * g.units; t += gridDim.x) {
+    const int64_t b = t / g.units, u = t - b * g.units;
+    if (!c.active[b]) continue;
+    int64_t ra, rb, bA;
+    int two;
+    pair_of<Real>(g, u, ra, rb, bA, two);
+    V* Xb = X + b * g.NC;
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      A[i] = Xb[ra * F + i];
+      if (two) A[lv.pitch + i] = Xb[rb * F + i];
+    }
+    V* out = cta_fft<-1>(A, Bf, lv, two ? 2 : 1, tb.tw);
+    V* stage = out == A ? Bf : A;
+    const int ob = two ? lv.pitch : 0;
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      int tm;
+      if (!mirror_t(g, bA, two, F, i, tm)) continue;
+      const int64_t k = bA + g.P * i;
+      const V Pv = out[i], Q = out[ob + tm];
+      if (k == 0) {
+        stage[0] = V{Pv.x + Pv.y, (Real)0};
+        Xn[b] = V{Pv.x - Pv.y, (Real)0};
+        continue;
+      }
+      const Real h = (Real)0.5;
+      const V E = V{h * (Pv.x + Q.x), h * (Pv.y - Q.y)};
+      const V D = V{h * (Pv.x - Q.x), h * (Pv.y + Q.y)};
+      const V O = V{D.y, -D.x};
+      const V TO = cmul(cconj(Er(tb, g.eb, 2 * k)), O);
+      stage[i] = cadd(E, TO);
+      stage[ob + tm] = cconj(csub(E, TO));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      Xb[ra * F + i] = stage[i];
+      if (two) Xb[rb * F + i] = stage[lv.pitch + i];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ a6 damping + pre-processing + row IDFTs
+// d = a^N (a = 1 - w_hat); X <- (1 - d) X; with A = d_k X_k/n, B = d_{NC-k} X_{NC-k}/n:
+// Z_k = S + T, Z_{NC-k} = conj(S - T), S = A + conj B, T = i e^{2 pi i k/n} (A - conj B)
+// (k = 0 pairs with the Nyquist bin), then the length-F IDFT of each row into the IMF slot.
+template <typename Real>
+__global__ void __launch_bounds__(kThreads) k_rows_inv(Geo g, Level lv, Real* __restrict__ imfs,
+                                                       typename Cx<Real>::V* __restrict__ X,
+                                                       typename Cx<Real>::V* __restrict__ Xn, Tabs<Real> tb,
+                                                       Ctl c) {
+  using V = typename Cx<Real>::V;
+  extern __shared__ __align__(16) char smem_raw[];
+  V* A = reinterpret_cast<V*>(smem_raw);
+  V* Bf = A + 2 * lv.pitch;
+  const int F = lv.F;
+  const double invn = 1.0 / (double)g.n;
+  for (int64_t t = blockIdx.x; t < g.batch * g.units; t += gridDim.x) {
+    const int64_t b = t / g.units, u = t - b * g.units;
+    if (!c.active[b]) continue;
+    int64_t ra, rb, bA;
+    int two;
+    pair_of<Real>(g, u, ra, rb, bA, two);
+    const int L = c.L[b], N = c.N[b];
+    V* Xb = X + b * g.NC;
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      A[i] = Xb[ra * F + i];
+      if (two) A[lv.pitch + i] = Xb[rb * F + i];
+    }
+    __syncthreads();
+    const int ob = two ? lv.pitch : 0;
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      int tm;
+      if (!mirror_t(g, bA, two, F, i, tm)) continue;
+      const int64_t k = bA + g.P * i;
+      const int64_t km = g.NC - k;  // NC (Nyquist) for k = 0
+      const V xk = A[i];
+      const V xm = k == 0 ? Xn[b] : A[ob + tm];
+      const double dk = upow_rt(1.0 - what_tab(g, tb, L, k), N);
+      const double dm = upow_rt(1.0 - what_tab(g, tb, L, km), N);
+      const V Av = cscale(xk, (Real)(dk * invn)), Bv = cscale(xm, (Real)(dm * invn));
+      const V S = V{Av.x + Bv.x, Av.y - Bv.y};
+      const V D = V{Av.x - Bv.x, Av.y + Bv.y};
+      const V T = mul_i<1>(cmul(Er(tb, g.eb, 2 * k), D));
+      Bf[i] = cadd(S, T);
+      Xb[ra * F + i] = cscale(xk, (Real)(1.0 - dk));
+      if (k == 0) {
+        Xn[b] = cscale(xm, (Real)(1.0 - dm));
+      } else {
+        Bf[ob + tm] = cconj(csub(S, T));
+        Xb[(two ? rb : ra) * F + tm] = cscale(xm, (Real)(1.0 - dm));
+      }
+    }
+    V* out = cta_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);
+    V* W = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      W[ra * F + i] = out[i];
+      if (two) W[rb * F + i] = out[lv.pitch + i];
+    }
+    __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ a5 probes
-// mode 0: cap probe (P, Q at N = max_inner); mode 1: K-ary probes N_i = lo + i*step, i = 1..kProbes
+// mode 0: cap probe (P, Q at N = max_inner); mode 1: K-ary probes N_i = lo + i*step, i = 1..kProbes.
+// Chunk = rpc rows; the last CTA of a signal folds the chunk partials (fixed order) and decides.
 template <typename Real>
 __global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Real>::V* __restrict__ X,
-                                                    const typename Cx<Real>::V* __restrict__ Xn, Ctl c, int mode) {
+                                                    const typename Cx<Real>::V* __restrict__ Xn, Tabs<Real> tb,
+                                                    Ctl c, int mode) {
   using V = typename Cx<Real>::V;
-  __shared__ double sred[kThreads / 32][2 * kProbes];
+  __shared__ double sred[kNW][2 * kProbes];
+  __shared__ int last;
+  const int F = g.Frow;
   for (int64_t t = blockIdx.x; t < g.batch * g.nbch; t += gridDim.x) {
     const int64_t b = t / g.nbch;
-    const int ch = (int)(t - b * g.nbch);
+    const int64_t ch = t - b * g.nbch;
     if (!c.active[b] || (mode == 1 && !c.search[b])) continue;
     const int L = c.L[b];
     int N0, step, nprobe;
-    if (mode == 0) { N0 = g.max_inner; step = 0; nprobe = 1; }
-    else {
+    if (mode == 0) {
+      N0 = g.max_inner; step = 0; nprobe = 1;
+    } else {
       const int lo = c.lo[b], hi = c.hi[b];
       step = (hi - lo + kProbes) / (kProbes + 1);
       if (step < 1) step = 1;
@@ -373,31 +654,39 @@ __global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Rea
     double acc[2 * kProbes];
 #pragma unroll
     for (int i = 0; i < 2 * kProbes; ++i) acc[i] = 0.0;
-    const int64_t p0 = (int64_t)ch * g.binch, p1 = min(p0 + g.binch, g.NC);
-    for (int64_t p = p0 + threadIdx.x; p < p1 + (ch == 0 ? 1 : 0); p += blockDim.x) {
-      int64_t k;
-      V x;
-      double cw;
-      if (p == p1) { k = g.NC; x = Xn[b]; cw = 1.0; }  // Nyquist (chunk 0 only)
-      else { k = bin_of_pos(g, p); x = X[b * g.NC + p]; cw = (k == 0) ? 1.0 : 2.0; }
-      const double w = what_st(g.n, L, k);
-      const double a = 1.0 - w;
-      const double pk = cw * ((double)x.x * (double)x.x + (double)x.y * (double)x.y);
-      const double pw = pk * w * w;
-      if (mode == 0) {
-        const double e = upow_rt(a, N0 - 1);
-        const double xx = e * e;
-        acc[0] += pk * xx;
-        acc[1] += pw * xx;
-      } else {
-        const double a2 = a * a;
-        double y = upow_rt(a2, N0 - 1);
-        const double z = upow_rt(a2, step);
+    const int64_t r0 = ch * g.rpc, r1 = min(r0 + g.rpc, g.P);
+    const V* Xb = X + b * g.NC;
+    for (int64_t row = r0; row < r1; ++row) {
+      const int64_t base = base_of_row(g, row);
+      for (int i = threadIdx.x; i <= F; i += blockDim.x) {
+        int64_t k;
+        V x;
+        double cw;
+        if (i == F) {  // Nyquist, once per signal
+          if (row != 0) continue;
+          k = g.NC; x = Xn[b]; cw = 1.0;
+        } else {
+          k = base + g.P * i; x = Xb[row * F + i]; cw = k == 0 ? 1.0 : 2.0;
+        }
+        const double w = what_tab(g, tb, L, k);
+        const double a = 1.0 - w;
+        const double pk = cw * ((double)x.x * (double)x.x + (double)x.y * (double)x.y);
+        const double pw = pk * w * w;
+        if (mode == 0) {
+          const double e = upow_rt(a, N0 - 1);
+          const double xx = e * e;
+          acc[0] += pk * xx;
+          acc[1] += pw * xx;
+        } else {
+          const double a2 = a * a;
+          double y = upow_rt(a2, N0 - 1);
+          const double z = upow_rt(a2, step);
 #pragma unroll
-        for (int i = 0; i < kProbes; ++i) {
-          acc[2 * i] += pk * y;
-          acc[2 * i + 1] += pw * y;
-          y *= z;
+          for (int q = 0; q < kProbes; ++q) {
+            acc[2 * q] += pk * y;
+            acc[2 * q + 1] += pw * y;
+            y *= z;
+          }
         }
       }
     }
@@ -412,149 +701,77 @@ __global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Rea
     __syncthreads();
     if (threadIdx.x < nv) {
       double v = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += sred[w][threadIdx.x];
+      for (int w = 0; w < kNW; ++w) v += sred[w][threadIdx.x];
       c.red[(b * g.nbch + ch) * (2 * kProbes) + threadIdx.x] = v;
     }
+    __threadfence();
     __syncthreads();
-  }
-}
-
-// per-signal: fold probe partials (fixed order) and update N / the search bracket
-__global__ void k_ctl_probe(Geo g, Ctl c, int mode) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < g.batch; b += (int64_t)gridDim.x * blockDim.x) {
-    if (!c.active[b]) continue;
-    if (mode == 0) {
-      double P = 0.0, Q = 0.0;
-      for (int ch = 0; ch < g.nbch; ++ch) {
-        P += c.red[(b * g.nbch + ch) * (2 * kProbes) + 0];
-        Q += c.red[(b * g.nbch + ch) * (2 * kProbes) + 1];
+    if (threadIdx.x == 0) last = atomicAdd(c.cnt + b, 1u) == (uint32_t)(g.nbch - 1);
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      // fold the chunk partials: thread-contiguous ranges, then a fixed-order tree
+      double s[2 * kProbes];
+#pragma unroll
+      for (int i = 0; i < 2 * kProbes; ++i) s[i] = 0.0;
+      const int64_t per = (g.nbch + blockDim.x - 1) / blockDim.x;
+      const int64_t a0 = (int64_t)threadIdx.x * per, a1 = min(a0 + per, g.nbch);
+      for (int64_t q = a0; q < a1; ++q)
+        for (int i = 0; i < nv; ++i) s[i] += __ldcg(c.red + (b * g.nbch + q) * (2 * kProbes) + i);
+      __syncthreads();
+      for (int i = 0; i < nv; ++i) {
+        double v = s[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5][i] = v;
       }
-      c.N[b] = g.max_inner;
-      if (Q <= g.delta2 * P) {  // SD(cap) <= delta: search [1, cap)
-        c.lo[b] = 0;
-        c.hi[b] = g.max_inner;
-        c.search[b] = g.max_inner > 1 ? 1 : 0;
-        if (g.max_inner == 1) c.N[b] = 1;
-      }
-    } else {
-      if (!c.search[b]) continue;
-      const int lo = c.lo[b], hi = c.hi[b];
-      int step = (hi - lo + kProbes) / (kProbes + 1);
-      if (step < 1) step = 1;
-      int nlo = lo, nhi = hi;
-      for (int i = 0; i < kProbes; ++i) {
-        const int Ni = lo + step * (i + 1);
-        if (Ni >= hi) break;
-        double P = 0.0, Q = 0.0;
-        for (int ch = 0; ch < g.nbch; ++ch) {
-          P += c.red[(b * g.nbch + ch) * (2 * kProbes) + 2 * i];
-          Q += c.red[(b * g.nbch + ch) * (2 * kProbes) + 2 * i + 1];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double PQ[2 * kProbes];
+        for (int i = 0; i < nv; ++i) {
+          double v = 0.0;
+          for (int w = 0; w < kNW; ++w) v += sred[w][i];
+          PQ[i] = v;
         }
-        if (Q <= g.delta2 * P) { nhi = Ni; break; }
-        nlo = Ni;
+        c.cnt[b] = 0;
+        if (mode == 0) {
+          c.N[b] = g.max_inner;
+          if (PQ[1] <= g.delta2 * PQ[0]) {  // SD(cap) <= delta: search [1, cap)
+            c.lo[b] = 0;
+            c.hi[b] = g.max_inner;
+            c.search[b] = g.max_inner > 1 ? 1 : 0;
+            if (g.max_inner == 1) c.N[b] = 1;
+          }
+        } else {
+          const int lo = c.lo[b], hi = c.hi[b];
+          int nlo = lo, nhi = hi;
+          for (int q = 0; q < kProbes; ++q) {
+            const int Nq = lo + step * (q + 1);
+            if (Nq >= hi) break;
+            if (PQ[2 * q + 1] <= g.delta2 * PQ[2 * q]) { nhi = Nq; break; }
+            nlo = Nq;
+          }
+          c.lo[b] = nlo;
+          c.hi[b] = nhi;
+          if (nhi - nlo <= 1) {
+            c.search[b] = 0;
+            c.N[b] = nhi;
+          }
+        }
       }
-      c.lo[b] = nlo;
-      c.hi[b] = nhi;
-      if (nhi - nlo <= 1) {
-        c.search[b] = 0;
-        c.N[b] = nhi;
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ a6 damping + pre-processing
-// One thread per Hermitian pair (k, NC - k) (threads whose bin k > NC/2 idle; k = 0 pairs with the
-// Nyquist bin): d = a^N, X <- (1 - d) X for both, and with A = d_k X_k / n, B = d_{NC-k} X_{NC-k} / n,
-// Z_k = S + T, Z_{NC-k} = conj(S - T), S = A + B*, T = i e^{2 pi i k/n} (A - B*).
-template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_damp_pre(Geo g, typename Cx<Real>::V* __restrict__ X,
-                                                       typename Cx<Real>::V* __restrict__ Xn,
-                                                       typename Cx<Real>::V* __restrict__ Z, Ctl c) {
-  using V = typename Cx<Real>::V;
-  const int64_t tot = g.batch * g.NC;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = i / g.NC, p = i - b * g.NC;
-    const int64_t k = bin_of_pos(g, p);
-    if (2 * k > g.NC) continue;  // handled by the mirror bin's thread
-    if (!c.active[b]) continue;
-    const int L = c.L[b], N = c.N[b];
-    const int64_t km = g.NC - k;  // == NC (Nyquist) for k = 0
-    const int64_t pm = (k == 0) ? -1 : pos_of_bin(g, km);
-    V* Xb = X + b * g.NC;
-    const V xk = Xb[p];
-    const V xm = (k == 0) ? Xn[b] : Xb[pm];
-    const double dk = upow_rt(1.0 - what_st(g.n, L, k), N);
-    const double dm = upow_rt(1.0 - what_st(g.n, L, km), N);
-    const Real invn = (Real)(1.0 / (double)g.n);
-    const V A = cscale(xk, (Real)dk * invn), B = cscale(xm, (Real)dm * invn);
-    const V S = V{A.x + B.x, A.y - B.y};
-    const V D = V{A.x - B.x, A.y + B.y};
-    const V Tm = mul_i<1>(cmul(cis<V>(k, g.n, +1), D));
-    V* Zb = Z + b * g.NC;
-    Zb[p] = cadd(S, Tm);
-    Xb[p] = cscale(xk, (Real)(1.0 - dk));
-    if (k == 0) {
-      Xn[b] = cscale(xm, (Real)(1.0 - dm));
-    } else if (km != k) {
-      Zb[pm] = cconj(csub(S, Tm));
-      Xb[pm] = cscale(xm, (Real)(1.0 - dm));
-    }
-  }
-}
-
-// inverse columns (step A'): DFT(+1) over k1 of column m2 -> natural-order z[N2 m1 + m2];
-// epilogue: IMF pair (Re, Im) -> imfs slot M, R -= IMF.
-template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_inv_cols(Geo g, const typename Cx<Real>::V* __restrict__ Z,
-                                                       const typename Cx<Real>::V* __restrict__ tw1,
-                                                       Real* __restrict__ imfs, Real* __restrict__ R,
-                                                       int64_t sig_stride, Ctl c) {
-  using V = typename Cx<Real>::V;
-  extern __shared__ __align__(16) char smem_raw[];
-  V* A = reinterpret_cast<V*>(smem_raw);
-  V* Bf = A + (size_t)g.N1 * g.C;
-  const int64_t tiles = g.N2 / g.C;
-  for (int64_t t = blockIdx.x; t < g.batch * tiles; t += gridDim.x) {
-    const int64_t b = t / tiles, c0 = (t - b * tiles) * g.C;
-    if (!c.active[b]) continue;
-    const V* Zb = Z + b * g.NC;
-    for (int i = threadIdx.x; i < g.N1 * g.C; i += blockDim.x) {
-      const int k1 = i / g.C, cc = i - k1 * g.C;
-      A[cc * g.N1 + k1] = Zb[(int64_t)k1 * g.N2 + c0 + cc];
-    }
-    V* out = cta_fft<1>(A, Bf, g.N1, g.C, g.rad1, g.np1, tw1);
-    V* imf = reinterpret_cast<V*>(imfs + b * sig_stride + (int64_t)c.M[b] * g.n);
-    V* Rb = reinterpret_cast<V*>(R + b * sig_stride);
-    for (int i = threadIdx.x; i < g.N1 * g.C; i += blockDim.x) {
-      const int m1 = i / g.C, cc = i - m1 * g.C;
-      const int64_t m = (int64_t)g.N2 * m1 + c0 + cc;
-      const V v = out[cc * g.N1 + m1];
-      __stcs(imf + m, v);
-      Rb[m] = csub(Rb[m], v);
     }
     __syncthreads();
   }
 }
 
-// per-signal bookkeeping after an IMF
-__global__ void k_ctl_done(Geo g, Ctl c, int32_t* lens, int32_t* iters) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < g.batch; b += (int64_t)gridDim.x * blockDim.x) {
-    if (!c.active[b]) continue;
-    const int M = c.M[b];
-    lens[b * g.max_imfs + M] = 2 * c.L[b];
-    iters[b * g.max_imfs + M] = c.N[b];
-    c.M[b] = M + 1;
-  }
-}
-
-// final: trend (R lives in slot max_imfs) to slot M, zeros after; counts; zero lens/iters past M
+// ------------------------------------------------------------------ a7 final
+// trend (R lives in slot max_imfs) to slot M, zeros after; counts; zero lens/iters past M
 template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_final(Geo g, Real* __restrict__ imfs, int64_t sig_stride, Ctl c,
-                                                    int32_t* count, int32_t* lens, int32_t* iters) {
+__global__ void __launch_bounds__(kThreads) k_final(Geo g, Real* __restrict__ imfs, Ctl c, int32_t* count,
+                                                    int32_t* lens, int32_t* iters) {
   for (int64_t t = blockIdx.x; t < g.batch; t += gridDim.x) {
     const int M = c.M[t];
-    Real* base = imfs + t * sig_stride;
+    Real* base = imfs + t * g.sig_stride;
     const Real* R = base + (int64_t)g.max_imfs * g.n;
     if (M < 0) {  // non-finite input
       for (int64_t i = threadIdx.x; i < (int64_t)(g.max_imfs + 1) * g.n; i += blockDim.x) base[i] = (Real)0;
@@ -566,7 +783,10 @@ __global__ void __launch_bounds__(kThreads) k_final(Geo g, Real* __restrict__ im
         base[i] = (Real)0;
     }
     for (int m = threadIdx.x; m < g.max_imfs; m += blockDim.x)
-      if (m >= M) { lens[t * g.max_imfs + m] = 0; iters[t * g.max_imfs + m] = 0; }
+      if (m >= M) {
+        lens[t * g.max_imfs + m] = 0;
+        iters[t * g.max_imfs + m] = 0;
+      }
     if (threadIdx.x == 0) count[t] = M;
     __syncthreads();
   }

@@ -129,3 +129,25 @@ def test_streamed_host_path():
     for a, b in zip(dev, outs):
         np.testing.assert_array_equal(a, b.numpy())
     plan.close()
+
+
+@pytest.mark.parametrize("n,rowmax,colmax", [(4096, 16, 16), (4096, 16, 8), (15360, 30, 16), (3 << 12, 24, 8)])
+def test_streamed_multilevel_vs_td_oracle(n, rowmax, colmax, monkeypatch):
+    """3- and 4-level geometries (forced by capping the level lengths) against the literal oracle."""
+    monkeypatch.setenv("FIF_ST_ROWMAX", str(rowmax))
+    monkeypatch.setenv("FIF_ST_COLMAX", str(colmax))
+    s = np.stack([signals.tones_signal(n, 26, i) for i in range(3)])
+    gpu = run_gpu(s, regime=ST)
+    ref = oracle.decompose(s)
+    for b in range(3):
+        assert_parity(s[b], gpu, ref, b, b)
+
+
+def test_streamed_long_single_signal_3level():
+    """One cfg3-recipe signal of n = 2^23 (3-level geometry, batch 1) against the direct form."""
+    n = 1 << 23
+    s = signals.cfg3_signal(0, n=n)[None, :]
+    gpu = run_gpu(s)
+    ref = df.decompose_batch(s)
+    assert_parity(s[0], gpu, ref, 0, 0)
+    assert np.abs(gpu[0][0].sum(axis=0) - s[0]).max() <= 1e-11 * np.abs(s).max()
