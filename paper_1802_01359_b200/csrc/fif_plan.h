@@ -1,0 +1,92 @@
+// fif_plan.h -- internal: the plan object shared by the translation units of libfif_b200.so
+// (fif.cu: C ABI; fif_res_f64.cu / fif_res_f32.cu: resident-regime launchers; fif_st.cu: streamed
+// regime host code).  Not part of the public ABI (include/fif.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/fif.h"
+#include "fif_streamed.cuh"
+
+namespace fifhost {
+
+enum { FIF_MAX_STAGES = 3 };
+// max_inner value with a compile-time-specialised kernel (the paper's/BASELINE's cap of 200,
+// PAPER.md:433 "limit on the maximal number of iterations"); any other value uses the generic kernel
+constexpr int kFastCap = 200;
+
+struct Staging {
+  void* d_in = nullptr;
+  void* d_out = nullptr;
+  int32_t* d_meta = nullptr;  // count | lens | iters
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+};
+
+}  // namespace fifhost
+
+struct fif_plan_s {
+  int64_t n = 0, batch = 0;
+  fif_dtype dtype = FIF_F64;
+  fif_window window = FIF_WINDOW_TRI_SQ;
+  double xi = 1.6, delta = 1e-3;
+  int32_t max_inner = 200, max_imfs = 10;
+  int device = 0, num_sms = 0;
+  int NC = 0;
+  void* d_sin = nullptr;   // Real[NC+1]  sin(pi j/n)
+  void* d_isin = nullptr;  // Real[NC+1]  1/sin(pi j/n) (j >= 1)
+  void* d_tw = nullptr;    // V[twtotal]  Stockham twiddles e^{-2 pi i k r/(NS RP)}
+  int block = 0, occ = 0;
+  size_t smem = 0;
+  int regime = 0;  // 0 resident, 1 streamed
+  // streamed regime
+  fifgpu::st::Geo geo{};
+  void* d_Eh = nullptr;   // double2 e^{i pi (h 2^eb)/n}
+  void* d_El = nullptr;   // double2 e^{i pi l/n}
+  void* d_Th = nullptr;   // V (Real) copies
+  void* d_Tl = nullptr;
+  void* d_twl = nullptr;  // V per-level Stockham twiddles
+  void* d_X = nullptr;    // V[B][NC] spectrum (digit-reversed multi-level order)
+  void* d_Xn = nullptr;   // V[B] Nyquist bins
+  void* d_ctl = nullptr;  // per-signal control arrays + partials
+  fifgpu::st::Ctl ctl{};
+  int st_rounds = 0, st_grid = 0, st_grid_col = 0, st_grid_rows = 0, st_grid_probe = 0;
+  int64_t st_wave = 1;
+  cudaStream_t st_streams[2] = {nullptr, nullptr};  // waves alternate between these
+  cudaEvent_t st_ev[3] = {nullptr, nullptr, nullptr};
+  size_t st_smem_col[fifgpu::st::kMaxLev] = {}, st_smem_rows = 0;
+  // host (e2e) path staging
+  int64_t chunk = 0;
+  int nstages = 0;
+  fifhost::Staging st[fifhost::FIF_MAX_STAGES];
+};
+
+namespace fifhost {
+using fifgpu::Cx;
+// resident regime: per-(dtype, NC) launchers (fif_res_f64.cu, fif_res_f32.cu)
+struct ResOps {
+  cudaError_t (*prepare)();
+  int (*occupancy)();
+  int threads;
+  size_t smem;
+  void (*decompose)(const fif_plan_s*, const void*, void*, int32_t*, int32_t*, int32_t*, int64_t, cudaStream_t);
+  void (*test_rfft)(const fif_plan_s*, const void*, void*, int64_t, cudaStream_t);
+  void (*test_irfft)(const fif_plan_s*, const void*, void*, int64_t, cudaStream_t);
+  void (*test_extrema)(const fif_plan_s*, const void*, int32_t*, int64_t, cudaStream_t);
+  void (*test_window)(const fif_plan_s*, int, void*, cudaStream_t);
+  void (*test_inner)(const fif_plan_s*, int, const void*, void*, int32_t*, int64_t, cudaStream_t);
+};
+const ResOps* res_ops_f64(int NC);
+const ResOps* res_ops_f32(int NC);
+inline const ResOps* res_ops(fif_dtype dt, int NC) { return dt == FIF_F64 ? res_ops_f64(NC) : res_ops_f32(NC); }
+
+// streamed regime (fif_st.cu)
+bool st_geometry(int64_t n, bool f64, fifgpu::st::Geo& g);
+fif_status st_setup(fif_plan_s* p);
+// signals [0, batch) of the call use the plan's work buffers from signal `boff` on
+void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
+                  int64_t batch, int64_t boff, cudaStream_t s);
+int st_kernels_per_call(const fif_plan_s* p);
+void st_free(fif_plan_s* p);
+}  // namespace fifhost

@@ -1,0 +1,106 @@
+// fif_res_impl.cuh -- resident-regime launchers for one element type (included by fif_res_f64.cu
+// and fif_res_f32.cu, which compile in parallel).  Kernels: fif_resident.cuh.
+#pragma once
+#include "fif_plan.h"
+
+namespace fifhost {
+using namespace fifgpu;
+
+template <typename Real, int NC>
+struct Inst {
+  using K = Resident<Real, NC>;
+  using V = typename Cx<Real>::V;
+  static cudaError_t prepare() {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, kFastCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, kFastCap>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem_bytes)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(fif_test_rfft_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_irfft_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_extrema_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_window_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    return cudaSuccess;
+  }
+  static int occupancy() {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC, kFastCap>, K::T, K::smem_bytes);
+    return occ;
+  }
+  static void decompose(const fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
+                        int64_t batch, cudaStream_t s) {
+    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
+    const int64_t cap = (int64_t)p->num_sms * p->occ;
+    const int grid = (int)(batch < cap ? batch : cap);
+    if (p->max_inner == kFastCap)
+      fif_resident_kernel<Real, NC, kFastCap><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
+    else
+      fif_resident_kernel<Real, NC, 0><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
+  }
+  static void test_rfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    fif_test_rfft_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
+        (const Real*)in, (Real*)out, batch, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw);
+  }
+  static void test_irfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    fif_test_irfft_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>(
+        (const Real*)in, (Real*)out, batch, (const Real*)p->d_sin, (const Real*)p->d_isin, (const V*)p->d_tw);
+  }
+  static void test_extrema(const fif_plan_s* p, const void* in, int32_t* k, int64_t batch, cudaStream_t s) {
+    (void)p;
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    fif_test_extrema_kernel<Real, NC><<<grid, K::T, K::smem_bytes, s>>>((const Real*)in, k, batch);
+  }
+  static void test_window(const fif_plan_s* p, int L, void* out, cudaStream_t s) {
+    fif_test_window_kernel<Real, NC><<<1, K::T, K::smem_bytes, s>>>((Real*)out, L, (const Real*)p->d_sin,
+                                                                        (const Real*)p->d_isin);
+  }
+  static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
+                         cudaStream_t s) {
+    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window};
+    const int grid = (int)(batch < 4096 ? batch : 4096);
+    if (p->max_inner == kFastCap)
+      fif_test_inner_kernel<Real, NC, kFastCap><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)in, (Real*)out, N, batch, L, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
+    else
+      fif_test_inner_kernel<Real, NC, 0><<<grid, K::T, K::smem_bytes, s>>>(
+          (const Real*)in, (Real*)out, N, batch, L, (const Real*)p->d_sin, (const Real*)p->d_isin,
+          (const V*)p->d_tw, prm);
+  }
+};
+
+
+template <typename Real, int NC>
+const ResOps* res_entry() {
+  using I = Inst<Real, NC>;
+  static const ResOps ops{&I::prepare, &I::occupancy, I::K::T, I::K::smem_bytes, &I::decompose, &I::test_rfft,
+                          &I::test_irfft, &I::test_extrema, &I::test_window, &I::test_inner};
+  return &ops;
+}
+template <typename Real>
+const ResOps* res_table(int NC) {
+  switch (NC) {
+    case 256: return res_entry<Real, 256>();
+    case 512: return res_entry<Real, 512>();
+    case 1024: return res_entry<Real, 1024>();
+    case 2048: return res_entry<Real, 2048>();
+    case 4096: return res_entry<Real, 4096>();
+    default: return nullptr;
+  }
+}
+}  // namespace fifhost

@@ -1,0 +1,347 @@
+// fif_st.cu -- host side of the streamed regime (fif_streamed.cuh): geometry, tables, L2 waves and
+// the per-IMF kernel sequence.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <utility>
+#include <vector>
+
+#include "fif_plan.h"
+
+namespace fifhost {
+using namespace fifgpu;
+namespace {
+// ---------------------------------------------------------------- streamed regime (fif_streamed.cuh)
+bool smooth235(int64_t x) {
+  if (x < 1) return false;
+  for (int f : {2, 3, 5})
+    while (x % f == 0) x /= f;
+  return x == 1;
+}
+// radix schedule: 8s, then the leftover power of two (4 or 2), then 3s and 5s
+int radices(int64_t N, int* rad) {
+  int np = 0, a = 0;
+  while (N % 2 == 0) { N /= 2; ++a; }
+  while (a >= 3) { rad[np++] = 8; a -= 3; }
+  if (a == 2) rad[np++] = 4;
+  if (a == 1) rad[np++] = 2;
+  while (N % 3 == 0) { N /= 3; rad[np++] = 3; }
+  while (N % 5 == 0) { N /= 5; rad[np++] = 5; }
+  return np;
+}
+// split x into m factors, each smooth and in [2, fmax], largest first
+bool split_factors(int64_t x, int m, int64_t fmax, std::vector<int64_t>& out) {
+  if (m == 1) {
+    if (x >= 2 && x <= fmax && smooth235(x)) { out.push_back(x); return true; }
+    return false;
+  }
+  for (int64_t d = fmax < x ? fmax : x; d >= 2; --d) {
+    if (x % d || !smooth235(d)) continue;
+    out.push_back(d);
+    if (split_factors(x / d, m - 1, fmax, out)) return true;
+    out.pop_back();
+  }
+  return false;
+}
+}  // namespace
+// Multi-level geometry: NC = F_0 ... F_{L-1}; the row level holds a mirror pair of rows (2 F_{L-1}
+// complex values per smem buffer), the column levels F_i C_i values with C_i >= 128 B of columns.
+bool st_geometry(int64_t n, bool f64, st::Geo& g) {
+  const int64_t NC = n / 2;
+  const int64_t Emax = f64 ? 2048 : 4096;
+  int64_t rowmax = Emax / 2, colmax = Emax / (f64 ? 8 : 16);
+  // test-only knobs: smaller level lengths force 3- and 4-level geometries at small n
+  if (getenv("FIF_ST_ROWMAX")) rowmax = atoll(getenv("FIF_ST_ROWMAX"));
+  if (getenv("FIF_ST_COLMAX")) colmax = atoll(getenv("FIF_ST_COLMAX"));
+  if (n % 2 || NC < 4 || !smooth235(NC)) return false;
+  for (int L = 2; L <= st::kMaxLev; ++L) {
+    for (int64_t row = rowmax < NC / 2 ? rowmax : NC / 2; row >= 2; --row) {
+      if (NC % row || !smooth235(row)) continue;
+      std::vector<int64_t> f;
+      if (!split_factors(NC / row, L - 1, colmax, f)) continue;
+      // level 0 gets the smallest factor (widest tiles: long extrema segments, coalesced rows)
+      std::vector<int64_t> F(f.rbegin(), f.rend());
+      F.push_back(row);
+      g = st::Geo{};
+      g.n = n; g.NC = NC; g.L = L;
+      int twoff = 0;
+      for (int i = 0; i < L; ++i) {
+        st::Level& lv = g.lv[i];
+        lv.F = (int)F[i];
+        int64_t S = 1;
+        for (int j = i + 1; j < L; ++j) S *= F[j];
+        lv.S = S;
+        lv.A = NC / (F[i] * S);
+        lv.E2 = 2 * n / (F[i] * S);
+        lv.np = radices(F[i], lv.rad);
+        lv.twoff = twoff;
+        twoff += lv.F;
+        if (i < L - 1) {
+          int64_t cmax = Emax / F[i], C = 1;
+          for (int64_t c = cmax < S ? cmax : S; c >= 1; --c)
+            if (S % c == 0) { C = c; break; }
+          lv.C = (int)C;
+          lv.pitch = lv.F + 1;
+          lv.tiles = lv.A * S / C;
+        } else {
+          lv.C = 2;
+          lv.pitch = lv.F;
+          lv.tiles = 0;
+        }
+        g.Fd[i] = lv.F;
+        g.Pd[i] = i == 0 ? 1 : g.Pd[i - 1] * F[i - 1];
+        g.Sr[i] = S / row;
+      }
+      g.Frow = (int)row;
+      g.P = NC / row;
+      g.units = g.P / 2 + 1;
+      g.nseg = NC / g.lv[0].C;
+      g.grp = 2048;
+      g.ngrp = (g.nseg + g.grp - 1) / g.grp;
+      g.rpc = 2;
+      g.nbch = g.units;  // one probe CTA per row-pair unit
+      int bits = 0;
+      while ((1LL << bits) < 2 * n + 1) ++bits;
+      g.eb = (bits + 1) / 2;
+      return true;
+    }
+  }
+  return false;
+}
+namespace {
+template <typename Real>
+fif_status st_tables(fif_plan_s* p) {
+  using V = typename Cx<Real>::V;
+  const long double PI = 3.141592653589793238462643383279502884L;
+  const st::Geo& g = p->geo;
+  const int64_t nh = (2 * g.n >> g.eb) + 1, nl = 1LL << g.eb;
+  auto cis = [&](int64_t j) {  // e^{i pi j/n}, argument reduced to [0, pi/4] for accuracy
+    const int64_t n = g.n, j2 = j % (2 * n);
+    // angle pi j2/n; use symmetry: quadrant q = floor(2 j2 / n)
+    long double c = cosl(PI * (long double)j2 / (long double)n), s = sinl(PI * (long double)j2 / (long double)n);
+    return std::pair<long double, long double>(c, s);
+  };
+  std::vector<double2> Eh(nh), El(nl);
+  std::vector<V> Th(nh), Tl(nl);
+  for (int64_t h = 0; h < nh; ++h) {
+    auto cs = cis(h << g.eb);
+    Eh[h] = double2{(double)cs.first, (double)cs.second};
+    Th[h] = V{(Real)cs.first, (Real)cs.second};
+  }
+  for (int64_t l = 0; l < nl; ++l) {
+    auto cs = cis(l);
+    El[l] = double2{(double)cs.first, (double)cs.second};
+    Tl[l] = V{(Real)cs.first, (Real)cs.second};
+  }
+  std::vector<V> tw;
+  for (int i = 0; i < g.L; ++i)
+    for (int j = 0; j < g.lv[i].F; ++j) {
+      const long double th = 2.0L * PI * (long double)j / (long double)g.lv[i].F;
+      tw.push_back(V{(Real)cosl(th), (Real)(-sinl(th))});
+    }
+  auto up = [](void** d, const void* h, size_t bytes) {
+    if (cudaMalloc(d, bytes) != cudaSuccess) return FIF_ERR_OOM;
+    return cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice) == cudaSuccess ? FIF_OK : FIF_ERR_CUDA;
+  };
+  fif_status s;
+  if ((s = up(&p->d_Eh, Eh.data(), sizeof(double2) * nh)) != FIF_OK) return s;
+  if ((s = up(&p->d_El, El.data(), sizeof(double2) * nl)) != FIF_OK) return s;
+  if ((s = up(&p->d_Th, Th.data(), sizeof(V) * nh)) != FIF_OK) return s;
+  if ((s = up(&p->d_Tl, Tl.data(), sizeof(V) * nl)) != FIF_OK) return s;
+  if ((s = up(&p->d_twl, tw.data(), sizeof(V) * tw.size())) != FIF_OK) return s;
+  return FIF_OK;
+}
+template <typename K>
+int occ_grid(const fif_plan_s* p, K kern, size_t smem) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, st::kThreads, smem);
+  return p->num_sms * (occ > 0 ? occ : 1);
+}
+template <typename Real>
+fif_status st_setup_t(fif_plan_s* p) {
+  using V = typename Cx<Real>::V;
+  st::Geo& g = p->geo;
+  if (!st_geometry(p->n, sizeof(Real) == 8, g)) return FIF_ERR_UNSUPPORTED_N;
+  g.batch = p->batch;
+  g.max_imfs = p->max_imfs; g.max_inner = p->max_inner; g.window = (int)p->window;
+  g.xi = p->xi; g.delta2 = p->delta * p->delta;
+  g.sig_stride = (int64_t)(p->max_imfs + 1) * p->n;
+  p->st_rounds = 0;  // K-ary rounds: the bracket shrinks from cap to ceil(len / (kProbes + 1)) per round
+  for (int64_t len = p->max_inner; len > 1; len = (len + st::kProbes) / (st::kProbes + 1)) ++p->st_rounds;
+  fif_status s = st_tables<Real>(p);
+  if (s != FIF_OK) return s;
+  // L2 waves: the working set of a signal (spectrum, remainder, IMF slot: 3 n b bytes) of a wave
+  // of signals stays in the 126 MB L2 across the passes of an IMF
+  const double wave_mb = getenv("FIF_WAVE_MB") ? atof(getenv("FIF_WAVE_MB")) : 1024.0;
+  const int64_t per_sig = 3 * p->n * (int64_t)sizeof(Real);
+  int64_t wave = (int64_t)(wave_mb * 1048576.0 / (double)per_sig);
+  if (wave < 1) wave = 1;
+  const int64_t B = p->batch > 0 ? p->batch : 1;
+  if (wave > B) wave = B;
+  p->st_wave = wave;
+  const size_t ni = (size_t)B * 10;
+  const size_t segb = (size_t)B * g.nseg * (sizeof(uint32_t) + 2 * sizeof(Real));
+  const size_t grpb = (size_t)B * g.ngrp * (sizeof(uint32_t) + 2 * sizeof(Real));
+  const size_t redb = (size_t)B * g.nbch * 2 * st::kProbes * sizeof(double);
+  const size_t ctl_bytes = ni * sizeof(int32_t) + segb + grpb + redb + 256;
+  if (cudaMalloc(&p->d_X, sizeof(V) * B * g.NC) != cudaSuccess || cudaMalloc(&p->d_Xn, sizeof(V) * B) != cudaSuccess ||
+      cudaMalloc(&p->d_ctl, ctl_bytes) != cudaSuccess)
+    return FIF_ERR_OOM;
+  char* q = (char*)p->d_ctl;
+  auto take = [&](size_t bytes) {
+    char* r = q;
+    q += (bytes + 15) & ~(size_t)15;
+    return (void*)r;
+  };
+  st::Ctl& c = p->ctl;
+  c.red = (double*)take(redb);
+  c.segv = take((size_t)B * g.nseg * 2 * sizeof(Real));
+  c.gv = take((size_t)B * g.ngrp * 2 * sizeof(Real));
+  c.segi = (uint32_t*)take((size_t)B * g.nseg * sizeof(uint32_t));
+  c.gi = (uint32_t*)take((size_t)B * g.ngrp * sizeof(uint32_t));
+  int32_t* ip = (int32_t*)take(ni * sizeof(int32_t));
+  c.k = ip; c.L = ip + B; c.N = ip + 2 * B; c.M = ip + 3 * B; c.active = ip + 4 * B; c.search = ip + 5 * B;
+  c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B);
+  if (cudaMemset(p->d_ctl, 0, ctl_bytes) != cudaSuccess) return FIF_ERR_CUDA;
+  // shared memory and grids
+  for (int i = 0; i < g.L - 1; ++i) p->st_smem_col[i] = 2 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch;
+  p->st_smem_rows = 2 * sizeof(V) * 2 * (size_t)g.lv[g.L - 1].pitch;
+  size_t smax = p->st_smem_rows;
+  for (int i = 0; i < g.L - 1; ++i) smax = smax > p->st_smem_col[i] ? smax : p->st_smem_col[i];
+  cudaError_t e = cudaSuccess;
+  auto attr = [&](auto kern) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+  };
+  attr(st::k_col<Real, -1, st::PASS_FWD_FIRST>);
+  attr(st::k_col<Real, -1, st::PASS_MID>);
+  attr(st::k_col<Real, 1, st::PASS_MID>);
+  attr(st::k_col<Real, 1, st::PASS_INV_LAST>);
+  attr(st::k_rows_fwd<Real>);
+  attr(st::k_rows_inv<Real, 0>);
+  attr(st::k_rows_inv<Real, kFastCap>);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "fif: streamed setup failed: %s\n", cudaGetErrorString(e));
+    return FIF_ERR_CUDA;
+  }
+  p->st_grid_col = occ_grid(p, st::k_col<Real, 1, st::PASS_INV_LAST>, smax);
+  p->st_grid_rows = occ_grid(p, st::k_rows_inv<Real, kFastCap>, p->st_smem_rows);
+  p->st_grid_probe = occ_grid(p, st::k_probe<Real, kFastCap, 1>, 0);
+  p->st_grid = p->st_grid_rows;
+  for (int i = 0; i < 2; ++i)
+    if (cudaStreamCreateWithFlags(&p->st_streams[i], cudaStreamNonBlocking) != cudaSuccess) return FIF_ERR_CUDA;
+  for (int i = 0; i < 3; ++i)
+    if (cudaEventCreateWithFlags(&p->st_ev[i], cudaEventDisableTiming) != cudaSuccess) return FIF_ERR_CUDA;
+  p->block = st::kThreads;
+  p->smem = smax;
+  p->occ = 1;
+  return FIF_OK;
+}
+
+// Ctl / geometry of the wave of signals [b0, b0 + nb)
+st::Ctl ctl_at(const st::Ctl& c, const st::Geo& g, int64_t b0, size_t rsz) {
+  st::Ctl r = c;
+  r.k += b0; r.L += b0; r.N += b0; r.M += b0; r.active += b0; r.search += b0; r.lo += b0; r.hi += b0;
+  r.bad += b0; r.cnt += b0;
+  r.segi += b0 * g.nseg;
+  r.segv = (char*)c.segv + b0 * g.nseg * 2 * rsz;
+  r.gi += b0 * g.ngrp;
+  r.gv = (char*)c.gv + b0 * g.ngrp * 2 * rsz;
+  r.red += b0 * g.nbch * 2 * st::kProbes;
+  return r;
+}
+int grid_for(int64_t work, int cap) { return (int)(work < cap ? (work > 0 ? work : 1) : cap); }
+
+// the whole decomposition as stream-ordered kernels (no host synchronisation), one L2 wave at a time
+template <typename Real>
+void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its, int64_t batch,
+                    int64_t boff, cudaStream_t s) {
+  using V = typename Cx<Real>::V;
+  const int TB = st::kThreads;
+  const st::Tabs<Real> tb{(const double2*)p->d_Eh, (const double2*)p->d_El, (const V*)p->d_Th, (const V*)p->d_Tl,
+                          (const V*)p->d_twl};
+  // waves alternate between two internal streams (independent signals: their latency-bound kernels
+  // overlap), joined back into the caller's stream at the end
+  const int64_t nw = (batch + p->st_wave - 1) / p->st_wave;
+  const int nstream = nw > 1 ? 2 : 1;
+  cudaStream_t user = s;
+  if (nstream > 1) {
+    cudaEventRecord(p->st_ev[0], user);
+    for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(p->st_streams[i], p->st_ev[0], 0);
+  }
+  for (int64_t b0 = 0, w = 0; b0 < batch; b0 += p->st_wave, ++w) {
+    s = nstream > 1 ? p->st_streams[w & 1] : user;
+    st::Geo g = p->geo;
+    g.batch = batch - b0 < p->st_wave ? batch - b0 : p->st_wave;
+    const st::Ctl c = ctl_at(p->ctl, g, boff + b0, sizeof(Real));
+    const Real* sg = (const Real*)sig + b0 * g.n;
+    Real* out = (Real*)imfs + b0 * g.sig_stride;
+    V* X = (V*)p->d_X + (boff + b0) * g.NC;
+    V* Xn = (V*)p->d_Xn + boff + b0;
+    int32_t* ln = lens + b0 * g.max_imfs;
+    int32_t* it = its + b0 * g.max_imfs;
+    const int Lv = g.L;
+    const bool fast = g.max_inner == kFastCap;
+    const st::Level& top = g.lv[Lv - 1];
+    const int gcol = p->st_grid_col, grow = grid_for(g.batch * g.units, p->st_grid_rows);
+    const int gprobe = grid_for(g.batch * g.nbch, p->st_grid_probe);
+    const int gfold = grid_for(g.batch * g.ngrp, p->num_sms * 4);
+    const int gsig = (int)((g.batch + TB - 1) / TB);
+    auto col = [&](int i) { return grid_for(g.batch * g.lv[i].tiles, gcol); };
+    st::k_init<<<gsig, TB, 0, s>>>(g, c);
+    st::k_col<Real, -1, st::PASS_FWD_FIRST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], sg, out, X, tb, c);
+    st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
+    for (int i = 1; i < Lv - 1; ++i)
+      st::k_col<Real, -1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], sg, out, X, tb, c);
+    st::k_rows_fwd<Real><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
+    for (int m = 0; m < g.max_imfs; ++m) {
+      if (fast) {
+        st::k_probe<Real, kFastCap, 0><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
+        for (int r = 0; r < p->st_rounds; ++r) st::k_probe<Real, kFastCap, 1><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
+        st::k_rows_inv<Real, kFastCap><<<grow, TB, p->st_smem_rows, s>>>(g, top, out, X, Xn, tb, c);
+      } else {
+        st::k_probe<Real, 0, 0><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
+        for (int r = 0; r < p->st_rounds; ++r) st::k_probe<Real, 0, 1><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
+        st::k_rows_inv<Real, 0><<<grow, TB, p->st_smem_rows, s>>>(g, top, out, X, Xn, tb, c);
+      }
+      for (int i = Lv - 2; i >= 1; --i)
+        st::k_col<Real, 1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], sg, out, X, tb, c);
+      st::k_col<Real, 1, st::PASS_INV_LAST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], sg, out, X, tb, c);
+      st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 1, ln, it);
+    }
+    st::k_final<Real><<<grid_for(g.batch, p->num_sms * 4), TB, 0, s>>>(g, out, c, cnt + b0, ln, it);
+  }
+  if (nstream > 1)
+    for (int i = 0; i < 2; ++i) {
+      cudaEventRecord(p->st_ev[1 + i], p->st_streams[i]);
+      cudaStreamWaitEvent(user, p->st_ev[1 + i], 0);
+    }
+}
+}  // namespace
+int st_kernels_per_call(const fif_plan_s* p) {
+  const int L = p->geo.L;
+  const int64_t waves = p->batch > 0 ? (p->batch + p->st_wave - 1) / p->st_wave : 0;
+  return (int)(waves * (2 + (L - 1) + 1 + p->max_imfs * (1 + p->st_rounds + L + 1) + 1));
+}
+
+fif_status st_setup(fif_plan_s* p) { return p->dtype == FIF_F64 ? st_setup_t<double>(p) : st_setup_t<float>(p); }
+void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
+                  int64_t batch, int64_t boff, cudaStream_t s) {
+  if (p->dtype == FIF_F64) st_decompose_t<double>(p, sig, imfs, cnt, lens, its, batch, boff, s);
+  else st_decompose_t<float>(p, sig, imfs, cnt, lens, its, batch, boff, s);
+}
+void st_free(fif_plan_s* p) {
+  cudaFree(p->d_Eh);
+  cudaFree(p->d_El);
+  cudaFree(p->d_Th);
+  cudaFree(p->d_Tl);
+  cudaFree(p->d_twl);
+  cudaFree(p->d_X);
+  cudaFree(p->d_Xn);
+  cudaFree(p->d_ctl);
+  for (int i = 0; i < 2; ++i)
+    if (p->st_streams[i]) cudaStreamDestroy(p->st_streams[i]);
+  for (int i = 0; i < 3; ++i)
+    if (p->st_ev[i]) cudaEventDestroy(p->st_ev[i]);
+}
+}  // namespace fifhost

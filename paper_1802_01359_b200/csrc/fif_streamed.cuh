@@ -69,8 +69,8 @@ struct Geo {
   int64_t nseg;          // extrema segments per signal = NC / C_0 (each 2 C_0 consecutive samples)
   int64_t grp;           // segments per fold group
   int64_t ngrp;          // fold groups per signal
-  int64_t rpc;           // probe: rows per chunk
-  int64_t nbch;          // probe chunks per signal
+  int64_t rpc;           // (unused)
+  int64_t nbch;          // probe chunks per signal (= units)
   int eb;                // E table split: E(j) = Eh[j >> eb] * El[j & (2^eb - 1)]
   int max_imfs, max_inner, window;
   double xi, delta2;
@@ -215,6 +215,48 @@ __device__ __forceinline__ double what_tab(const Geo& g, const Tabs<Real>& tb, i
   const double s2 = s * s;
   return s2 * s2;
 }
+// x mod n for 0 <= x < 2^53 (one fp64 multiply by 1/n, one correction step)
+__device__ __forceinline__ int64_t mod_n(int64_t x, int64_t n, double invn) {
+  const int64_t q = (int64_t)((double)x * invn);
+  int64_t m = x - q * n;
+  if (m < 0) m += n;
+  else if (m >= n) m -= n;
+  return m;
+}
+// a4 for a Hermitian pair (k, NC - k), 0 <= k < NC: one division for both bins.
+// L (NC - k) = L NC - L k, and L NC = 0 (L even) or NC (L odd) mod n.
+template <typename Real>
+__device__ __forceinline__ void what_pair(const Geo& g, const Tabs<Real>& tb, int L, double invn, int64_t k,
+                                          double& wk, double& wm) {
+  const int64_t km = g.NC - k;
+  const int64_t mk = mod_n((int64_t)L * k, g.n, invn);
+  int64_t mm = ((L & 1) ? g.NC : 0) - mk;
+  if (mm < 0) mm += g.n;
+  const int64_t rk = mk <= g.NC ? mk : g.n - mk, rm = mm <= g.NC ? mm : g.n - mm;
+  const double nk = sin_n(tb.Eh, tb.El, g.eb, rk), nm = sin_n(tb.Eh, tb.El, g.eb, rm);
+  const double dm = sin_n(tb.Eh, tb.El, g.eb, km);
+  const double Ld = (double)L;
+  double sk, sm;
+  if (k == 0) {
+    sk = 1.0;
+    sm = nm / (Ld * dm);
+  } else {
+    const double dk = sin_n(tb.Eh, tb.El, g.eb, k);
+    const double inv = 1.0 / (Ld * Ld * dk * dm);
+    sk = nk * Ld * dm * inv;
+    sm = nm * Ld * dk * inv;
+  }
+  sk *= sk;
+  sm *= sm;
+  wk = sk * sk;
+  wm = sm * sm;
+}
+template <int E>
+__device__ __forceinline__ double upow_c(double a) {
+  double e[1], x[1] = {a};
+  upow_ct<E, 1, double>(e, x);
+  return e[0];
+}
 __device__ __forceinline__ double upow_rt(double a, int e) {
   double r = 1.0, b = a;
   while (e) {
@@ -355,7 +397,7 @@ __device__ __forceinline__ int filter_half_length(const Geo& g, int k) {
 }
 
 // ------------------------------------------------------------------ init
-__global__ void k_init(Geo g, Ctl c) {
+static __global__ void k_init(const __grid_constant__ Geo g, const __grid_constant__ Ctl c) {
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < g.batch;
        b += (int64_t)gridDim.x * blockDim.x) {
     c.M[b] = 0;
@@ -375,9 +417,9 @@ enum { PASS_MID = 0, PASS_FWD_FIRST = 1, PASS_INV_LAST = 2 };
 // non-finite samples, writing extrema partials of s); INV_LAST finishes the IMF in natural order,
 // updates R and writes the extrema partials of the new remainder.
 template <typename Real, int DIR, int KIND>
-__global__ void __launch_bounds__(kThreads) k_col(Geo g, Level lv, const Real* __restrict__ sig,
+__global__ void __launch_bounds__(kThreads, 3) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv, const Real* __restrict__ sig,
                                                   Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
-                                                  Tabs<Real> tb, Ctl c) {
+                                                  const __grid_constant__ Tabs<Real> tb, const __grid_constant__ Ctl c) {
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   V* A = reinterpret_cast<V*>(smem_raw);
@@ -443,7 +485,7 @@ __global__ void __launch_bounds__(kThreads) k_col(Geo g, Level lv, const Real* _
 // Groups of segments -> group partials; the last CTA of a signal folds the groups, gets k, and
 // decides.  mode 0: after the forward transform (k of s); mode 1: after IMF M (bookkeeping first).
 template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_fold(Geo g, Ctl c, int mode, int32_t* __restrict__ lens,
+__global__ void __launch_bounds__(kThreads) k_fold(const __grid_constant__ Geo g, const __grid_constant__ Ctl c, int mode, int32_t* __restrict__ lens,
                                                    int32_t* __restrict__ iters) {
   __shared__ Mono sm[kNW];
   __shared__ int last;
@@ -515,9 +557,10 @@ __device__ __forceinline__ bool mirror_t(const Geo& g, int64_t bA, int two, int 
 }
 
 template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_rows_fwd(Geo g, Level lv, typename Cx<Real>::V* __restrict__ X,
-                                                       typename Cx<Real>::V* __restrict__ Xn, Tabs<Real> tb,
-                                                       Ctl c) {
+__global__ void __launch_bounds__(kThreads, 3) k_rows_fwd(const __grid_constant__ Geo g, const __grid_constant__ Level lv, typename Cx<Real>::V* __restrict__ X,
+                                                       typename Cx<Real>::V* __restrict__ Xn,
+                                                       const __grid_constant__ Tabs<Real> tb,
+                                                       const __grid_constant__ Ctl c) {
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   V* A = reinterpret_cast<V*>(smem_raw);
@@ -568,11 +611,12 @@ __global__ void __launch_bounds__(kThreads) k_rows_fwd(Geo g, Level lv, typename
 // d = a^N (a = 1 - w_hat); X <- (1 - d) X; with A = d_k X_k/n, B = d_{NC-k} X_{NC-k}/n:
 // Z_k = S + T, Z_{NC-k} = conj(S - T), S = A + conj B, T = i e^{2 pi i k/n} (A - conj B)
 // (k = 0 pairs with the Nyquist bin), then the length-F IDFT of each row into the IMF slot.
-template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_rows_inv(Geo g, Level lv, Real* __restrict__ imfs,
+template <typename Real, int CAP>
+__global__ void __launch_bounds__(kThreads, 3) k_rows_inv(const __grid_constant__ Geo g, const __grid_constant__ Level lv, Real* __restrict__ imfs,
                                                        typename Cx<Real>::V* __restrict__ X,
-                                                       typename Cx<Real>::V* __restrict__ Xn, Tabs<Real> tb,
-                                                       Ctl c) {
+                                                       typename Cx<Real>::V* __restrict__ Xn,
+                                                       const __grid_constant__ Tabs<Real> tb,
+                                                       const __grid_constant__ Ctl c) {
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
   V* A = reinterpret_cast<V*>(smem_raw);
@@ -597,11 +641,18 @@ __global__ void __launch_bounds__(kThreads) k_rows_inv(Geo g, Level lv, Real* __
       int tm;
       if (!mirror_t(g, bA, two, F, i, tm)) continue;
       const int64_t k = bA + g.P * i;
-      const int64_t km = g.NC - k;  // NC (Nyquist) for k = 0
       const V xk = A[i];
       const V xm = k == 0 ? Xn[b] : A[ob + tm];
-      const double dk = upow_rt(1.0 - what_tab(g, tb, L, k), N);
-      const double dm = upow_rt(1.0 - what_tab(g, tb, L, km), N);
+      double wk, wm;
+      what_pair(g, tb, L, invn, k, wk, wm);
+      double dk, dm;
+      if (CAP > 0 && N == CAP) {
+        dk = upow_c<CAP>(1.0 - wk);
+        dm = upow_c<CAP>(1.0 - wm);
+      } else {
+        dk = upow_rt(1.0 - wk, N);
+        dm = upow_rt(1.0 - wm, N);
+      }
       const V Av = cscale(xk, (Real)(dk * invn)), Bv = cscale(xm, (Real)(dm * invn));
       const V S = V{Av.x + Bv.x, Av.y - Bv.y};
       const V D = V{Av.x - Bv.x, Av.y + Bv.y};
@@ -627,72 +678,87 @@ __global__ void __launch_bounds__(kThreads) k_rows_inv(Geo g, Level lv, Real* __
 
 // ------------------------------------------------------------------ a5 probes
 // mode 0: cap probe (P, Q at N = max_inner); mode 1: K-ary probes N_i = lo + i*step, i = 1..kProbes.
-// Chunk = rpc rows; the last CTA of a signal folds the chunk partials (fixed order) and decides.
-template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Real>::V* __restrict__ X,
-                                                    const typename Cx<Real>::V* __restrict__ Xn, Tabs<Real> tb,
-                                                    Ctl c, int mode) {
+// One CTA per row-pair unit (both bins of every Hermitian pair share one window evaluation); the
+// last CTA of a signal folds the unit partials (fixed order) and decides.
+template <typename Real, int CAP, int MODE>
+__global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ Geo g,
+                                                       const typename Cx<Real>::V* __restrict__ X,
+                                                       const typename Cx<Real>::V* __restrict__ Xn,
+                                                       const __grid_constant__ Tabs<Real> tb,
+                                                       const __grid_constant__ Ctl c) {
+  constexpr int mode = MODE;
+  constexpr int NV = MODE == 0 ? 2 : 2 * kProbes;
   using V = typename Cx<Real>::V;
   __shared__ double sred[kNW][2 * kProbes];
   __shared__ int last;
   const int F = g.Frow;
+  const double invn = 1.0 / (double)g.n;
   for (int64_t t = blockIdx.x; t < g.batch * g.nbch; t += gridDim.x) {
     const int64_t b = t / g.nbch;
     const int64_t ch = t - b * g.nbch;
     if (!c.active[b] || (mode == 1 && !c.search[b])) continue;
     const int L = c.L[b];
-    int N0, step, nprobe;
+    int N0, step;
     if (mode == 0) {
-      N0 = g.max_inner; step = 0; nprobe = 1;
+      N0 = g.max_inner; step = 0;
     } else {
       const int lo = c.lo[b], hi = c.hi[b];
       step = (hi - lo + kProbes) / (kProbes + 1);
       if (step < 1) step = 1;
       N0 = lo + step;
-      nprobe = kProbes;
     }
-    double acc[2 * kProbes];
+    double acc[NV];
 #pragma unroll
-    for (int i = 0; i < 2 * kProbes; ++i) acc[i] = 0.0;
-    const int64_t r0 = ch * g.rpc, r1 = min(r0 + g.rpc, g.P);
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    int64_t ra, rb, bA;
+    int two;
+    pair_of<Real>(g, ch, ra, rb, bA, two);
     const V* Xb = X + b * g.NC;
-    for (int64_t row = r0; row < r1; ++row) {
-      const int64_t base = base_of_row(g, row);
-      for (int i = threadIdx.x; i <= F; i += blockDim.x) {
-        int64_t k;
-        V x;
-        double cw;
-        if (i == F) {  // Nyquist, once per signal
-          if (row != 0) continue;
-          k = g.NC; x = Xn[b]; cw = 1.0;
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      int tm;
+      if (!mirror_t(g, bA, two, F, i, tm)) continue;
+      const int64_t k = bA + g.P * i;
+      const V xk = Xb[ra * F + i];
+      const V xm = k == 0 ? Xn[b] : Xb[(two ? rb : ra) * F + tm];
+      double wk, wm;
+      what_pair(g, tb, L, invn, k, wk, wm);
+      // Parseval weights c_k: 1 for k = 0 and the Nyquist bin, 2 otherwise; a self-paired bin
+      // (k = NC - k) is counted once
+      const bool self = !two && i == tm && k != 0;
+      const double ck = k == 0 ? 1.0 : 2.0, cm = self ? 0.0 : (k == 0 ? 1.0 : 2.0);
+      const double pk = ck * ((double)xk.x * (double)xk.x + (double)xk.y * (double)xk.y);
+      const double pm = cm * ((double)xm.x * (double)xm.x + (double)xm.y * (double)xm.y);
+      const double ak = 1.0 - wk, am = 1.0 - wm;
+      if constexpr (MODE == 0) {
+        double ek, em;
+        if (CAP > 0 && N0 == CAP) {
+          ek = upow_c<CAP - 1>(ak);
+          em = upow_c<CAP - 1>(am);
         } else {
-          k = base + g.P * i; x = Xb[row * F + i]; cw = k == 0 ? 1.0 : 2.0;
+          ek = upow_rt(ak, N0 - 1);
+          em = upow_rt(am, N0 - 1);
         }
-        const double w = what_tab(g, tb, L, k);
-        const double a = 1.0 - w;
-        const double pk = cw * ((double)x.x * (double)x.x + (double)x.y * (double)x.y);
-        const double pw = pk * w * w;
-        if (mode == 0) {
-          const double e = upow_rt(a, N0 - 1);
-          const double xx = e * e;
-          acc[0] += pk * xx;
-          acc[1] += pw * xx;
-        } else {
-          const double a2 = a * a;
-          double y = upow_rt(a2, N0 - 1);
-          const double z = upow_rt(a2, step);
+        ek *= ek;
+        em *= em;
+        acc[0] += pk * ek + pm * em;
+        acc[1] += pk * wk * wk * ek + pm * wm * wm * em;
+      } else {
+        const double a2k = ak * ak, a2m = am * am;
+        double yk = upow_rt(a2k, N0 - 1), ym = upow_rt(a2m, N0 - 1);
+        const double zk = upow_rt(a2k, step), zm = upow_rt(a2m, step);
+        const double qk = pk * wk * wk, qm = pm * wm * wm;
 #pragma unroll
-          for (int q = 0; q < kProbes; ++q) {
-            acc[2 * q] += pk * y;
-            acc[2 * q + 1] += pw * y;
-            y *= z;
-          }
+        for (int q = 0; q < kProbes; ++q) {
+          acc[2 * q] += pk * yk + pm * ym;
+          acc[2 * q + 1] += qk * yk + qm * ym;
+          yk *= zk;
+          ym *= zm;
         }
       }
     }
-    const int nv = 2 * nprobe;
-    for (int i = 0; i < 2 * kProbes; ++i) {
-      if (i >= nv) break;
+    constexpr int nv = NV;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
       double v = acc[i];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -711,15 +777,17 @@ __global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Rea
     if (last) {
       __threadfence();
       // fold the chunk partials: thread-contiguous ranges, then a fixed-order tree
-      double s[2 * kProbes];
+      double s[NV];
 #pragma unroll
-      for (int i = 0; i < 2 * kProbes; ++i) s[i] = 0.0;
+      for (int i = 0; i < NV; ++i) s[i] = 0.0;
       const int64_t per = (g.nbch + blockDim.x - 1) / blockDim.x;
       const int64_t a0 = (int64_t)threadIdx.x * per, a1 = min(a0 + per, g.nbch);
       for (int64_t q = a0; q < a1; ++q)
-        for (int i = 0; i < nv; ++i) s[i] += __ldcg(c.red + (b * g.nbch + q) * (2 * kProbes) + i);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) s[i] += __ldcg(c.red + (b * g.nbch + q) * (2 * kProbes) + i);
       __syncthreads();
-      for (int i = 0; i < nv; ++i) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
         double v = s[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -727,14 +795,15 @@ __global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Rea
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        double PQ[2 * kProbes];
-        for (int i = 0; i < nv; ++i) {
+        double PQ[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
           double v = 0.0;
           for (int w = 0; w < kNW; ++w) v += sred[w][i];
           PQ[i] = v;
         }
         c.cnt[b] = 0;
-        if (mode == 0) {
+        if constexpr (MODE == 0) {
           c.N[b] = g.max_inner;
           if (PQ[1] <= g.delta2 * PQ[0]) {  // SD(cap) <= delta: search [1, cap)
             c.lo[b] = 0;
@@ -745,6 +814,7 @@ __global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Rea
         } else {
           const int lo = c.lo[b], hi = c.hi[b];
           int nlo = lo, nhi = hi;
+#pragma unroll
           for (int q = 0; q < kProbes; ++q) {
             const int Nq = lo + step * (q + 1);
             if (Nq >= hi) break;
@@ -767,7 +837,7 @@ __global__ void __launch_bounds__(kThreads) k_probe(Geo g, const typename Cx<Rea
 // ------------------------------------------------------------------ a7 final
 // trend (R lives in slot max_imfs) to slot M, zeros after; counts; zero lens/iters past M
 template <typename Real>
-__global__ void __launch_bounds__(kThreads) k_final(Geo g, Real* __restrict__ imfs, Ctl c, int32_t* count,
+__global__ void __launch_bounds__(kThreads) k_final(const __grid_constant__ Geo g, Real* __restrict__ imfs, const __grid_constant__ Ctl c, int32_t* count,
                                                     int32_t* lens, int32_t* iters) {
   for (int64_t t = blockIdx.x; t < g.batch; t += gridDim.x) {
     const int M = c.M[t];
