@@ -101,6 +101,34 @@ fif_status fif_decompose(fif_plan_t plan, const void* d_signals, void* d_imfs, i
 fif_status fif_decompose_host(fif_plan_t plan, const void* h_signals, void* h_imfs, int32_t* h_imf_count,
                               int32_t* h_filter_len, int32_t* h_iters, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Distributed regime: ONE long signal (BASELINE config 3) time-block sharded over nranks GPUs,
+ * one process per GPU, NCCL over NVLink for the exchange steps.  Rank r owns the
+ * samples [r n/nranks, (r+1) n/nranks).  Per IMF the ranks exchange: an all-gather of the
+ * stopping-rule partial sums (Parseval :175-180), two all-to-alls (the FFT digit
+ * that spans the ranks) and an all-gather of the extrema partials; every rank then
+ * takes the same decisions.
+ *   n_global : even, n_global/2 divisible by nranks^2, n_global/(2 nranks) of the form
+ *              2^a 3^b 5^c with a streamed-regime geometry; nranks in [1, 64].
+ *   nccl_unique_id : 128 bytes from fif_nccl_unique_id() on rank 0, broadcast by the caller
+ *              (e.g. torch.distributed); ignored when nranks == 1.
+ * fif_decompose on a distributed plan: d_signals = this rank's block [n_global/nranks];
+ * d_imfs [max_imfs+1][n_global/nranks] (this rank's block of every IMF and of the trend);
+ * d_imf_count [1], d_filter_len / d_iters [max_imfs]: identical on every rank.  All ranks must
+ * call it (collectives inside); it is stream-ordered like the batch regimes.
+ * ------------------------------------------------------------------------- */
+fif_status fif_nccl_unique_id(void* out128);
+fif_status fif_plan_create_dist(fif_plan_t* out, int64_t n_global, fif_dtype dtype, fif_window window, double xi,
+                                double delta, int32_t max_inner, int32_t max_imfs, const void* nccl_unique_id,
+                                int32_t rank, int32_t nranks);
+/* The same algorithm with all nranks ranks in this process on the current device, run back to back;
+ * the collectives become device-to-device copies (tests; single-GPU runs of the distributed path).
+ * Buffers hold every rank's block: d_signals [nranks][n/nranks], d_imfs [nranks][max_imfs+1][n/nranks],
+ * d_imf_count [nranks], d_filter_len / d_iters [nranks][max_imfs] (rows identical). */
+fif_status fif_plan_create_dist_emulated(fif_plan_t* out, int64_t n_global, fif_dtype dtype, fif_window window,
+                                         double xi, double delta, int32_t max_inner, int32_t max_imfs,
+                                         int32_t nranks);
+
 /* Free the plan's tables and staging buffers (synchronises the device first).  NULL is a no-op. */
 fif_status fif_destroy(fif_plan_t plan);
 
@@ -108,7 +136,7 @@ fif_status fif_destroy(fif_plan_t plan);
 const char* fif_status_string(fif_status s);
 
 /* Plan introspection: number of kernels one fif_decompose launches, the regime name
- * ("resident" / "streamed"), and the main kernel's grid / block / dynamic smem. */
+ * ("resident" / "streamed" / "distributed"), and the main kernel's grid / block / dynamic smem. */
 int32_t fif_plan_kernels_per_call(fif_plan_t plan);
 const char* fif_plan_regime(fif_plan_t plan);
 fif_status fif_plan_launch_config(fif_plan_t plan, int32_t* grid, int32_t* block, int32_t* smem_bytes);

@@ -78,6 +78,7 @@ void free_plan(fif_plan_s* p) {
   cudaFree(p->d_isin);
   cudaFree(p->d_tw);
   st_free(p);
+  dist_free(p);
   for (int i = 0; i < p->nstages; ++i) {
     cudaFree(p->st[i].d_in);
     cudaFree(p->st[i].d_out);
@@ -164,6 +165,47 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
   return FIF_OK;
 }
 
+fif_status fif_nccl_unique_id(void* out128) {
+  if (!out128) return FIF_ERR_INVALID_ARG;
+  return nccl_unique_id(out128);
+}
+
+static fif_status create_dist(fif_plan_t* out, int64_t n, fif_dtype dtype, fif_window window, double xi,
+                              double delta, int32_t max_inner, int32_t max_imfs, const void* uid, int32_t rank,
+                              int32_t nranks, int emulated) {
+  if (!out) return FIF_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n < 9 || !(xi > 0.0) || !isfinite(xi) || !(delta > 0.0) || !isfinite(delta) || max_inner < 1 || max_imfs < 1 ||
+      (dtype != FIF_F64 && dtype != FIF_F32) || (window != FIF_WINDOW_TRI_SQ && window != FIF_WINDOW_TRI_SQ_WIDE) ||
+      nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks || (!emulated && nranks > 1 && !uid))
+    return FIF_ERR_INVALID_ARG;
+  if (n % 2 || (n / 2) % ((int64_t)nranks * nranks)) return FIF_ERR_UNSUPPORTED_N;
+  st::Geo g;
+  if (!st_geometry(n / nranks, dtype == FIF_F64, g)) return FIF_ERR_UNSUPPORTED_N;
+  fif_plan_s* p = new fif_plan_s();
+  p->n = n; p->batch = 1; p->dtype = dtype; p->window = window; p->xi = xi; p->delta = delta;
+  p->max_inner = max_inner; p->max_imfs = max_imfs; p->regime = 2;
+  if (cudaGetDevice(&p->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
+    free_plan(p);
+    return FIF_ERR_CUDA;
+  }
+  fif_status st = dist_create(p, uid, rank, nranks, emulated);
+  if (st != FIF_OK) { free_plan(p); return st; }
+  *out = p;
+  return FIF_OK;
+}
+fif_status fif_plan_create_dist(fif_plan_t* out, int64_t n_global, fif_dtype dtype, fif_window window, double xi,
+                                double delta, int32_t max_inner, int32_t max_imfs, const void* nccl_unique_id,
+                                int32_t rank, int32_t nranks) {
+  return create_dist(out, n_global, dtype, window, xi, delta, max_inner, max_imfs, nccl_unique_id, rank, nranks, 0);
+}
+fif_status fif_plan_create_dist_emulated(fif_plan_t* out, int64_t n_global, fif_dtype dtype, fif_window window,
+                                         double xi, double delta, int32_t max_inner, int32_t max_imfs,
+                                         int32_t nranks) {
+  return create_dist(out, n_global, dtype, window, xi, delta, max_inner, max_imfs, nullptr, 0, nranks, 1);
+}
+
 fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int32_t* d_imf_count,
                          int32_t* d_filter_len, int32_t* d_iters, void* stream) {
   if (!p) return FIF_ERR_INVALID_ARG;
@@ -171,6 +213,11 @@ fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int3
   if (!d_signals || !d_imfs || !d_imf_count || !d_filter_len || !d_iters) return FIF_ERR_INVALID_ARG;
   if (((uintptr_t)d_signals | (uintptr_t)d_imfs) & 15) return FIF_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  if (p->regime == 2) {
+    fif_status st = dist_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, s);
+    if (st != FIF_OK) return st;
+    return launch_status();
+  }
   if (p->regime == 1) {
     st_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, 0, s);
     return launch_status();
@@ -184,6 +231,7 @@ fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs,
   if (!p) return FIF_ERR_INVALID_ARG;
   if (p->batch == 0) return FIF_OK;
   if (!h_signals || !h_imfs || !h_imf_count || !h_filter_len || !h_iters) return FIF_ERR_INVALID_ARG;
+  if (p->regime == 2) return FIF_ERR_INVALID_ARG;  // distributed plans take device buffers
   const size_t es = elem_size(p->dtype);
   const size_t in_sig = (size_t)p->n * es, out_sig = in_sig * (size_t)(p->max_imfs + 1);
   const size_t meta_sig = (size_t)(1 + 2 * p->max_imfs);
@@ -251,10 +299,14 @@ fif_status fif_destroy(fif_plan_t p) {
 
 int32_t fif_plan_kernels_per_call(fif_plan_t p) {
   if (!p || p->batch == 0) return 0;
+  if (p->regime == 2) return dist_kernels_per_call(p);
   return p->regime == 1 ? st_kernels_per_call(p) : 1;
 }
 
-const char* fif_plan_regime(fif_plan_t p) { return p ? (p->regime == 1 ? "streamed" : "resident") : "none"; }
+const char* fif_plan_regime(fif_plan_t p) {
+  if (!p) return "none";
+  return p->regime == 2 ? "distributed" : (p->regime == 1 ? "streamed" : "resident");
+}
 
 fif_status fif_plan_launch_config(fif_plan_t p, int32_t* grid, int32_t* block, int32_t* smem_bytes) {
   if (!p) return FIF_ERR_INVALID_ARG;

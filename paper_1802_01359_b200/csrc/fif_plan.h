@@ -10,6 +10,7 @@
 #include "fif_streamed.cuh"
 
 namespace fifhost {
+struct DistPlan;
 
 enum { FIF_MAX_STAGES = 3 };
 // max_inner value with a compile-time-specialised kernel (the paper's/BASELINE's cap of 200,
@@ -53,6 +54,7 @@ struct fif_plan_s {
   fifgpu::st::Ctl ctl{};
   int st_rounds = 0, st_grid = 0, st_grid_col = 0, st_grid_rows = 0, st_grid_probe = 0;
   int64_t st_wave = 1;
+  fifhost::DistPlan* dist = nullptr;  // distributed regime (fif_dist.cu)
   cudaStream_t st_streams[2] = {nullptr, nullptr};  // waves alternate between these
   cudaEvent_t st_ev[3] = {nullptr, nullptr, nullptr};
   size_t st_smem_col[fifgpu::st::kMaxLev] = {}, st_smem_rows = 0;
@@ -89,4 +91,12 @@ void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int3
                   int64_t batch, int64_t boff, cudaStream_t s);
 int st_kernels_per_call(const fif_plan_s* p);
 void st_free(fif_plan_s* p);
+
+// distributed regime (fif_dist.cu): one signal time-block sharded over nranks GPUs
+fif_status dist_create(fif_plan_s* p, const void* nccl_uid, int rank, int nranks, int emulated);
+fif_status dist_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
+                          cudaStream_t s);
+void dist_free(fif_plan_s* p);
+int dist_kernels_per_call(const fif_plan_s* p);
+fif_status nccl_unique_id(void* out);
 }  // namespace fifhost

@@ -22,7 +22,8 @@ STATUS = {0: "FIF_OK", 1: "FIF_ERR_INVALID_ARG", 2: "FIF_ERR_UNSUPPORTED_N", 3: 
 REGIME_AUTO, REGIME_RESIDENT, REGIME_STREAMED = 0, 1, 2
 SYMBOLS = ["fif_plan_create", "fif_plan_create_ex", "fif_decompose", "fif_decompose_host", "fif_destroy", "fif_status_string",
            "fif_plan_kernels_per_call", "fif_plan_regime", "fif_plan_launch_config", "fif_test_rfft",
-           "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner"]
+           "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner", "fif_nccl_unique_id",
+           "fif_plan_create_dist", "fif_plan_create_dist_emulated"]
 
 
 class FifError(RuntimeError):
@@ -61,6 +62,11 @@ def lib():
         L.fif_test_extrema.argtypes = [vp, i64, vp, vp, vp]
         L.fif_test_window_spectrum.argtypes = [vp, i32, vp, vp]
         L.fif_test_inner.argtypes = [vp, i64, i32, vp, vp, vp, vp]
+        L.fif_nccl_unique_id.argtypes = [vp]
+        L.fif_plan_create_dist.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32, i32, vp,
+                                           i32, i32]
+        L.fif_plan_create_dist_emulated.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32,
+                                                    i32, i32]
         for name in SYMBOLS:
             if name not in ("fif_status_string", "fif_plan_kernels_per_call", "fif_plan_regime"):
                 getattr(L, name).restype = ctypes.c_int
@@ -82,6 +88,13 @@ def _stream_ptr(stream):
         import torch
         stream = torch.cuda.current_stream()
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def nccl_unique_id() -> bytes:
+    """fif_nccl_unique_id: 128 bytes for fif_plan_create_dist (call on rank 0, broadcast)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().fif_nccl_unique_id(buf), "fif_nccl_unique_id")
+    return buf.raw
 
 
 class Plan:
@@ -121,6 +134,27 @@ class Plan:
         """fif_decompose_host on (pinned) host tensors; synchronous."""
         _check(lib().fif_decompose_host(self._h, _ptr(signals), _ptr(imfs), _ptr(count), _ptr(lens), _ptr(iters),
                                         _stream_ptr(stream)), "fif_decompose_host")
+
+    @classmethod
+    def dist(cls, n_global, rank, nranks, uid=None, dtype="f64", window=WINDOW_TRI_SQ, xi=1.6, delta=1e-3,
+             max_inner=200, max_imfs=10, emulated=False):
+        """fif_plan_create_dist (one rank of nranks; uid = nccl_unique_id() of rank 0) or, with
+        emulated=True, fif_plan_create_dist_emulated (all nranks ranks on this device)."""
+        self = cls.__new__(cls)
+        self.n, self.max_imfs, self.dtype = int(n_global) // int(nranks), int(max_imfs), dtype
+        self.batch = int(nranks) if emulated else 1
+        self._h = ctypes.c_void_p()
+        dt = F64 if dtype == "f64" else F32
+        if emulated:
+            _check(lib().fif_plan_create_dist_emulated(ctypes.byref(self._h), int(n_global), dt, int(window),
+                                                       float(xi), float(delta), int(max_inner), int(max_imfs),
+                                                       int(nranks)), "fif_plan_create_dist_emulated")
+        else:
+            ub = ctypes.create_string_buffer(bytes(uid) if uid is not None else bytes(128), 128)
+            _check(lib().fif_plan_create_dist(ctypes.byref(self._h), int(n_global), dt, int(window), float(xi),
+                                              float(delta), int(max_inner), int(max_imfs), ub, int(rank),
+                                              int(nranks)), "fif_plan_create_dist")
+        return self
 
     def launch_config(self):
         g, b, s = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
