@@ -38,7 +38,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg4"])
+    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--emulate", type=int, default=0,
+                    help="cfg3 on one GPU: run the distributed algorithm with this many emulated ranks")
     ap.add_argument("--n", type=int, default=1 << 14, help="signal length for cfg4 (fp32 sweep)")
     ap.add_argument("--batch", type=int, default=None, help="signals per rank (default: the config's)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -52,6 +54,8 @@ def workload(cfg, batch, n4=1 << 14):
 
     if cfg == "cfg4":
         return n4, signals.cfg4_batch(n4) if batch is None else batch, 1e-3, "f32"
+    if cfg == "cfg3":
+        return (signals.CONFIGS["cfg3"]["n"] if n4 is None or n4 == 1 << 14 else n4), 1, 1e-3, "f64"
     c = signals.CONFIGS[cfg]
     B = c["batch"] if batch is None else batch
     return c["n"], B, c["delta"], c["dtype"]
@@ -125,6 +129,17 @@ def cpu_baseline(cfg, n, delta, budget_s=12.0, max_signals=256, n4=None):
     from paper_1802_01359_b200 import signals
 
     ncores = oracle.num_threads()
+    if cfg == "cfg3":  # one 2^26 signal: the literal iteration is out of reach; the paper's direct form
+        from oracle import direct_form as df  # (numpy FFT, linear N scan) on a 2^22 cfg3-recipe signal
+
+        m = 1 << 22
+        s = signals.cfg3_signal(0, n=m)
+        t0 = time.perf_counter()
+        df.decompose(s, delta=delta)
+        t_total = time.perf_counter() - t0
+        return {"value": m / t_total, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"one cfg3-recipe signal of n=2^22 through oracle/direct_form.py (numpy FFT direct form, "
+                          f"linear N scan), {t_total:.1f} s, single-threaded numpy"}
     done, t_total, start = 0, 0.0, 0
     chunk = max(ncores, 8)
     while t_total < budget_s and done < max_signals:
@@ -156,6 +171,20 @@ def max_over_ranks(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def share_uid(rank: int, make_uid) -> bytes:
+    """Rank 0 makes the NCCL unique id (fif_nccl_unique_id); every rank receives it (torch.distributed)."""
+    import torch.distributed as tdist
+
+    obj = [make_uid() if rank == 0 else None]
+    tdist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def time_block(full, rank: int, world: int):
+    """Config 3 sharding: rank r owns samples [r n/world, (r+1) n/world) of the one long signal."""
+    return np.ascontiguousarray(full.reshape(world, -1)[rank])
+
+
 def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -177,6 +206,30 @@ def run_reference(args, world, rank):
     from paper_1802_01359_b200 import signals
 
     ncores = oracle.num_threads()
+    if args.config == "cfg3":
+        # one 2^26 signal is out of the literal iteration's reach: each step is the paper's direct form
+        # (oracle/direct_form.py) on a 2^20-sample cfg3-recipe signal
+        from oracle import direct_form as dfo
+
+        S, m = 1, 1 << 20
+        s = signals.cfg3_signal(0, n=m)
+        for _ in range(min(args.warmup, 1)):
+            dfo.decompose(s, delta=delta)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            dfo.decompose(s, delta=delta)
+        dt_s = (time.perf_counter() - t0) / args.steps
+        value = m / dt_s
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt_s * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"cfg3 recipe, one n=2^20 signal per step (bounded sample of the n={n} signal)",
+                           "n": m, "xi": 1.6, "delta": delta, "max_inner": 200, "max_imfs": 10},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                 "sample": "oracle/direct_form.py on one 2^20 cfg3-recipe signal per step"},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     S = max(ncores, 16) if n <= 8192 else ncores  # signals per step (bounded sample of the batch)
     s = signals.make_batch(args.config, batch=S, n=n if args.config == "cfg4" else None).astype(np.float64)
     for _ in range(args.warmup):
@@ -209,10 +262,29 @@ def main():
     from paper_1802_01359_b200 import fif, signals
 
     n, B, delta, dt = workload(args.config, args.batch, args.n)
-    s_host = signals.make_batch(args.config, batch=B, start=rank_start(rank, B),
-                                n=n if args.config == "cfg4" else None)
+    scaling, parallelism = "weak", f"batch split x{world}, no collective"
+    if args.config == "cfg3":
+        # one long signal: strong scaling over the ranks (time-block shards, NCCL exchange steps)
+        full = signals.cfg3_signal(0, n=n)
+        if world > 1:
+            plan = fif.Plan.dist(n, rank, world, uid=share_uid(rank, fif.nccl_unique_id), delta=delta)
+            s_host = time_block(full, rank, world)
+            parallelism = f"distributed x{world}: time-block shards, NCCL all-to-all + all-gather per IMF"
+        elif args.emulate > 1:
+            plan = fif.Plan.dist(n, 0, args.emulate, delta=delta, emulated=True)
+            s_host = np.ascontiguousarray(full.reshape(args.emulate, n // args.emulate))
+            parallelism = f"distributed algorithm, {args.emulate} ranks emulated on 1 GPU"
+        else:
+            plan = fif.Plan(n, 1, dt, delta=delta)
+            s_host = full[None]
+            parallelism = "single GPU, streamed regime"
+        scaling = "strong"
+        del full
+    else:
+        s_host = signals.make_batch(args.config, batch=B, start=rank_start(rank, B),
+                                    n=n if args.config == "cfg4" else None)
+        plan = fif.Plan(n, B, dt, delta=delta)
     x = torch.from_numpy(s_host).cuda()
-    plan = fif.Plan(n, B, dt, delta=delta)
     imfs, count, lens, iters = plan.alloc_outputs()
     stream = torch.cuda.current_stream()
     cfgl = plan.launch_config()
@@ -243,12 +315,16 @@ def main():
 
     # roofline (dominant kernel = the single resident kernel: its launch duration = the step)
     cnt = count.cpu().numpy()
+    if cfgl["regime"] == "distributed":
+        cnt = cnt[:1]  # one signal; the count is replicated on every (emulated) rank
     Mtot = int(np.clip(cnt, 0, None).sum())
     eb = 8 if dt == "f64" else 4
     passes = 2 if cfgl["regime"] == "resident" else 4  # four-step: two read+write passes per transform
     fft_bytes = passes * n * eb * (Mtot + B)      # passes*n*b per transform, (M+1) transforms per signal
     comp_bytes = n * eb * (Mtot + 2 * B)          # read s once + write M IMFs + trend
     written_bytes = n * eb * B * (plan.max_imfs + 1) + n * eb * B  # output slots + input
+    if args.config == "cfg3" and world > 1:       # per-GPU roofline: this rank's share of the bytes
+        fft_bytes, comp_bytes, written_bytes = fft_bytes // world, comp_bytes // world, written_bytes // world
     peak, peak_kind = hbm_peak()
     ach = fft_bytes / (ms * 1e-3) / 1e9
     traffic = None
@@ -259,12 +335,33 @@ def main():
         except Exception:
             traffic = None
 
-    samples = B * n * world
+    samples = n if args.config == "cfg3" else B * n * world
     value = samples / (ms * 1e-3)
 
     # e2e through the public host API (pinned host buffers; H2D + kernels + D2H inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and cfgl["regime"] == "distributed":
+        # e2e through fif_decompose with this rank's block copied in from pinned host memory and its
+        # IMF block + integers copied back, inside the timed region
+        hs = torch.from_numpy(s_host).pin_memory()
+        h_out = [torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory() for t in (imfs, count, lens, iters)]
+        ksteps = max(1, min(args.steps, 3))
+        barrier()
+        torch.cuda.synchronize()
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        for _ in range(ksteps):
+            x.copy_(hs, non_blocking=True)
+            plan.decompose(x, imfs, count, lens, iters, stream=stream)
+            for h, d in zip(h_out, (imfs, count, lens, iters)):
+                h.copy_(d, non_blocking=True)
+        e3.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(e2.elapsed_time(e3) / ksteps, world, "cuda")
+        e2e = {"value": samples / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": hs.numel() * hs.element_size(),
+               "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in h_out), "ms_per_step": ems,
+               "steps": ksteps, "path": "fif_decompose + cudaMemcpyAsync from/to pinned host (per rank)"}
+    elif not args.no_e2e:
         hs = torch.from_numpy(s_host).pin_memory()
         h_out = [torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory() for t in (imfs, count, lens, iters)]
         plan.decompose_host(hs, *h_out, stream=stream)  # warm-up (allocates staging)
@@ -290,12 +387,14 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": dt, "data": "synthetic",
-            "config": {"workload": f"{args.config}: {B} signals x n={n} {dt} per GPU (BASELINE.json configs"
-                                   f"[{args.config[-1]}])",
+            "config": {"workload": (f"{args.config}: one signal of n={n} {dt} over {world} GPU(s) (BASELINE.json "
+                                    f"configs[3])") if args.config == "cfg3" else
+                                   (f"{args.config}: {B} signals x n={n} {dt} per GPU (BASELINE.json configs"
+                                    f"[{args.config[-1]}])"),
                        "n": n, "batch_per_gpu": B, "xi": 1.6, "delta": delta, "max_inner": 200, "max_imfs": 10,
-                       "window": "tri_sq (R1)", "parallelism": f"batch split x{world}, no collective", "regime": cfgl["regime"],
+                       "window": "tri_sq (R1)", "parallelism": parallelism, "regime": cfgl["regime"],
                        "l2": f"inputs+outputs {written_bytes / 1e9:.2f} GB/step > 126 MB L2 (no flush needed)",
                        "imfs_per_signal_mean": Mtot / B, "launch": cfgl},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,

@@ -107,18 +107,40 @@ __global__ void __launch_bounds__(kThreads, 3) k_d_pass(const __grid_constant__ 
   for (int64_t t = blockIdx.x; t < lv.tiles; t += gridDim.x) {
     const int64_t a = t / spt, s0 = (t - a * spt) * lv.C;
     const int64_t base = a * (int64_t)lv.F * lv.S + s0;
-    for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
-      const int f = i / lv.C, cc = i - f * lv.C;
-      V v = buf[base + (int64_t)f * lv.S + cc];
-      if (DIR > 0 && lv.S > 1) v = cmul(v, st::Er(tb, d.g.eb, lv.E2 * (s0 + cc) * f));
-      A[cc * lv.pitch + f] = v;
+    const int FC = lv.F * lv.C;
+    constexpr int U = st::TileCap<Real>::value / kThreads;
+    V v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = threadIdx.x + j * kThreads;
+      if (i < FC) {
+        int f, cc;
+        st::tile_fc(lv, i, f, cc);
+        v[j] = buf[base + (int64_t)f * lv.S + cc];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = threadIdx.x + j * kThreads;
+      if (i < FC) {
+        int f, cc;
+        st::tile_fc(lv, i, f, cc);
+        V x = v[j];
+        if (DIR > 0 && lv.S > 1) x = cmul(x, st::Er(tb, d.g.eb, lv.E2 * (s0 + cc) * f));
+        A[st::sidx<V>(cc, f, lv.pitch, lv.swz)] = x;
+      }
     }
     V* out = st::cta_fft<DIR>(A, Bf, lv, lv.C, tb.tw);
-    for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
-      const int f = i / lv.C, cc = i - f * lv.C;
-      V v = out[cc * lv.pitch + f];
-      if (DIR < 0 && lv.S > 1) v = cmul(v, cconj(st::Er(tb, d.g.eb, lv.E2 * (s0 + cc) * f)));
-      buf[base + (int64_t)f * lv.S + cc] = v;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = threadIdx.x + j * kThreads;
+      if (i < FC) {
+        int f, cc;
+        st::tile_fc(lv, i, f, cc);
+        V x = out[st::sidx<V>(cc, f, lv.pitch, lv.swz)];
+        if (DIR < 0 && lv.S > 1) x = cmul(x, cconj(st::Er(tb, d.g.eb, lv.E2 * (s0 + cc) * f)));
+        buf[base + (int64_t)f * lv.S + cc] = x;
+      }
     }
     __syncthreads();
   }
@@ -681,7 +703,8 @@ fif_status dist_setup_t(fif_plan_s* p, DistPlan& D) {
     lv.E2 = 2 * n / ((int64_t)lv.F * lv.S);
     if (i == g.L - 1) {
       lv.C = 1;
-      lv.pitch = lv.F + 1;
+      lv.cs = 0;
+      lv.pitch = lv.swz ? lv.F : lv.F + 1;
       lv.tiles = lv.A;
     }
   }

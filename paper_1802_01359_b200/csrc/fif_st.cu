@@ -82,13 +82,18 @@ bool st_geometry(int64_t n, bool f64, st::Geo& g) {
           for (int64_t c = cmax < S ? cmax : S; c >= 1; --c)
             if (S % c == 0) { C = c; break; }
           lv.C = (int)C;
-          lv.pitch = lv.F + 1;
+          lv.swz = lv.F % (f64 ? 8 : 16) == 0;
+          lv.pitch = lv.swz ? lv.F : lv.F + 1;
           lv.tiles = lv.A * S / C;
         } else {
           lv.C = 2;
+          lv.swz = lv.F % (f64 ? 8 : 16) == 0;
           lv.pitch = lv.F;
           lv.tiles = 0;
         }
+        lv.cs = -1;
+        if ((lv.C & (lv.C - 1)) == 0)
+          for (lv.cs = 0; (1 << lv.cs) < lv.C; ++lv.cs) {}
         g.Fd[i] = lv.F;
         g.Pd[i] = i == 0 ? 1 : g.Pd[i - 1] * F[i - 1];
         g.Sr[i] = S / row;

@@ -54,7 +54,31 @@ struct Level {
   int64_t A;      // blocks = NC / (F S)
   int64_t E2;     // 2n / (F S): E-table index step of the inter-level twiddle
   int64_t tiles;  // tiles per signal = A S / C (column levels)
+  int cs;         // log2(C) when C is a power of two, else -1
+  int swz;        // 1: XOR-swizzled columns (F a multiple of the 128-byte row), pitch = F
 };
+
+// shared-memory slot of element i of column c: with swz, the 16-byte (8-byte) bank group of i is
+// XORed with (i / row) ^ c, so column-strided (tile loads), radix-strided (Stockham stores) and
+// contiguous accesses all spread over the banks
+template <typename V>
+__device__ __forceinline__ int sidx(int c, int i, int pitch, int swz) {
+  constexpr int ROW = 128 / (int)sizeof(V), LR = sizeof(V) == 16 ? 3 : 4;
+  return c * pitch + (swz ? (i ^ (((i >> LR) ^ c) & (ROW - 1))) : i);
+}
+
+// complex elements per tile buffer (F C <= kTile): 32 KiB of shared memory per buffer
+template <typename Real> struct TileCap { static constexpr int value = 16384 / (int)sizeof(Real); };
+// tile element i -> (digit f, column cc)
+__device__ __forceinline__ void tile_fc(const Level& lv, int i, int& f, int& cc) {
+  if (lv.cs >= 0) {
+    f = i >> lv.cs;
+    cc = i & (lv.C - 1);
+  } else {
+    f = i / lv.C;
+    cc = i - f * lv.C;
+  }
+}
 
 struct Geo {
   int64_t n, NC, batch;
@@ -135,21 +159,30 @@ __device__ __forceinline__ void dft5(V& x0, V& x1, V& x2, V& x3, V& x4) {
   x3 = csub(t2, u2);
 }
 
-// One Stockham pass of radix p over `cols` independent length-Ns FFTs, column c at offset c*pitch:
-// src[c, i] -> dst[c, j].  tw[j] = e^{-2 pi i j/Ns}.
+// One Stockham pass of radix p over `cols` independent length-Ns FFTs, column c at offset c*pitch
+// (slots through sidx): src[c, i] -> dst[c, j].  tw[j] = e^{-2 pi i j/Ns}.
 template <int DIR, typename V>
-__device__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int p, int NS,
+__device__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int swz, int p, int NS,
                          const V* __restrict__ tw) {
   const int per = Ns / p;
   const int tstride = Ns / (NS * p);
+  const bool pow2 = ((Ns & (Ns - 1)) == 0) && ((NS & (NS - 1)) == 0);
+  const int lper = __ffs(per) - 1;
   for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
-    const int f = idx / per, vt = idx - f * per;
-    const int k = vt % NS;
-    const V* s = src + f * pitch + vt;
+    int f, vt, k;
+    if (pow2) {
+      f = idx >> lper;
+      vt = idx & (per - 1);
+      k = vt & (NS - 1);
+    } else {
+      f = idx / per;
+      vt = idx - f * per;
+      k = vt % NS;
+    }
     V x[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
-      if (r < p) x[r] = s[r * per];
+      if (r < p) x[r] = src[sidx<V>(f, vt + r * per, pitch, swz)];
     if (NS > 1) {
 #pragma unroll
       for (int r = 1; r < 8; ++r)
@@ -166,10 +199,10 @@ __device__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int 
       case 5: dft5<DIR>(x[0], x[1], x[2], x[3], x[4]); break;
       default: dft8<DIR>(x); break;
     }
-    V* d = dst + f * pitch + (vt / NS) * NS * p + k;
+    const int j0 = (vt - k) * p + k;  // (vt / NS) NS p + k
 #pragma unroll
     for (int r = 0; r < 8; ++r)
-      if (r < p) d[r * NS] = x[r];
+      if (r < p) dst[sidx<V>(f, j0 + r * NS, pitch, swz)] = x[r];
   }
 }
 
@@ -179,7 +212,7 @@ __device__ V* cta_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict
   int NS = 1;
   for (int ps = 0; ps < lv.np; ++ps) {
     __syncthreads();
-    cta_pass<DIR>(a, b, lv.F, cols, lv.pitch, lv.rad[ps], NS, tw + lv.twoff);
+    cta_pass<DIR>(a, b, lv.F, cols, lv.pitch, lv.swz, lv.rad[ps], NS, tw + lv.twoff);
     NS *= lv.rad[ps];
     V* t = a; a = b; b = t;
   }
@@ -223,25 +256,26 @@ __device__ __forceinline__ int64_t mod_n(int64_t x, int64_t n, double invn) {
   else if (m >= n) m -= n;
   return m;
 }
-// a4 for a Hermitian pair (k, NC - k), 0 <= k < NC: one division for both bins.
-// L (NC - k) = L NC - L k, and L NC = 0 (L even) or NC (L odd) mod n.
+// a4 for a Hermitian pair (k, NC - k), 0 <= k < NC, given mk = L k mod n: one division and two
+// table products for both bins.  sin(pi (NC-k)/n) = cos(pi k/n); L (NC - k) = L NC - L k with
+// L NC = 0 (L even) or NC (L odd) mod n, so sin(pi r_{NC-k}/n) = sin(pi mk/n) (L even) or
+// |cos(pi mk/n)| (L odd).  A cosine near zero carries a larger relative error, but it then belongs
+// to a bin whose w_hat is tiny or whose a^N vanishes, so the absolute error of a^N stays at
+// rounding level (|d a^N| <= N a^{N-1} |d w| <= |d w / w| / e).  Returns e^{i pi k/n} in Ek.
 template <typename Real>
-__device__ __forceinline__ void what_pair(const Geo& g, const Tabs<Real>& tb, int L, double invn, int64_t k,
-                                          double& wk, double& wm) {
-  const int64_t km = g.NC - k;
-  const int64_t mk = mod_n((int64_t)L * k, g.n, invn);
-  int64_t mm = ((L & 1) ? g.NC : 0) - mk;
-  if (mm < 0) mm += g.n;
-  const int64_t rk = mk <= g.NC ? mk : g.n - mk, rm = mm <= g.NC ? mm : g.n - mm;
-  const double nk = sin_n(tb.Eh, tb.El, g.eb, rk), nm = sin_n(tb.Eh, tb.El, g.eb, rm);
-  const double dm = sin_n(tb.Eh, tb.El, g.eb, km);
+__device__ __forceinline__ void what_pair_m(const Geo& g, const Tabs<Real>& tb, int L, int64_t k, int64_t mk,
+                                            double& wk, double& wm, double2& Ek) {
+  const int64_t rk = mk <= g.NC ? mk : g.n - mk;
+  Ek = E64(tb.Eh, tb.El, g.eb, k);                 // (cos, sin)(pi k/n), first quadrant
+  const double2 Er_ = E64(tb.Eh, tb.El, g.eb, rk);  // (cos, sin)(pi rk/n), first quadrant
+  const double nk = Er_.y, nm = (L & 1) ? fabs(Er_.x) : Er_.y;
+  const double dk = Ek.y, dm = Ek.x;
   const double Ld = (double)L;
   double sk, sm;
   if (k == 0) {
     sk = 1.0;
     sm = nm / (Ld * dm);
   } else {
-    const double dk = sin_n(tb.Eh, tb.El, g.eb, k);
     const double inv = 1.0 / (Ld * Ld * dk * dm);
     sk = nk * Ld * dm * inv;
     sm = nm * Ld * dk * inv;
@@ -250,6 +284,13 @@ __device__ __forceinline__ void what_pair(const Geo& g, const Tabs<Real>& tb, in
   sm *= sm;
   wk = sk * sk;
   wm = sm * sm;
+}
+// the same from k alone
+template <typename Real>
+__device__ __forceinline__ void what_pair(const Geo& g, const Tabs<Real>& tb, int L, double invn, int64_t k,
+                                          double& wk, double& wm) {
+  double2 Ek;
+  what_pair_m(g, tb, L, k, mod_n((int64_t)L * k, g.n, invn), wk, wm, Ek);
 }
 template <int E>
 __device__ __forceinline__ double upow_c(double a) {
@@ -343,7 +384,7 @@ __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, 
     const int d0 = lane * q, d1 = min(d0 + q, nd);
     if (d0 < d1) {
       auto x_at = [&](int j) -> Real {
-        const auto v = buf[(j >> 1) * lv.pitch + f];
+        const auto v = buf[sidx<typename Cx<Real>::V>(j >> 1, f, lv.pitch, lv.swz)];
         return (j & 1) ? v.y : v.x;
       };
       Real prev = x_at(d0);
@@ -357,8 +398,8 @@ __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, 
     if (lane == 0) {
       const int64_t s = seg0 + (int64_t)f * segstep;
       segi[s] = mpack(m);
-      segv[2 * s] = buf[f].x;
-      segv[2 * s + 1] = buf[(lv.C - 1) * lv.pitch + f].y;
+      segv[2 * s] = buf[sidx<typename Cx<Real>::V>(0, f, lv.pitch, lv.swz)].x;
+      segv[2 * s + 1] = buf[sidx<typename Cx<Real>::V>(lv.C - 1, f, lv.pitch, lv.swz)].y;
     }
   }
 }
@@ -436,17 +477,34 @@ __global__ void __launch_bounds__(kThreads, 3) k_col(const __grid_constant__ Geo
     if (DIR < 0) buf = X + b * g.NC;
     else buf = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
     const V* src = KIND == PASS_FWD_FIRST ? reinterpret_cast<const V*>(sig + b * g.n) : buf;
-    bool finite = true;
-    for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
-      const int f = i / lv.C, cc = i - f * lv.C;
-      const int64_t gi = base + (int64_t)f * lv.S + cc;
-      V v = src[gi];
-      if (KIND == PASS_FWD_FIRST) {
-        finite &= isfinite(v.x) && isfinite(v.y);
-        reinterpret_cast<V*>(Rb)[gi] = v;
+    const int FC = lv.F * lv.C;
+    constexpr int U = TileCap<Real>::value / kThreads;
+    // all of this thread's tile loads in flight at once
+    V v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = threadIdx.x + j * kThreads;
+      if (i < FC) {
+        int f, cc;
+        tile_fc(lv, i, f, cc);
+        v[j] = src[base + (int64_t)f * lv.S + cc];
       }
-      if (DIR > 0 && lv.E2 > 0) v = cmul(v, Er(tb, g.eb, lv.E2 * (s0 + cc) * f));
-      A[cc * lv.pitch + f] = v;
+    }
+    bool finite = true;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = threadIdx.x + j * kThreads;
+      if (i < FC) {
+        int f, cc;
+        tile_fc(lv, i, f, cc);
+        V x = v[j];
+        if (KIND == PASS_FWD_FIRST) {
+          finite &= isfinite(x.x) && isfinite(x.y);
+          reinterpret_cast<V*>(Rb)[base + (int64_t)f * lv.S + cc] = x;
+        }
+        if (DIR > 0) x = cmul(x, Er(tb, g.eb, lv.E2 * (s0 + cc) * f));
+        A[sidx<V>(cc, f, lv.pitch, lv.swz)] = x;
+      }
     }
     if (KIND == PASS_FWD_FIRST) {
       if (!finite) atomicOr(c.bad + b, 1);
@@ -456,25 +514,43 @@ __global__ void __launch_bounds__(kThreads, 3) k_col(const __grid_constant__ Geo
     V* out = cta_fft<DIR>(A, Bf, lv, lv.C, tb.tw);
     if (KIND == PASS_INV_LAST) {
       V* stage = out == A ? Bf : A;
-      for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
-        const int f = i / lv.C, cc = i - f * lv.C;
-        const int64_t gi = base + (int64_t)f * lv.S + cc;
-        const V v = out[cc * lv.pitch + f];
-        __stcs(buf + gi, v);
-        V* Rv = reinterpret_cast<V*>(Rb) + gi;
-        const V r = csub(*Rv, v);
-        *Rv = r;
-        stage[cc * lv.pitch + f] = r;
+      V r[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < FC) {
+          int f, cc;
+          tile_fc(lv, i, f, cc);
+          r[j] = reinterpret_cast<const V*>(Rb)[base + (int64_t)f * lv.S + cc];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < FC) {
+          int f, cc;
+          tile_fc(lv, i, f, cc);
+          const int64_t gi = base + (int64_t)f * lv.S + cc;
+          const V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
+          __stcs(buf + gi, x);
+          const V rn = csub(r[j], x);
+          reinterpret_cast<V*>(Rb)[gi] = rn;
+          stage[sidx<V>(cc, f, lv.pitch, lv.swz)] = rn;
+        }
       }
       __syncthreads();
       tile_segments<Real>(stage, lv, b * g.nseg + s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     } else {
-      for (int i = threadIdx.x; i < lv.F * lv.C; i += blockDim.x) {
-        const int f = i / lv.C, cc = i - f * lv.C;
-        const int64_t gi = base + (int64_t)f * lv.S + cc;
-        V v = out[cc * lv.pitch + f];
-        if (DIR < 0 && lv.E2 > 0) v = cmul(v, cconj(Er(tb, g.eb, lv.E2 * (s0 + cc) * f)));
-        buf[gi] = v;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < FC) {
+          int f, cc;
+          tile_fc(lv, i, f, cc);
+          V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
+          if (DIR < 0) x = cmul(x, cconj(Er(tb, g.eb, lv.E2 * (s0 + cc) * f)));
+          buf[base + (int64_t)f * lv.S + cc] = x;
+        }
       }
     }
     __syncthreads();
@@ -573,20 +649,36 @@ __global__ void __launch_bounds__(kThreads, 3) k_rows_fwd(const __grid_constant_
     int two;
     pair_of<Real>(g, u, ra, rb, bA, two);
     V* Xb = X + b * g.NC;
-    for (int i = threadIdx.x; i < F; i += blockDim.x) {
-      A[i] = Xb[ra * F + i];
-      if (two) A[lv.pitch + i] = Xb[rb * F + i];
+    {
+      constexpr int UR = TileCap<Real>::value / 2 / kThreads;
+      V xa[UR], xb[UR];
+#pragma unroll
+      for (int j = 0; j < UR; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < F) {
+          xa[j] = Xb[ra * F + i];
+          if (two) xb[j] = Xb[rb * F + i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < UR; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < F) {
+          A[sidx<V>(0, i, lv.pitch, lv.swz)] = xa[j];
+          if (two) A[sidx<V>(1, i, lv.pitch, lv.swz)] = xb[j];
+        }
+      }
     }
     V* out = cta_fft<-1>(A, Bf, lv, two ? 2 : 1, tb.tw);
     V* stage = out == A ? Bf : A;
-    const int ob = two ? lv.pitch : 0;
+    const int cb = two ? 1 : 0;
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
       int tm;
       if (!mirror_t(g, bA, two, F, i, tm)) continue;
       const int64_t k = bA + g.P * i;
-      const V Pv = out[i], Q = out[ob + tm];
+      const V Pv = out[sidx<V>(0, i, lv.pitch, lv.swz)], Q = out[sidx<V>(cb, tm, lv.pitch, lv.swz)];
       if (k == 0) {
-        stage[0] = V{Pv.x + Pv.y, (Real)0};
+        stage[sidx<V>(0, 0, lv.pitch, lv.swz)] = V{Pv.x + Pv.y, (Real)0};
         Xn[b] = V{Pv.x - Pv.y, (Real)0};
         continue;
       }
@@ -595,13 +687,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_rows_fwd(const __grid_constant_
       const V D = V{h * (Pv.x - Q.x), h * (Pv.y + Q.y)};
       const V O = V{D.y, -D.x};
       const V TO = cmul(cconj(Er(tb, g.eb, 2 * k)), O);
-      stage[i] = cadd(E, TO);
-      stage[ob + tm] = cconj(csub(E, TO));
+      stage[sidx<V>(0, i, lv.pitch, lv.swz)] = cadd(E, TO);
+      stage[sidx<V>(cb, tm, lv.pitch, lv.swz)] = cconj(csub(E, TO));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
-      Xb[ra * F + i] = stage[i];
-      if (two) Xb[rb * F + i] = stage[lv.pitch + i];
+      Xb[ra * F + i] = stage[sidx<V>(0, i, lv.pitch, lv.swz)];
+      if (two) Xb[rb * F + i] = stage[sidx<V>(1, i, lv.pitch, lv.swz)];
     }
     __syncthreads();
   }
@@ -631,20 +723,40 @@ __global__ void __launch_bounds__(kThreads, 3) k_rows_inv(const __grid_constant_
     pair_of<Real>(g, u, ra, rb, bA, two);
     const int L = c.L[b], N = c.N[b];
     V* Xb = X + b * g.NC;
-    for (int i = threadIdx.x; i < F; i += blockDim.x) {
-      A[i] = Xb[ra * F + i];
-      if (two) A[lv.pitch + i] = Xb[rb * F + i];
+    {
+      constexpr int UR = TileCap<Real>::value / 2 / kThreads;
+      V xa[UR], xb[UR];
+#pragma unroll
+      for (int j = 0; j < UR; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < F) {
+          xa[j] = Xb[ra * F + i];
+          if (two) xb[j] = Xb[rb * F + i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < UR; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < F) {
+          A[sidx<V>(0, i, lv.pitch, lv.swz)] = xa[j];
+          if (two) A[sidx<V>(1, i, lv.pitch, lv.swz)] = xb[j];
+        }
+      }
     }
     __syncthreads();
-    const int ob = two ? lv.pitch : 0;
-    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    const int cb = two ? 1 : 0;
+    // L k mod n, advanced by L P blockDim per iteration
+    int64_t mk = mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
+    const int64_t mstep = mod_n((int64_t)L * ((g.P * blockDim.x) % g.n), g.n, invn);
+    for (int i = threadIdx.x; i < F; i += blockDim.x, mk = (mk + mstep >= g.n) ? mk + mstep - g.n : mk + mstep) {
       int tm;
       if (!mirror_t(g, bA, two, F, i, tm)) continue;
       const int64_t k = bA + g.P * i;
-      const V xk = A[i];
-      const V xm = k == 0 ? Xn[b] : A[ob + tm];
+      const V xk = A[sidx<V>(0, i, lv.pitch, lv.swz)];
+      const V xm = k == 0 ? Xn[b] : A[sidx<V>(cb, tm, lv.pitch, lv.swz)];
       double wk, wm;
-      what_pair(g, tb, L, invn, k, wk, wm);
+      double2 Ek;
+      what_pair_m(g, tb, L, k, mk, wk, wm, Ek);
       double dk, dm;
       if (CAP > 0 && N == CAP) {
         dk = upow_c<CAP>(1.0 - wk);
@@ -656,21 +768,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_rows_inv(const __grid_constant_
       const V Av = cscale(xk, (Real)(dk * invn)), Bv = cscale(xm, (Real)(dm * invn));
       const V S = V{Av.x + Bv.x, Av.y - Bv.y};
       const V D = V{Av.x - Bv.x, Av.y + Bv.y};
-      const V T = mul_i<1>(cmul(Er(tb, g.eb, 2 * k), D));
-      Bf[i] = cadd(S, T);
+      const double2 E2k = cmul(Ek, Ek);  // e^{2 pi i k/n}
+      const V T = mul_i<1>(cmul(V{(Real)E2k.x, (Real)E2k.y}, D));
+      Bf[sidx<V>(0, i, lv.pitch, lv.swz)] = cadd(S, T);
       Xb[ra * F + i] = cscale(xk, (Real)(1.0 - dk));
       if (k == 0) {
         Xn[b] = cscale(xm, (Real)(1.0 - dm));
       } else {
-        Bf[ob + tm] = cconj(csub(S, T));
+        Bf[sidx<V>(cb, tm, lv.pitch, lv.swz)] = cconj(csub(S, T));
         Xb[(two ? rb : ra) * F + tm] = cscale(xm, (Real)(1.0 - dm));
       }
     }
     V* out = cta_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);
     V* W = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
-      W[ra * F + i] = out[i];
-      if (two) W[rb * F + i] = out[lv.pitch + i];
+      W[ra * F + i] = out[sidx<V>(0, i, lv.pitch, lv.swz)];
+      if (two) W[rb * F + i] = out[sidx<V>(1, i, lv.pitch, lv.swz)];
     }
     __syncthreads();
   }
@@ -714,14 +827,30 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
     int two;
     pair_of<Real>(g, ch, ra, rb, bA, two);
     const V* Xb = X + b * g.NC;
-    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    constexpr int UR = TileCap<Real>::value / 2 / kThreads;
+    V xkv[UR], xmv[UR];
+#pragma unroll
+    for (int j = 0; j < UR; ++j) {
+      const int i = threadIdx.x + j * kThreads;
       int tm;
-      if (!mirror_t(g, bA, two, F, i, tm)) continue;
+      if (i < F && mirror_t(g, bA, two, F, i, tm)) {
+        xkv[j] = Xb[ra * F + i];
+        xmv[j] = (bA == 0 && i == 0) ? Xn[b] : Xb[(two ? rb : ra) * F + tm];
+      }
+    }
+    int64_t mk = mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
+    const int64_t mstep = mod_n((int64_t)L * ((g.P * kThreads) % g.n), g.n, invn);
+#pragma unroll
+    for (int j = 0; j < UR; ++j, mk = (mk + mstep >= g.n) ? mk + mstep - g.n : mk + mstep) {
+      const int i = threadIdx.x + j * kThreads;
+      int tm;
+      if (i >= F || !mirror_t(g, bA, two, F, i, tm)) continue;
       const int64_t k = bA + g.P * i;
-      const V xk = Xb[ra * F + i];
-      const V xm = k == 0 ? Xn[b] : Xb[(two ? rb : ra) * F + tm];
+      const V xk = xkv[j];
+      const V xm = xmv[j];
       double wk, wm;
-      what_pair(g, tb, L, invn, k, wk, wm);
+      double2 Ek;
+      what_pair_m(g, tb, L, k, mk, wk, wm, Ek);
       // Parseval weights c_k: 1 for k = 0 and the Nyquist bin, 2 otherwise; a self-paired bin
       // (k = NC - k) is counted once
       const bool self = !two && i == tm && k != 0;

@@ -65,3 +65,32 @@ def test_reference_arm_rank0_only(tmp_path):
 
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+
+
+def _worker_cfg3(rank, world, port, out):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_1802_01359_b200 import signals
+
+    uid = bench.share_uid(rank, lambda: bytes(range(128)))
+    full = signals.cfg3_signal(0, n=1 << 12)
+    blk = bench.time_block(full, rank, world)
+    np.save(os.path.join(out, f"b{rank}.npy"), blk)
+    with open(os.path.join(out, f"u{rank}.bin"), "wb") as f:
+        f.write(uid)
+    dist.destroy_process_group()
+
+
+def test_cfg3_time_blocks_and_uid_broadcast(tmp_path):
+    """Config 3 (distributed plan) host logic: every rank gets rank 0's NCCL id; blocks tile the signal."""
+    world = 2
+    mp.spawn(_worker_cfg3, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    from paper_1802_01359_b200 import signals
+
+    full = signals.cfg3_signal(0, n=1 << 12)
+    blocks = [np.load(tmp_path / f"b{r}.npy") for r in range(world)]
+    np.testing.assert_array_equal(np.concatenate(blocks), full)
+    for r in range(world):
+        assert (tmp_path / f"u{r}.bin").read_bytes() == bytes(range(128))
