@@ -54,7 +54,8 @@ bool st_geometry(int64_t n, bool f64, st::Geo& g) {
   // test-only knobs: smaller level lengths force 3- and 4-level geometries at small n
   if (getenv("FIF_ST_ROWMAX")) rowmax = atoll(getenv("FIF_ST_ROWMAX"));
   if (getenv("FIF_ST_COLMAX")) colmax = atoll(getenv("FIF_ST_COLMAX"));
-  if (n % 2 || NC < 4 || !smooth235(NC)) return false;
+  // L k mod n is evaluated through fp64 (exact below 2^53: L k < n^2/8), so n <= 2^27
+  if (n % 2 || NC < 4 || n > (1LL << 27) || !smooth235(NC)) return false;
   for (int L = 2; L <= st::kMaxLev; ++L) {
     for (int64_t row = rowmax < NC / 2 ? rowmax : NC / 2; row >= 2; --row) {
       if (NC % row || !smooth235(row)) continue;

@@ -57,7 +57,7 @@ def test_unsupported_n_reported():
 
     h = ctypes.c_void_p()
     lib = fif.lib()
-    for n in (7 * 1024, 2 * 11 * 512, 1 << 26, 1 << 28):  # not 2^a 3^b 5^c, or beyond the streamed factorisation
+    for n in (7 * 1024, 2 * 11 * 512, 1 << 28, 3 << 27):  # not 2^a 3^b 5^c, or beyond n = 2^27
         assert lib.fif_plan_create(ctypes.byref(h), n, 1, 0, 0, 1.6, 1e-3, 200, 10) == 2, n
     assert lib.fif_plan_create_ex(ctypes.byref(h), 3 * 1024, 1, 0, 0, 1.6, 1e-3, 200, 10, 1) == 2  # not resident
     assert lib.fif_plan_create_ex(ctypes.byref(h), 1024, 1, 0, 0, 1.6, 1e-3, 200, 10, 9) == 1    # bad regime
