@@ -60,7 +60,12 @@ def lib():
         L.oracle_window.restype = i64
         L.oracle_inner.argtypes = [dp, i64, i64, d, i32, dp, dp, ctypes.c_int]
         L.oracle_inner.restype = i32
-        L.oracle_decompose_batch.argtypes = [dp, i64, i64, ctypes.c_int, d, d, i32, i32, dp, ip, ip, ip, ip, dp]
+        L.oracle_decompose_batch.argtypes = [dp, i64, i64, ctypes.c_int, d, d, i32, i32, dp, ip, ip, ip, ip, dp,
+                                             ctypes.c_int]
+        L.oracle_inner_n0.argtypes = [dp, i64, i64, d, i32, dp, dp, ctypes.c_int]
+        L.oracle_inner_n0.restype = i32
+        L.oracle_dft_inf.argtypes = [dp, i64]
+        L.oracle_dft_inf.restype = d
         L.oracle_decompose_batch.restype = None
         L.oracle_n0_bound.argtypes = [d]
         L.oracle_n0_bound.restype = i64
@@ -114,8 +119,29 @@ def inner(r, L, delta, max_inner, parallel=False):
     return imf, int(N), float(sd[0]), float(sd[1])
 
 
-def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ):
+STOP_SD, STOP_N0 = 0, 1
+
+
+def dft_inf(r):
+    """||U^T r||_inf, U the unitary DFT (reading A16), by the O(n^2) definition."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    return float(lib().oracle_dft_inf(_dp(r), r.shape[0]))
+
+
+def inner_n0(r, L, delta, max_inner, parallel=False):
+    """A-priori rule: (I-W)^N r with N = min(N0, max_inner); returns (imf, N)."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    imf = np.zeros_like(r)
+    sd = np.zeros(4)
+    N = lib().oracle_inner_n0(_dp(r), r.shape[0], int(L), float(delta), int(max_inner), _dp(imf), _dp(sd),
+                              1 if parallel else 0)
+    return imf, int(N)
+
+
+def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, stop=STOP_SD):
     """Time-domain oracle decomposition of a batch [B, n] (or one signal [n]).
+    stop = STOP_SD: the relative SD rule (reading A5); STOP_N0: the a-priori N0 of Thm DIF_conv_stop with
+    the absolute delta (readings A16-A18).
 
     Returns dict: imfs [B, max_imfs+1, n], count [B], l [B, max_imfs], N [B, max_imfs],
     k [B, max_imfs+1] (extrema count at each outer step), margins [B, max_imfs+1, 2]
@@ -130,7 +156,7 @@ def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WI
     k = np.zeros((B, max_imfs + 1), dtype=np.int32)
     margins = np.zeros((B, max_imfs + 1, 2))
     lib().oracle_decompose_batch(_dp(s), B, n, int(window), float(xi), float(delta), int(max_inner), int(max_imfs),
-                                 _dp(imfs), _ip(count), _ip(l), _ip(N), _ip(k), _dp(margins))
+                                 _dp(imfs), _ip(count), _ip(l), _ip(N), _ip(k), _dp(margins), int(stop))
     return {"imfs": imfs, "count": count, "l": l, "N": N, "k": k, "margins": margins}
 
 

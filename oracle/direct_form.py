@@ -27,6 +27,28 @@ import numpy as np
 
 WINDOW_TRI_SQ = 0
 WINDOW_TRI_SQ_WIDE = 1
+STOP_SD, STOP_N0 = 0, 1
+
+
+def n0_f(N: int) -> float:
+    """N^N / (N+1)^(N+1) in the stable form exp(N ln(N/(N+1))) / (N+1)."""
+    return math.exp(N * math.log(N / (N + 1))) / (N + 1)
+
+
+def n0_capped(rhs: float, cap: int) -> int:
+    """min(N0, cap), N0 = the minimum N with n0_f(N) < rhs (Thm DIF_conv_stop)."""
+    for N in range(1, cap + 1):
+        if n0_f(N) < rhs:
+            return N
+    return cap
+
+
+def threshold_pin(d: np.ndarray, gamma: float) -> np.ndarray:
+    """gamma-threshold: whenever (1 - w_hat)^N >= 1 - gamma, w_hat is replaced by
+    zero, i.e. the damping factor becomes exactly 1 (the bin passes whole into the IMF)."""
+    if gamma <= 0.0:
+        return d
+    return np.where(d >= 1.0 - gamma, 1.0, d)
 
 
 def count_extrema(r: np.ndarray) -> int:
@@ -83,9 +105,11 @@ def sd_curve(rhat: np.ndarray, lam: np.ndarray, n: int, max_inner: int) -> np.nd
     return out
 
 
-def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ):
+def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0, stop=STOP_SD):
     """Full FIF decomposition of one real signal.  Returns dict with imfs [(max_imfs+1), n]
-    (trend in slot M), M, l (2L per IMF), N, k (extrema counts), sd (SD_N, SD_{N-1})."""
+    (trend in slot M), M, l (2L per IMF), N, k (extrema counts), sd (SD_N, SD_{N-1}).
+    stop = STOP_N0: N = min(N0, max_inner) from the a-priori bound with the absolute delta (PAPER.md:599,
+    :611-618; readings A16-A18); gamma > 0: the threshold variant (reading A19)."""
     s = np.asarray(s, dtype=np.float64)
     n = s.shape[0]
     r = s.copy()
@@ -106,9 +130,14 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
         lam = eigenvalues(n, L)
         rhat = np.fft.rfft(r)
         curve = sd_curve(rhat, lam, n, max_inner)
-        hit = np.nonzero(curve <= delta)[0]
-        N = int(hit[0]) + 1 if hit.size else max_inner
-        imf = np.fft.irfft(damping(lam, N) * rhat, n)
+        if stop == STOP_N0:
+            # ||U^T r||_inf = max_k |X_k| / sqrt(n) (unitary DFT, A16); k = 0 zero eigenvalues (A17)
+            rhs = delta / (float(np.abs(rhat).max()) / math.sqrt(n) * math.sqrt(n - 1))
+            N = n0_capped(rhs, max_inner)
+        else:
+            hit = np.nonzero(curve <= delta)[0]
+            N = int(hit[0]) + 1 if hit.size else max_inner
+        imf = np.fft.irfft(threshold_pin(damping(lam, N), gamma) * rhat, n)
         imfs[M] = imf
         r = r - imf
         ls.append(2 * L)
@@ -122,9 +151,14 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
         a = np.clip(1.0 - lam, 0.0, 1.0)
         def itn(m):
             return math.sqrt(float(np.sum(cw * np.abs(a ** m * rhat) ** 2)) / n)
-        sm = abs(curve[N - 1] - delta) / delta * (itn(N - 1) / snorm if snorm > 0 else 1.0)
-        if N > 1:
-            sm = min(sm, abs(curve[N - 2] - delta) / delta * (itn(N - 2) / snorm if snorm > 0 else 1.0))
+        if stop == STOP_N0:
+            sm = abs(n0_f(N) / rhs - 1.0)
+            if N > 1:
+                sm = min(sm, abs(n0_f(N - 1) / rhs - 1.0))
+        else:
+            sm = abs(curve[N - 1] - delta) / delta * (itn(N - 1) / snorm if snorm > 0 else 1.0)
+            if N > 1:
+                sm = min(sm, abs(curve[N - 2] - delta) / delta * (itn(N - 2) / snorm if snorm > 0 else 1.0))
         margins[M, 1] = sm
         M += 1
     if M == max_imfs:
@@ -133,7 +167,8 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
     return {"imfs": imfs, "M": M, "l": ls, "N": Ns, "k": ks, "sd": sds, "margins": margins}
 
 
-def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ):
+def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0,
+                    stop=STOP_SD):
     """CPU-DF over a batch, returned in the TD oracle's dict layout (imfs, count, l, N, margins)."""
     S = np.atleast_2d(np.asarray(signals, dtype=np.float64))
     B, n = S.shape
@@ -141,7 +176,7 @@ def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, win
            "l": np.zeros((B, max_imfs), np.int32), "N": np.zeros((B, max_imfs), np.int32),
            "margins": np.full((B, max_imfs + 1, 2), np.nan)}
     for b in range(B):
-        d = decompose(S[b], xi, delta, max_inner, max_imfs, window)
+        d = decompose(S[b], xi, delta, max_inner, max_imfs, window, gamma, stop)
         M = d["M"]
         out["imfs"][b] = d["imfs"]
         out["count"][b] = M

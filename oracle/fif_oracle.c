@@ -151,6 +151,67 @@ static void extend(const double* c, int64_t n, int64_t H, double* cext) {
   }
 }
 
+int64_t oracle_n0_bound(double rhs);
+
+/* ||U^T r||_inf with U the unitary DFT matrix (reading A16: "U^T s is the DFT of s"):
+ * max_k |sum_j r_j e^{-2 pi i jk/n}| / sqrt(n), by the plain O(n^2) definition (exact integer
+ * reduction of jk mod n). */
+double oracle_dft_inf(const double* r, int64_t n) {
+  double mx = 0.0;
+  const double tp = 6.283185307179586476925286766559;
+  for (int64_t k = 0; k <= n / 2; ++k) {
+    double re = 0.0, im = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t m = (j * k) % n;
+      const double a = tp * (double)m / (double)n;
+      re += r[j] * cos(a);
+      im -= r[j] * sin(a);
+    }
+    const double v = sqrt(re * re + im * im);
+    if (v > mx) mx = v;
+  }
+  return mx / sqrt((double)n);
+}
+
+/* ---------------------------------------------------------------------------
+ * A-priori inner loop (Thm DIF_conv_stop; the absolute criterion
+ * ||s_{m+1} - s_m||_2 < delta of Eq. Discrete_Abs_StopCond): N0 = the minimum N0 with
+ * N0^N0/(N0+1)^(N0+1) < delta / (||U^T r||_inf sqrt(n-1-k)), k = 0 (reading A17, SPEC.md:255's
+ * conservative choice), N = min(N0, max_inner) (A18), and IMF = (I-W)^N r by N literal steps.
+ * sd_out[0] = f(N0) / rhs - 1, sd_out[1] = f(N0-1) / rhs - 1 (decision margins; NaN if N0 = 1).
+ * ------------------------------------------------------------------------- */
+static void dif_step(const double* cext, const double* w, int64_t H, int64_t n, double* out, int par);
+static void extend(const double* c, int64_t n, int64_t H, double* cext);
+int32_t oracle_inner_n0(const double* r, int64_t n, int64_t L, double delta, int32_t max_inner, double* imf,
+                        double* sd_out, int par) {
+  const double rhs = delta / (oracle_dft_inf(r, n) * sqrt((double)(n - 1)));
+  int64_t N0 = oracle_n0_bound(rhs);
+  if (N0 < 0 || N0 > max_inner) N0 = max_inner;
+  const int32_t N = (int32_t)N0;
+  int64_t H = 2 * L - 2;
+  double* w = (double*)malloc(sizeof(double) * (size_t)(2 * H + 1));
+  oracle_window(L, w);
+  double* cext = (double*)malloc(sizeof(double) * (size_t)(n + 2 * H));
+  double* c = (double*)malloc(sizeof(double) * (size_t)n);
+  double* cn = (double*)malloc(sizeof(double) * (size_t)n);
+  memcpy(c, r, sizeof(double) * (size_t)n);
+  for (int32_t m = 1; m <= N; ++m) {
+    extend(c, n, H, cext);
+    dif_step(cext, w, H, n, cn, par);
+    double* t = c; c = cn; cn = t;
+  }
+  memcpy(imf, c, sizeof(double) * (size_t)n);
+  if (sd_out) {
+    const double f = exp((double)N0 * log((double)N0 / (double)(N0 + 1))) / (double)(N0 + 1);
+    const double fp = N0 > 1 ? exp((double)(N0 - 1) * log((double)(N0 - 1) / (double)N0)) / (double)N0 : NAN;
+    sd_out[0] = f / rhs - 1.0;
+    sd_out[1] = fp / rhs - 1.0;
+    sd_out[2] = sd_out[3] = 1.0;
+  }
+  free(w); free(cext); free(c); free(cn);
+  return N;
+}
+
 /* ---------------------------------------------------------------------------
  * Inner loop (Alg. 2 inner while; SD PAPER.md:431; cap :433).
  * imf <- (I-W)^N r with N the first m in [1, max_inner] with SD_m <= delta.
@@ -203,7 +264,7 @@ int32_t oracle_inner(const double* r, int64_t n, int64_t L, double delta, int32_
  * ------------------------------------------------------------------------- */
 int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, double delta, int32_t max_inner,
                              int32_t max_imfs, double* imfs, int32_t* l_out, int32_t* N_out, int32_t* k_out,
-                             double* margins, int par) {
+                             double* margins, int par, int stop) {
   double* r = (double*)malloc(sizeof(double) * (size_t)n);
   memcpy(r, s, sizeof(double) * (size_t)n);
   memset(imfs, 0, sizeof(double) * (size_t)n * (size_t)(max_imfs + 1));
@@ -223,11 +284,17 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
     int64_t L = oracle_filter_half_length(xi, n, k, window);
     double sd[4];
     double* imf = imfs + (size_t)M * (size_t)n;
-    int32_t N = oracle_inner(r, n, L, delta, max_inner, imf, sd, par);
+    int32_t N = stop ? oracle_inner_n0(r, n, L, delta, max_inner, imf, sd, par)
+                     : oracle_inner(r, n, L, delta, max_inner, imf, sd, par);
     for (int64_t i = 0; i < n; ++i) r[i] -= imf[i]; /* s = s - s_m */
     l_out[M] = (int32_t)(2 * L);
     N_out[M] = N;
-    if (margins) {
+    if (margins && stop) {
+      /* N0 rule: relative distance of f(N0), f(N0-1) to the right-hand side */
+      double sm = fabs(sd[0]);
+      if (!isnan(sd[1]) && fabs(sd[1]) < sm) sm = fabs(sd[1]);
+      margins[2 * M + 1] = sm;
+    } else if (margins) {
       /* |SD - delta| / delta, scaled by ||iterate|| / ||s||: absolute rounding differences are
          ~1e-16 ||s||, so a decision on a remainder at rounding level has no margin. */
       double sm = fabs(sd[0] - delta) / delta * (snorm > 0.0 ? sd[2] / snorm : 1.0);
@@ -249,7 +316,7 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
  * stencil when batch == 1).  Non-finite input -> count = -1, outputs zeroed. */
 void oracle_decompose_batch(const double* s, int64_t batch, int64_t n, int window, double xi, double delta,
                             int32_t max_inner, int32_t max_imfs, double* imfs, int32_t* counts, int32_t* l_out,
-                            int32_t* N_out, int32_t* k_out, double* margins) {
+                            int32_t* N_out, int32_t* k_out, double* margins, int stop) {
   int par_inner = (batch == 1);
 #pragma omp parallel for schedule(dynamic, 1) if (batch > 1)
   for (int64_t b = 0; b < batch; ++b) {
@@ -268,7 +335,8 @@ void oracle_decompose_batch(const double* s, int64_t batch, int64_t n, int windo
       counts[b] = -1;
       continue;
     }
-    counts[b] = oracle_decompose_one(sb, n, window, xi, delta, max_inner, max_imfs, ib, lb, nb, kb, mb, par_inner);
+    counts[b] = oracle_decompose_one(sb, n, window, xi, delta, max_inner, max_imfs, ib, lb, nb, kb, mb, par_inner,
+                                     stop);
   }
 }
 

@@ -393,3 +393,90 @@ def test_wide_window_two_tone_separation():
     assert len(sig) == 2
     assert np.corrcoef(sig[0], hi)[0, 1] > 0.95
     assert np.corrcoef(sig[1], lo)[0, 1] > 0.95
+
+
+# ------------------------------------------------------------------ NEXT rows: a-priori N0 rule, gamma threshold
+def test_dft_inf_is_the_unitary_dft_max():
+    """oracle_dft_inf (O(n^2) definition) = max |FFT| / sqrt(n) (reading A16: U^T s is the DFT)."""
+    rng = np.random.default_rng(7)
+    for n in (16, 33, 100, 256):
+        r = rng.standard_normal(n)
+        assert abs(oracle.dft_inf(r) - np.abs(np.fft.fft(r)).max() / math.sqrt(n)) <= 1e-12 * math.sqrt(n)
+
+
+def test_n0_rule_pure_tone_closed_form():
+    """Pure tone A cos(2 pi f j/n + phi): ||U^T s||_inf = A sqrt(n)/2 in closed form, so N0 is fixed by
+    Eq. N0_discrete without any DFT, and the IMF is (1 - w_f)^N s (tone = eigenvector)."""
+    n, f, A, phi = 1024, 20, 1.7, 0.4
+    x = A * np.cos(2 * np.pi * f * np.arange(n) / n + phi)
+    for delta in (0.5, 2.0, 8.0):
+        rhs = delta / (A * math.sqrt(n) / 2 * math.sqrt(n - 1))
+        N_expect = next((N for N in range(1, 201) if N ** N / (N + 1) ** (N + 1) < rhs), 200)
+        k = oracle.count_extrema(x)[0]
+        L = oracle.filter_half_length(1.6, n, k)
+        imf, N = oracle.inner_n0(x, L, delta, 200)
+        assert N == N_expect, (delta, N, N_expect)
+        wf = df.eigenvalues(n, L)[f]
+        np.testing.assert_allclose(imf, (1 - wf) ** N * x, atol=1e-12)
+
+
+def test_n0_rule_bound_is_sound():
+    """Thm DIF_conv_stop: after N0 steps, ||s_{N0+1} - s_N0||_2 < delta (N0 below the cap)."""
+    for i in range(4):
+        s = signals.tones_signal(512, 41, i)
+        k = oracle.count_extrema(s)[0]
+        L = oracle.filter_half_length(1.6, 512, k)
+        for delta in (1.0, 3.0):
+            imf, N = oracle.inner_n0(s, L, delta, 10 ** 6)
+            nxt = oracle.inner_n0(imf, L, 1e300, 1)[0]  # one more literal step (N0 = 1 for a huge delta)
+            assert np.linalg.norm(nxt - imf) < delta, (i, delta, N)
+
+
+def test_n0_rule_td_equals_direct_form():
+    s = np.stack([signals.tones_signal(1024, 40, i) for i in range(3)])
+    for delta in (2.0, 5.0):
+        a = oracle.decompose(s, delta=delta, stop=oracle.STOP_N0)
+        b = df.decompose_batch(s, delta=delta, stop=df.STOP_N0)
+        np.testing.assert_array_equal(a["count"], b["count"])
+        np.testing.assert_array_equal(a["l"], b["l"])
+        np.testing.assert_array_equal(a["N"], b["N"])
+        assert np.abs(a["imfs"] - b["imfs"]).max() <= 1e-11
+
+
+def test_gamma_threshold_equivalence_spec_example():
+    """gamma = 0.75, N = 2 -> threshold 1 - 0.5 = 0.5; (1-w)^N >= 1-gamma <=> w <= 1-(1-gamma)^(1/N)."""
+    lam = np.linspace(0.0, 1.0, 100001)
+    pinned = df.threshold_pin(df.damping(lam, 2), 0.75) == 1.0
+    np.testing.assert_array_equal(pinned, lam <= 0.5)
+    for gamma, N in ((0.1, 50), (0.3, 7), (0.9, 200)):
+        th = 1.0 - (1.0 - gamma) ** (1.0 / N)
+        pinned = df.threshold_pin(df.damping(lam, N), gamma) == 1.0
+        off = np.abs(lam - th) > 1e-12
+        np.testing.assert_array_equal(pinned[off], (lam <= th)[off])
+
+
+def test_gamma_threshold_masked_bins_pass_whole():
+    """SPEC.md:251 / PAPER.md:262 (Eq. IMF_cont_stop_threshold): bins in I_gamma pass into the IMF exactly,
+    the others are damped by (1 - w)^N; the IMF is never larger than the remainder (no fake oscillations)."""
+    n = 2048
+    s = signals.tones_signal(n, 42, 0)
+    plain = df.decompose(s, max_imfs=1)
+    th = df.decompose(s, max_imfs=1, gamma=0.3)
+    assert th["l"] == plain["l"] and th["N"] == plain["N"]
+    L, N = th["l"][0] // 2, th["N"][0]
+    lam = df.eigenvalues(n, L)
+    d = np.clip(1 - lam, 0, 1) ** N
+    mask = d >= 0.7
+    assert mask.any() and (~mask).any()
+    S, I = np.fft.rfft(s), np.fft.rfft(th["imfs"][0])
+    np.testing.assert_allclose(I[mask], S[mask], atol=1e-10 * np.abs(S).max())
+    np.testing.assert_allclose(I[~mask], d[~mask] * S[~mask], atol=1e-10 * np.abs(S).max())
+    assert (np.abs(I) <= np.abs(S) + 1e-9 * np.abs(S).max()).all()
+
+
+def test_gamma_to_zero_is_the_plain_method():
+    s = signals.tones_signal(1024, 43, 0)
+    a = df.decompose(s)
+    b = df.decompose(s, gamma=1e-300)
+    assert a["N"] == b["N"] and a["l"] == b["l"]
+    assert np.abs(a["imfs"] - b["imfs"]).max() == 0.0
