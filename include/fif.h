@@ -78,6 +78,20 @@ fif_status fif_plan_create(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype 
 fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window,
                               double xi, double delta, int32_t max_inner, int32_t max_imfs, fif_regime regime);
 
+/* Method options -- SURVEY.md §8f "next" rows; both default off (the graded method):
+ *   stop  : FIF_STOP_SD (default) -- N = the first N with SD_N <= delta, the relative criterion
+ *           (reading A5);
+ *           FIF_STOP_N0 -- the a-priori bound of Thm DIF_conv_stop (Eq. N0_discrete):
+ *           N = min(N0, max_inner), N0 = min N with N^N/(N+1)^(N+1) < delta/(||U^T r||_inf sqrt(n-1)),
+ *           delta read as the ABSOLUTE delta of ||s_{m+1} - s_m||_2 < delta, ||U^T r||_inf =
+ *           max_k |DFT(r)_k| / sqrt(n) (readings A16-A18).
+ *   gamma : 0 = off; 0 < gamma < 1 -- the threshold variant: after N is
+ *           fixed, every bin with (1 - w_hat_k)^N >= 1 - gamma passes into the IMF whole (its damping
+ *           factor becomes 1, its remainder spectrum 0) (reading A19).
+ * Applies to the following fif_decompose calls.  Errors: FIF_ERR_INVALID_ARG (bad values). */
+typedef enum { FIF_STOP_SD = 0, FIF_STOP_N0 = 1 } fif_stop_rule;
+fif_status fif_plan_set_options(fif_plan_t plan, fif_stop_rule stop, double gamma);
+
 /* Decompose the batch (device pointers, caller-owned, current device):
  *   d_signals    [batch][n] dtype, read only.
  *   d_imfs       [batch][max_imfs+1][n] dtype: IMF_0..IMF_{M-1} in slots 0..M-1, the

@@ -165,6 +165,14 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
   return FIF_OK;
 }
 
+fif_status fif_plan_set_options(fif_plan_t p, fif_stop_rule stop, double gamma) {
+  if (!p || (stop != FIF_STOP_SD && stop != FIF_STOP_N0) || !(gamma >= 0.0) || !(gamma < 1.0))
+    return FIF_ERR_INVALID_ARG;
+  p->stop = (int32_t)stop;
+  p->gamma = gamma;
+  return FIF_OK;
+}
+
 fif_status fif_nccl_unique_id(void* out128) {
   if (!out128) return FIF_ERR_INVALID_ARG;
   return nccl_unique_id(out128);

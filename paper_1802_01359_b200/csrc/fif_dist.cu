@@ -93,7 +93,7 @@ __device__ __forceinline__ int64_t local_bin(const st::Geo& g, int64_t pos) {
 // Level tile = C consecutive lower indices x F digit values; DIR -1 forward (DFT, twiddle),
 // +1 inverse (conjugate twiddle, IDFT).  Twiddles use the global-n table (E2 = 2n/(F S)).
 template <typename Real, int DIR>
-__global__ void __launch_bounds__(kThreads, 3) k_d_pass(const __grid_constant__ DGeo d,
+__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_d_pass(const __grid_constant__ DGeo d,
                                                         const __grid_constant__ Level lv,
                                                         typename Cx<Real>::V* __restrict__ buf,
                                                         const __grid_constant__ Tabs<Real> tb,
@@ -376,10 +376,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_d_probe(const __grid_constant__
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  const bool useMax = MODE == 0 && d.g.stop == 1;
   auto add = [&](const V& x, double w, double cw) {
     const double pk = cw * ((double)x.x * (double)x.x + (double)x.y * (double)x.y);
     const double a = 1.0 - w;
-    if constexpr (MODE == 0) {
+    if (useMax) {  // N0 rule: max |X_k|^2
+      acc[0] = fmax(acc[0], pk / cw);
+    } else if constexpr (MODE == 0) {
       double e = (CAP > 0 && N0 == CAP) ? st::upow_c<(CAP > 0 ? CAP - 1 : 1)>(a) : st::upow_rt(a, N0 - 1);
       e *= e;
       acc[0] += pk * e;
@@ -409,13 +412,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_d_probe(const __grid_constant__
   for (int i = 0; i < NV; ++i) {
     double v = acc[i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = useMax ? fmax(v, u) : v + u;
+    }
     if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5][i] = v;
   }
   __syncthreads();
   if (threadIdx.x < NV) {
     double v = 0.0;
-    for (int w = 0; w < kNW; ++w) v += sred[w][threadIdx.x];
+    for (int w = 0; w < kNW; ++w) v = useMax ? fmax(v, sred[w][threadIdx.x]) : v + sred[w][threadIdx.x];
     c.red[(int64_t)blockIdx.x * (2 * kProbes) + threadIdx.x] = v;
   }
   __threadfence();
@@ -425,7 +431,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_d_probe(const __grid_constant__
   if (last && threadIdx.x < NV) {  // this rank's partial: CTA partials in block order
     __threadfence();
     double v = 0.0;
-    for (unsigned bq = 0; bq < gridDim.x; ++bq) v += __ldcg(c.red + (int64_t)bq * (2 * kProbes) + threadIdx.x);
+    for (unsigned bq = 0; bq < gridDim.x; ++bq) {
+      const double u = __ldcg(c.red + (int64_t)bq * (2 * kProbes) + threadIdx.x);
+      v = useMax ? fmax(v, u) : v + u;
+    }
     c.pr_send[threadIdx.x] = v;
     if (threadIdx.x == 0) c.s[S_CNT] = 0;
   }
@@ -439,12 +448,17 @@ __global__ void k_d_decide_probe(const __grid_constant__ DGeo d, DCtl c) {
   if (!s[S_ACT] || (MODE == 1 && !s[S_SEARCH])) return;
   constexpr int NV = MODE == 0 ? 2 : 2 * kProbes;
   double PQ[NV];
+  const bool useMax = MODE == 0 && d.g.stop == 1;
   for (int i = 0; i < NV; ++i) {
     double v = 0.0;
-    for (int r = 0; r < d.P; ++r) v += c.pr_recv[r * (2 * kProbes) + i];
+    for (int r = 0; r < d.P; ++r) v = useMax ? fmax(v, c.pr_recv[r * (2 * kProbes) + i]) : v + c.pr_recv[r * (2 * kProbes) + i];
     PQ[i] = v;
   }
-  if (MODE == 0) {
+  if (useMax) {  // N = min(N0, cap) from the global max |X_k|^2 (A16-A18)
+    const double rhs = d.g.delta / (sqrt(PQ[0] / (double)d.g.n) * sqrt((double)(d.g.n - 1)));
+    s[S_N] = n0_capped(rhs, d.g.max_inner);
+    s[S_SEARCH] = 0;
+  } else if (MODE == 0) {
     s[S_N] = d.g.max_inner;
     if (PQ[1] <= d.g.delta2 * PQ[0]) {
       s[S_LO] = 0;
@@ -495,6 +509,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_d_pre(const __grid_constant__ D
     } else {
       dk = st::upow_rt(1.0 - wk, N);
       dm = st::upow_rt(1.0 - wm, N);
+    }
+    if (d.g.gamma > 0.0) {  // gamma-threshold (A19)
+      if (dk >= 1.0 - d.g.gamma) dk = 1.0;
+      if (dm >= 1.0 - d.g.gamma) dm = 1.0;
     }
     const V xk = X[pos], xm = Xm[pos];
     const V Av = cscale(xk, (Real)(dk * invn)), Bv = cscale(xm, (Real)(dm * invn));
@@ -818,6 +836,11 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
   fif_status st = FIF_OK;
   auto ok = [&](fif_status x) { if (st == FIF_OK) st = x; };
   auto all = [&](auto fn) { for (int li = 0; li < nl; ++li) fn(li, D.ranks[li]); };
+  for (DRank& R : D.ranks) {  // method options (fif_plan_set_options)
+    R.d.g.stop = p->stop;
+    R.d.g.delta = p->delta;
+    R.d.g.gamma = p->gamma;
+  }
   const size_t qb = sizeof(V) * (size_t)Q, wb = sizeof(V) * (size_t)W;
   auto ext_gather = [&]() {
     ok(c_allgather(D, [&](int, DRank& R) { return (const void*)R.c.ext_send; },

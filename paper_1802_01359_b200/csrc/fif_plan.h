@@ -33,6 +33,8 @@ struct fif_plan_s {
   fif_window window = FIF_WINDOW_TRI_SQ;
   double xi = 1.6, delta = 1e-3;
   int32_t max_inner = 200, max_imfs = 10;
+  int32_t stop = 0;     // fif_stop_rule
+  double gamma = 0.0;   // gamma-threshold (0: off)
   int device = 0, num_sms = 0;
   int NC = 0;
   void* d_sin = nullptr;   // Real[NC+1]  sin(pi j/n)

@@ -58,7 +58,29 @@ struct Params {
   int32_t max_inner;
   int32_t max_imfs;
   int32_t window;   // 0 = R1, 1 = R3 (wide)
+  int32_t stop;     // 0: relative SD rule (A5); 1: a-priori N0 with the absolute delta (A16-A18)
+  double delta;     // delta (absolute, for stop = 1)
+  double gamma;     // > 0: gamma-threshold variant (A19)
 };
+
+// ------------------------------------------------------------------ a5 alternative: a-priori N0
+// (Thm DIF_conv_stop): N0 = min N with N^N/(N+1)^(N+1) < rhs, the sequence in the
+// stable form exp(N ln(N/(N+1)))/(N+1); capped at `cap` (A18).  f is strictly
+// decreasing (~1/(e(N+1/2))), so the search starts at that estimate and walks to the minimum.
+__device__ __forceinline__ double n0_f(int N) {
+  return exp((double)N * log((double)N / (double)(N + 1))) / (double)(N + 1);
+}
+__device__ inline int n0_capped(double rhs, int cap) {
+  if (!(rhs > 0.0)) return cap;
+  const double g0 = 1.0 / (2.718281828459045 * rhs) - 3.0;
+  int g = g0 < 1.0 ? 1 : (g0 > (double)cap ? cap : (int)g0);
+  if (n0_f(g) < rhs) {
+    while (g > 1 && n0_f(g - 1) < rhs) --g;
+    return g;
+  }
+  while (g < cap && !(n0_f(g) < rhs)) ++g;
+  return g;
+}
 
 // ------------------------------------------------------------------ radix schedule (compile time)
 // pass 0: radix 4; then the radix-8 factorisation of NC/4 with the leftover (2 or 4) first.
@@ -774,10 +796,36 @@ struct Resident {
     slot ^= 1;
     double Pv, Qv, dd[NB];
     const int cap = p.max_inner;
-    if constexpr (CAP > 0) probe<CAP - 1>(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
-    else probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
     int N = cap;
-    if (Qv <= p.delta2 * Pv) N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
+    if (p.stop == 1) {
+      // N0 rule: ||U^T r||_inf = max_k |X_k| / sqrt(n) (A16), k = 0 zero eigenvalues (A17)
+      double mx = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) mx = fmax(mx, (double)X[q].x * (double)X[q].x + (double)X[q].y * (double)X[q].y);
+      if (j == 0) mx = fmax(mx, (double)Xn.x * (double)Xn.x);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if ((j & 31) == 0) red[j >> 5] = mx;
+      __syncthreads();
+      mx = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) mx = fmax(mx, red[w]);
+      const double rhs = p.delta / (sqrt(mx / (double)n) * sqrt((double)(n - 1)));
+      N = n0_capped(rhs, cap);
+      bool lo, hi;
+      double* red2 = sm.red + slot * 4 * NW;
+      slot ^= 1;
+      verify(X, Xn, sm, L, invL, N, p.delta2, lo, hi, dd, red2, j);
+    } else {
+      if constexpr (CAP > 0) probe<CAP - 1>(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+      else probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+      if (Qv <= p.delta2 * Pv) N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
+    }
+    if (p.gamma > 0.0) {  // gamma-threshold: (1 - w)^N >= 1 - gamma -> factor 1 (A19)
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+        if (dd[q] >= 1.0 - p.gamma) dd[q] = 1.0;
+    }
 #pragma unroll
     for (int q = 0; q < R; ++q) d[q] = (Real)dd[q];
     dn = (Real)dd[R];

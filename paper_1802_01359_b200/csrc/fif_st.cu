@@ -19,13 +19,16 @@ bool smooth235(int64_t x) {
     while (x % f == 0) x /= f;
   return x == 1;
 }
-// radix schedule: 8s, then the leftover power of two (4 or 2), then 3s and 5s
+// radix schedule: powers of two in radix-16 passes, the remainder as one radix-4 or -8 pass (two 8s
+// instead of 16 x 2), then 3s and 5s
 int radices(int64_t N, int* rad) {
   int np = 0, a = 0;
   while (N % 2 == 0) { N /= 2; ++a; }
-  while (a >= 3) { rad[np++] = 8; a -= 3; }
-  if (a == 2) rad[np++] = 4;
-  if (a == 1) rad[np++] = 2;
+  if (a % 4 == 1 && a >= 5) { rad[np++] = 8; rad[np++] = 4; a -= 5; }
+  else if (a % 4 == 1) { rad[np++] = 2; a -= 1; }
+  if (a % 4 == 2) { rad[np++] = 4; a -= 2; }
+  if (a % 4 == 3) { rad[np++] = 8; a -= 3; }
+  while (a >= 4) { rad[np++] = 16; a -= 4; }
   while (N % 3 == 0) { N /= 3; rad[np++] = 3; }
   while (N % 5 == 0) { N /= 5; rad[np++] = 5; }
   return np;
@@ -279,6 +282,9 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     s = nstream > 1 ? p->st_streams[w & 1] : user;
     st::Geo g = p->geo;
     g.batch = batch - b0 < p->st_wave ? batch - b0 : p->st_wave;
+    g.stop = p->stop;
+    g.delta = p->delta;
+    g.gamma = p->gamma;
     const st::Ctl c = ctl_at(p->ctl, g, boff + b0, sizeof(Real));
     const Real* sg = (const Real*)sig + b0 * g.n;
     Real* out = (Real*)imfs + b0 * g.sig_stride;

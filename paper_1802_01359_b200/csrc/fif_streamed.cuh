@@ -42,6 +42,9 @@ constexpr int kMaxPass = 16;
 constexpr int kProbes = 15;  // K-ary search: probes per round
 constexpr int kThreads = 256;
 constexpr int kNW = kThreads / 32;
+#ifndef FIF_ST_MINB
+#define FIF_ST_MINB 3  // resident CTAs per SM the heavy streamed kernels are register-budgeted for
+#endif
 
 struct Level {
   int F;          // sub-FFT length of this digit
@@ -99,6 +102,8 @@ struct Geo {
   int max_imfs, max_inner, window;
   double xi, delta2;
   int64_t sig_stride;    // reals per signal in d_imfs = (max_imfs + 1) n
+  int stop;              // 0: SD rule; 1: a-priori N0 (absolute delta)
+  double delta, gamma;   // delta (absolute, stop = 1); gamma-threshold (0: off)
 };
 
 template <typename Real>
@@ -159,13 +164,62 @@ __device__ __forceinline__ void dft5(V& x0, V& x1, V& x2, V& x3, V& x4) {
   x3 = csub(t2, u2);
 }
 
-// One Stockham pass of radix p over `cols` independent length-Ns FFTs, column c at offset c*pitch
-// (slots through sidx): src[c, i] -> dst[c, j].  tw[j] = e^{-2 pi i j/Ns}.
+// radix-16 DFT (natural order in and out) as 4 x 4 with the internal twiddles e^{DIR 2 pi i n2 k1/16}
 template <int DIR, typename V>
-__device__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int swz, int p, int NS,
-                         const V* __restrict__ tw) {
-  const int per = Ns / p;
-  const int tstride = Ns / (NS * p);
+__device__ __forceinline__ void dft16(V* x) {
+  using S = decltype(x[0].x);
+  const S c1 = (S)0.92387953251128675612818318939678829, s1 = (S)0.38268343236508977172845998403039887;
+  const S h = (S)0.70710678118654752440084436210484903928;
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<DIR>(x[n2], x[4 + n2], x[8 + n2], x[12 + n2]);
+  // y[n2][k1] sits at x[4 k1 + n2]; multiply by w^{n2 k1}, w = e^{DIR 2 pi i/16}
+  auto tw = [&](V& v, S c, S sn) { v = V{v.x * c - (S)DIR * v.y * sn, (S)DIR * v.x * sn + v.y * c}; };
+  tw(x[4 + 1], c1, s1);   // n2 = 1, k1 = 1: w^1
+  tw(x[8 + 1], h, h);     // w^2
+  tw(x[12 + 1], s1, c1);  // w^3
+  tw(x[4 + 2], h, h);     // w^2
+  x[8 + 2] = mul_i<DIR>(x[8 + 2]);  // w^4
+  tw(x[12 + 2], -h, h);   // w^6
+  tw(x[4 + 3], s1, c1);   // w^3
+  tw(x[8 + 3], -h, h);    // w^6
+  tw(x[12 + 3], -c1, -s1);  // w^9
+  V y[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) y[i] = x[i];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    dft4<DIR>(y[4 * k1 + 0], y[4 * k1 + 1], y[4 * k1 + 2], y[4 * k1 + 3]);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = y[4 * k1 + k2];
+  }
+}
+
+template <int P, int DIR, typename V>
+__device__ __forceinline__ void dft_small(V* x) {
+  if constexpr (P == 2) {
+    const V a = cadd(x[0], x[1]), b = csub(x[0], x[1]);
+    x[0] = a;
+    x[1] = b;
+  } else if constexpr (P == 3) {
+    dft3<DIR>(x[0], x[1], x[2]);
+  } else if constexpr (P == 4) {
+    dft4<DIR>(x[0], x[1], x[2], x[3]);
+  } else if constexpr (P == 5) {
+    dft5<DIR>(x[0], x[1], x[2], x[3], x[4]);
+  } else if constexpr (P == 8) {
+    dft8<DIR>(x);
+  } else {
+    dft16<DIR>(x);
+  }
+}
+
+// One Stockham pass of compile-time radix P over `cols` independent length-Ns FFTs, column c at
+// offset c*pitch (slots through sidx): src[c, i] -> dst[c, j].  tw[j] = e^{-2 pi i j/Ns}.
+template <int P, int DIR, typename V>
+__device__ void cta_pass_t(const V* src, V* dst, int Ns, int cols, int pitch, int swz, int NS,
+                           const V* __restrict__ tw) {
+  const int per = Ns / P;
+  const int tstride = Ns / (NS * P);
   const bool pow2 = ((Ns & (Ns - 1)) == 0) && ((NS & (NS - 1)) == 0);
   const int lper = __ffs(per) - 1;
   for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
@@ -179,30 +233,34 @@ __device__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int 
       vt = idx - f * per;
       k = vt % NS;
     }
-    V x[8];
+    V x[P];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < p) x[r] = src[sidx<V>(f, vt + r * per, pitch, swz)];
+    for (int r = 0; r < P; ++r) x[r] = src[sidx<V>(f, vt + r * per, pitch, swz)];
     if (NS > 1) {
+      const int kt = k * tstride;
 #pragma unroll
-      for (int r = 1; r < 8; ++r)
-        if (r < p) {
-          V t = __ldg(tw + k * r * tstride);
-          if (DIR > 0) t.y = -t.y;
-          x[r] = cmul(x[r], t);
-        }
+      for (int r = 1; r < P; ++r) {
+        V t = __ldg(tw + r * kt);
+        if (DIR > 0) t.y = -t.y;
+        x[r] = cmul(x[r], t);
+      }
     }
-    switch (p) {
-      case 2: { V a = cadd(x[0], x[1]), b = csub(x[0], x[1]); x[0] = a; x[1] = b; } break;
-      case 3: dft3<DIR>(x[0], x[1], x[2]); break;
-      case 4: dft4<DIR>(x[0], x[1], x[2], x[3]); break;
-      case 5: dft5<DIR>(x[0], x[1], x[2], x[3], x[4]); break;
-      default: dft8<DIR>(x); break;
-    }
-    const int j0 = (vt - k) * p + k;  // (vt / NS) NS p + k
+    dft_small<P, DIR>(x);
+    const int j0 = (vt - k) * P + k;  // (vt / NS) NS P + k
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < p) dst[sidx<V>(f, j0 + r * NS, pitch, swz)] = x[r];
+    for (int r = 0; r < P; ++r) dst[sidx<V>(f, j0 + r * NS, pitch, swz)] = x[r];
+  }
+}
+template <int DIR, typename V>
+__device__ __forceinline__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int swz, int p, int NS,
+                                         const V* __restrict__ tw) {
+  switch (p) {
+    case 2: cta_pass_t<2, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
+    case 3: cta_pass_t<3, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
+    case 4: cta_pass_t<4, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
+    case 5: cta_pass_t<5, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
+    case 8: cta_pass_t<8, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
+    default: cta_pass_t<16, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
   }
 }
 
@@ -458,7 +516,7 @@ enum { PASS_MID = 0, PASS_FWD_FIRST = 1, PASS_INV_LAST = 2 };
 // non-finite samples, writing extrema partials of s); INV_LAST finishes the IMF in natural order,
 // updates R and writes the extrema partials of the new remainder.
 template <typename Real, int DIR, int KIND>
-__global__ void __launch_bounds__(kThreads, 3) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv, const Real* __restrict__ sig,
+__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv, const Real* __restrict__ sig,
                                                   Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
                                                   const __grid_constant__ Tabs<Real> tb, const __grid_constant__ Ctl c) {
   using V = typename Cx<Real>::V;
@@ -633,7 +691,7 @@ __device__ __forceinline__ bool mirror_t(const Geo& g, int64_t bA, int two, int 
 }
 
 template <typename Real>
-__global__ void __launch_bounds__(kThreads, 3) k_rows_fwd(const __grid_constant__ Geo g, const __grid_constant__ Level lv, typename Cx<Real>::V* __restrict__ X,
+__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid_constant__ Geo g, const __grid_constant__ Level lv, typename Cx<Real>::V* __restrict__ X,
                                                        typename Cx<Real>::V* __restrict__ Xn,
                                                        const __grid_constant__ Tabs<Real> tb,
                                                        const __grid_constant__ Ctl c) {
@@ -704,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_rows_fwd(const __grid_constant_
 // Z_k = S + T, Z_{NC-k} = conj(S - T), S = A + conj B, T = i e^{2 pi i k/n} (A - conj B)
 // (k = 0 pairs with the Nyquist bin), then the length-F IDFT of each row into the IMF slot.
 template <typename Real, int CAP>
-__global__ void __launch_bounds__(kThreads, 3) k_rows_inv(const __grid_constant__ Geo g, const __grid_constant__ Level lv, Real* __restrict__ imfs,
+__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(const __grid_constant__ Geo g, const __grid_constant__ Level lv, Real* __restrict__ imfs,
                                                        typename Cx<Real>::V* __restrict__ X,
                                                        typename Cx<Real>::V* __restrict__ Xn,
                                                        const __grid_constant__ Tabs<Real> tb,
@@ -764,6 +822,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_rows_inv(const __grid_constant_
       } else {
         dk = upow_rt(1.0 - wk, N);
         dm = upow_rt(1.0 - wm, N);
+      }
+      if (g.gamma > 0.0) {  // gamma-threshold (A19)
+        if (dk >= 1.0 - g.gamma) dk = 1.0;
+        if (dm >= 1.0 - g.gamma) dm = 1.0;
       }
       const V Av = cscale(xk, (Real)(dk * invn)), Bv = cscale(xm, (Real)(dm * invn));
       const V S = V{Av.x + Bv.x, Av.y - Bv.y};
@@ -858,7 +920,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
       const double pk = ck * ((double)xk.x * (double)xk.x + (double)xk.y * (double)xk.y);
       const double pm = cm * ((double)xm.x * (double)xm.x + (double)xm.y * (double)xm.y);
       const double ak = 1.0 - wk, am = 1.0 - wm;
-      if constexpr (MODE == 0) {
+      if (MODE == 0 && g.stop == 1) {  // N0 rule: max |X_k|^2 (A16)
+        acc[0] = fmax(acc[0], fmax(pk / ck, cm > 0.0 ? pm / cm : 0.0));
+      } else if constexpr (MODE == 0) {
         double ek, em;
         if (CAP > 0 && N0 == CAP) {
           ek = upow_c<CAP - 1>(ak);
@@ -886,17 +950,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
       }
     }
     constexpr int nv = NV;
+    const bool useMax = MODE == 0 && g.stop == 1;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       double v = acc[i];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = useMax ? fmax(v, u) : v + u;
+      }
       if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5][i] = v;
     }
     __syncthreads();
     if (threadIdx.x < nv) {
       double v = 0.0;
-      for (int w = 0; w < kNW; ++w) v += sred[w][threadIdx.x];
+      for (int w = 0; w < kNW; ++w) v = useMax ? fmax(v, sred[w][threadIdx.x]) : v + sred[w][threadIdx.x];
       c.red[(b * g.nbch + ch) * (2 * kProbes) + threadIdx.x] = v;
     }
     __threadfence();
@@ -913,13 +981,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
       const int64_t a0 = (int64_t)threadIdx.x * per, a1 = min(a0 + per, g.nbch);
       for (int64_t q = a0; q < a1; ++q)
 #pragma unroll
-        for (int i = 0; i < NV; ++i) s[i] += __ldcg(c.red + (b * g.nbch + q) * (2 * kProbes) + i);
+        for (int i = 0; i < NV; ++i) {
+          const double u = __ldcg(c.red + (b * g.nbch + q) * (2 * kProbes) + i);
+          s[i] = useMax ? fmax(s[i], u) : s[i] + u;
+        }
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
         double v = s[i];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        for (int o = 16; o > 0; o >>= 1) {
+          const double u = __shfl_xor_sync(0xffffffffu, v, o);
+          v = useMax ? fmax(v, u) : v + u;
+        }
         if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5][i] = v;
       }
       __syncthreads();
@@ -928,11 +1002,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
           double v = 0.0;
-          for (int w = 0; w < kNW; ++w) v += sred[w][i];
+          for (int w = 0; w < kNW; ++w) v = useMax ? fmax(v, sred[w][i]) : v + sred[w][i];
           PQ[i] = v;
         }
         c.cnt[b] = 0;
-        if constexpr (MODE == 0) {
+        if (useMax) {
+          // N = min(N0, cap), rhs = delta / (||U^T r||_inf sqrt(n-1)), ||U^T r||_inf = max|X| / sqrt(n)
+          const double rhs = g.delta / (sqrt(PQ[0] / (double)g.n) * sqrt((double)(g.n - 1)));
+          c.N[b] = n0_capped(rhs, g.max_inner);
+          c.search[b] = 0;
+        } else if constexpr (MODE == 0) {
           c.N[b] = g.max_inner;
           if (PQ[1] <= g.delta2 * PQ[0]) {  // SD(cap) <= delta: search [1, cap)
             c.lo[b] = 0;

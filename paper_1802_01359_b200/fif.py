@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfif_b200.so")
+LIB_PATH = os.environ.get("FIF_LIB_PATH", os.path.join(_HERE, "libfif_b200.so"))  # override: dev A/B builds
 
 F64, F32 = 0, 1
 WINDOW_TRI_SQ, WINDOW_TRI_SQ_WIDE = 0, 1
@@ -23,7 +23,8 @@ REGIME_AUTO, REGIME_RESIDENT, REGIME_STREAMED = 0, 1, 2
 SYMBOLS = ["fif_plan_create", "fif_plan_create_ex", "fif_decompose", "fif_decompose_host", "fif_destroy", "fif_status_string",
            "fif_plan_kernels_per_call", "fif_plan_regime", "fif_plan_launch_config", "fif_test_rfft",
            "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner", "fif_nccl_unique_id",
-           "fif_plan_create_dist", "fif_plan_create_dist_emulated"]
+           "fif_plan_create_dist", "fif_plan_create_dist_emulated", "fif_plan_set_options"]
+STOP_SD, STOP_N0 = 0, 1
 
 
 class FifError(RuntimeError):
@@ -63,6 +64,7 @@ def lib():
         L.fif_test_window_spectrum.argtypes = [vp, i32, vp, vp]
         L.fif_test_inner.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         L.fif_nccl_unique_id.argtypes = [vp]
+        L.fif_plan_set_options.argtypes = [vp, ctypes.c_int, d]
         L.fif_plan_create_dist.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32, i32, vp,
                                            i32, i32]
         L.fif_plan_create_dist_emulated.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32,
@@ -124,6 +126,11 @@ class Plan:
         lens = torch.empty((self.batch, self.max_imfs), dtype=torch.int32, device=device)
         iters = torch.empty((self.batch, self.max_imfs), dtype=torch.int32, device=device)
         return imfs, count, lens, iters
+
+    def set_options(self, stop=STOP_SD, gamma=0.0):
+        """fif_plan_set_options: stopping rule (STOP_SD / STOP_N0) and gamma-threshold (0 = off)."""
+        _check(lib().fif_plan_set_options(self._h, int(stop), float(gamma)), "fif_plan_set_options")
+        return self
 
     def decompose(self, signals, imfs, count, lens, iters, stream=None):
         """fif_decompose on device tensors (asynchronous on `stream`)."""

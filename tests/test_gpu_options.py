@@ -1,0 +1,98 @@
+"""GPU parity of the method options (SURVEY.md §8f "next" rows) in every regime:
+  * the a-priori N0 stopping rule (Thm DIF_conv_stop; absolute delta, readings A16-A18)
+    against the literal time-domain oracle (which iterates exactly N = min(N0, max_inner) times);
+  * the gamma-threshold variant (reading A19) against the paper's direct form
+    (oracle/direct_form.py; the threshold is a spectral operation, so the literal oracle has none).
+Same protocol as test_gpu_parity.py (integers exact, IMFs <= 1e-9 fp64 / 2e-4 fp32, margin screening)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import direct_form as df  # noqa: E402
+from paper_1802_01359_b200 import fif, signals  # noqa: E402
+from test_gpu_parity import assert_parity  # noqa: E402
+from test_gpu_dist import run_dist  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+
+    ge.build_native()
+    torch.cuda.set_device(0)
+
+
+def run_opt(s, stop=0, gamma=0.0, dtype="f64", regime=fif.REGIME_AUTO, **kw):
+    s = np.ascontiguousarray(s)
+    plan = fif.Plan(s.shape[1], s.shape[0], dtype, regime=regime, **kw).set_options(stop, gamma)
+    x = torch.from_numpy(s).cuda()
+    out = plan.alloc_outputs()
+    plan.decompose(x, *out)
+    torch.cuda.synchronize()
+    res = [t.cpu().numpy() for t in out]
+    plan.close()
+    return res
+
+
+REGIMES = [("resident", fif.REGIME_RESIDENT, 4096), ("streamed", fif.REGIME_STREAMED, 4096),
+           ("streamed-3x", fif.REGIME_STREAMED, 3 * 1024)]
+
+
+@pytest.mark.parametrize("name,regime,n", REGIMES)
+@pytest.mark.parametrize("delta", [8.0, 20.0])
+def test_n0_rule_vs_td_oracle(name, regime, n, delta):
+    s = np.stack([signals.tones_signal(n, 50, i) for i in range(4)])
+    gpu = run_opt(s, stop=fif.STOP_N0, regime=regime, delta=delta)
+    ref = oracle.decompose(s, delta=delta, stop=oracle.STOP_N0)
+    assert (ref["N"][:, :3] < 200).all()  # the rule, not the cap, decides
+    for b in range(4):
+        assert_parity(s[b], gpu, ref, b, b)
+
+
+@pytest.mark.parametrize("name,regime,n", REGIMES)
+@pytest.mark.parametrize("gamma", [0.1, 0.4])
+def test_gamma_threshold_vs_direct_form(name, regime, n, gamma):
+    s = np.stack([signals.tones_signal(n, 51, i) for i in range(4)])
+    gpu = run_opt(s, gamma=gamma, regime=regime)
+    ref = df.decompose_batch(s, gamma=gamma)
+    for b in range(4):
+        assert_parity(s[b], gpu, ref, b, b)
+
+
+def test_gamma_and_n0_combined_fp32():
+    n = 1 << 14
+    s32 = np.stack([signals.cfg4_signal(n, i) for i in range(3)])
+    gpu = run_opt(s32, stop=fif.STOP_N0, gamma=0.2, dtype="f32", delta=20.0)
+    s64 = s32.astype(np.float64)
+    ref = df.decompose_batch(s64, delta=20.0, gamma=0.2, stop=df.STOP_N0)
+    for b in range(3):
+        assert_parity(s64[b], gpu, ref, b, b, "f32")
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_options_distributed(P):
+    n = 4096
+    s = signals.tones_signal(n, 52, 0)
+    plan = fif.Plan.dist(n, 0, P, emulated=True, delta=20.0).set_options(fif.STOP_N0, 0.25)
+    x = torch.from_numpy(np.ascontiguousarray(s.reshape(P, n // P))).cuda()
+    imfs, count, lens, iters = plan.alloc_outputs()
+    plan.decompose(x, imfs, count, lens, iters)
+    torch.cuda.synchronize()
+    full = np.concatenate(list(imfs.cpu().numpy()), axis=1)[None]
+    gpu = [full, count.cpu().numpy()[:1], lens.cpu().numpy()[:1], iters.cpu().numpy()[:1]]
+    plan.close()
+    ref = df.decompose_batch(s[None], delta=20.0, gamma=0.25, stop=df.STOP_N0)
+    assert_parity(s, gpu, ref, 0, 0)
+
+
+def test_options_validation():
+    plan = fif.Plan(1024, 1)
+    for stop, gamma in ((2, 0.0), (0, -0.1), (0, 1.0), (0, float("nan"))):
+        with pytest.raises(fif.FifError):
+            plan.set_options(stop, gamma)
+    plan.close()
