@@ -79,14 +79,13 @@ __device__ __forceinline__ int64_t partner_pos0(const st::Geo& g, int64_t pos) {
   const int F = g.Frow;
   const int64_t row = pos / F;
   const int t = (int)(pos - row * F);
-  const int64_t base = st::base_of_row(g, row);
-  if (base == 0) return (t == 0 ? 0 : F - t);
-  return st::row_of_base(g, g.P - base) * F + (F - 1 - t);
+  if (__ldg(g.rbase + row) == 0) return (t == 0 ? 0 : F - t);
+  return (int64_t)__ldg(g.rmir + row) * F + (F - 1 - t);
 }
 __device__ __forceinline__ int64_t local_bin(const st::Geo& g, int64_t pos) {
   const int F = g.Frow;
   const int64_t row = pos / F;
-  return st::base_of_row(g, row) + g.P * (pos - row * F);
+  return __ldg(g.rbase + row) + g.P * (pos - row * F);
 }
 
 // ---------------------------------------------------------------- local multi-level passes (in place)
@@ -628,6 +627,7 @@ struct DistPlan {
   ncclComm_t comm = nullptr;
   std::vector<DRank> ranks;      // 1 (NCCL) or P (emulated)
   void *Eh = nullptr, *El = nullptr, *Th = nullptr, *Tl = nullptr, *tw = nullptr;
+  void *utab = nullptr, *rbase = nullptr, *rmir = nullptr;
   size_t smem_pass[st::kMaxLev] = {};
   int grid_pass = 0, grid_elem = 0, grid_probe = 0;
   int rounds = 0;
@@ -756,6 +756,10 @@ fif_status dist_setup_t(fif_plan_s* p, DistPlan& D) {
   if ((s = up(&D.Th, Th.data(), sizeof(V) * nh)) != FIF_OK) return s;
   if ((s = up(&D.Tl, Tl.data(), sizeof(V) * nl)) != FIF_OK) return s;
   if ((s = up(&D.tw, tw.data(), sizeof(V) * tw.size())) != FIF_OK) return s;
+  if ((s = st_row_tables(g, &D.utab, &D.rbase, &D.rmir)) != FIF_OK) return s;
+  g.utab = (const int2*)D.utab;
+  g.rbase = (const int*)D.rbase;
+  g.rmir = (const int*)D.rmir;
   // launch shapes
   size_t smax = 0;
   for (int i = 0; i < g.L; ++i) {
@@ -958,6 +962,9 @@ void dist_free(fif_plan_s* p) {
   cudaFree(D->Th);
   cudaFree(D->Tl);
   cudaFree(D->tw);
+  cudaFree(D->utab);
+  cudaFree(D->rbase);
+  cudaFree(D->rmir);
   if (D->comm) nccl().commDestroy(D->comm);
   delete D;
   p->dist = nullptr;

@@ -53,6 +53,9 @@ struct fif_plan_s {
   void* d_X = nullptr;    // V[B][NC] spectrum (digit-reversed multi-level order)
   void* d_Xn = nullptr;   // V[B] Nyquist bins
   void* d_ctl = nullptr;  // per-signal control arrays + partials
+  void* d_utab = nullptr;   // int2[units] mirror-pair rows
+  void* d_rbase = nullptr;  // int[rows] row bin bases
+  void* d_rmir = nullptr;   // int[rows] mirror rows
   fifgpu::st::Ctl ctl{};
   int st_rounds = 0, st_grid = 0, st_grid_col = 0, st_grid_rows = 0, st_grid_probe = 0;
   int64_t st_wave = 1;
@@ -87,6 +90,7 @@ inline const ResOps* res_ops(fif_dtype dt, int NC) { return dt == FIF_F64 ? res_
 
 // streamed regime (fif_st.cu)
 bool st_geometry(int64_t n, bool f64, fifgpu::st::Geo& g);
+fif_status st_row_tables(const fifgpu::st::Geo& g, void** d_utab, void** d_rbase, void** d_rmir);
 fif_status st_setup(fif_plan_s* p);
 // signals [0, batch) of the call use the plan's work buffers from signal `boff` on
 void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,

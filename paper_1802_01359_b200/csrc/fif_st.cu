@@ -118,6 +118,35 @@ bool st_geometry(int64_t n, bool f64, st::Geo& g) {
   }
   return false;
 }
+// row tables of a geometry: utab[u] = (row of base u, row of base (P-u) mod P), rbase[row], rmir[row]
+// (same digit arithmetic as st::row_of_base / base_of_row)
+fif_status st_row_tables(const st::Geo& g, void** d_utab, void** d_rbase, void** d_rmir) {
+  auto row_of_base = [&](int64_t base) {
+    int64_t r = 0;
+    for (int i = 0; i < g.L - 1; ++i) r += ((base / g.Pd[i]) % g.Fd[i]) * g.Sr[i];
+    return r;
+  };
+  auto base_of_row = [&](int64_t row) {
+    int64_t b = 0;
+    for (int i = 0; i < g.L - 1; ++i) b += ((row / g.Sr[i]) % g.Fd[i]) * g.Pd[i];
+    return b;
+  };
+  std::vector<int2> ut(g.units);
+  for (int64_t u = 0; u < g.units; ++u) ut[u] = int2{(int)row_of_base(u), (int)row_of_base((g.P - u) % g.P)};
+  std::vector<int> rb(g.P), rm(g.P);
+  for (int64_t r = 0; r < g.P; ++r) {
+    rb[r] = (int)base_of_row(r);
+    rm[r] = (int)row_of_base((g.P - rb[r]) % g.P);
+  }
+  auto up = [](void** d, const void* h, size_t bytes) {
+    if (cudaMalloc(d, bytes) != cudaSuccess) return FIF_ERR_OOM;
+    return cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice) == cudaSuccess ? FIF_OK : FIF_ERR_CUDA;
+  };
+  fif_status st;
+  if ((st = up(d_utab, ut.data(), sizeof(int2) * ut.size())) != FIF_OK) return st;
+  if ((st = up(d_rbase, rb.data(), sizeof(int) * rb.size())) != FIF_OK) return st;
+  return up(d_rmir, rm.data(), sizeof(int) * rm.size());
+}
 namespace {
 template <typename Real>
 fif_status st_tables(fif_plan_s* p) {
@@ -180,6 +209,10 @@ fif_status st_setup_t(fif_plan_s* p) {
   for (int64_t len = p->max_inner; len > 1; len = (len + st::kProbes) / (st::kProbes + 1)) ++p->st_rounds;
   fif_status s = st_tables<Real>(p);
   if (s != FIF_OK) return s;
+  if ((s = st_row_tables(g, &p->d_utab, &p->d_rbase, &p->d_rmir)) != FIF_OK) return s;
+  g.utab = (const int2*)p->d_utab;
+  g.rbase = (const int*)p->d_rbase;
+  g.rmir = (const int*)p->d_rmir;
   // L2 waves: the working set of a signal (spectrum, remainder, IMF slot: 3 n b bytes) of a wave
   // of signals stays in the 126 MB L2 across the passes of an IMF
   const double wave_mb = getenv("FIF_WAVE_MB") ? atof(getenv("FIF_WAVE_MB")) : 1024.0;
@@ -351,6 +384,9 @@ void st_free(fif_plan_s* p) {
   cudaFree(p->d_X);
   cudaFree(p->d_Xn);
   cudaFree(p->d_ctl);
+  cudaFree(p->d_utab);
+  cudaFree(p->d_rbase);
+  cudaFree(p->d_rmir);
   for (int i = 0; i < 2; ++i)
     if (p->st_streams[i]) cudaStreamDestroy(p->st_streams[i]);
   for (int i = 0; i < 3; ++i)

@@ -67,7 +67,7 @@ struct Level {
 template <typename V>
 __device__ __forceinline__ int sidx(int c, int i, int pitch, int swz) {
   constexpr int ROW = 128 / (int)sizeof(V), LR = sizeof(V) == 16 ? 3 : 4;
-  return c * pitch + (swz ? (i ^ (((i >> LR) ^ c) & (ROW - 1))) : i);
+  return c * pitch + (i ^ (((i >> LR) ^ c) & ((ROW - 1) & -swz)));
 }
 
 // complex elements per tile buffer (F C <= kTile): 32 KiB of shared memory per buffer
@@ -104,6 +104,9 @@ struct Geo {
   int64_t sig_stride;    // reals per signal in d_imfs = (max_imfs + 1) n
   int stop;              // 0: SD rule; 1: a-priori N0 (absolute delta)
   double delta, gamma;   // delta (absolute, stop = 1); gamma-threshold (0: off)
+  const int2* utab;      // [units] rows (ra, rb) of the mirror-pair unit u (bases u and P - u)
+  const int* rbase;      // [P] bin base of each row
+  const int* rmir;       // [P] row holding the mirror bins of each row
 };
 
 template <typename Real>
@@ -523,12 +526,13 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_col(const __grid_cons
   extern __shared__ __align__(16) char smem_raw[];
   V* A = reinterpret_cast<V*>(smem_raw);
   V* Bf = A + (size_t)lv.C * lv.pitch;
-  const int64_t spt = lv.S / lv.C;
-  const int64_t total = g.batch * lv.tiles;
-  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-    const int64_t b = t / lv.tiles, tt = t - b * lv.tiles;
+  const uint32_t spt = (uint32_t)(lv.S / lv.C), tiles = (uint32_t)lv.tiles;
+  const uint32_t total = (uint32_t)(g.batch * lv.tiles);
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t b = t / tiles, tt = t - b * tiles;
     if (KIND != PASS_FWD_FIRST && !c.active[b]) continue;
-    const int64_t a = tt / spt, s0 = (tt - a * spt) * lv.C;
+    const uint32_t a = tt / spt;
+    const int64_t s0 = (int64_t)(tt - a * spt) * lv.C;
     const int64_t base = a * (int64_t)lv.F * lv.S + s0;
     Real* Rb = imfs + b * g.sig_stride + (int64_t)g.max_imfs * g.n;
     V* buf;
@@ -675,9 +679,9 @@ __global__ void __launch_bounds__(kThreads) k_fold(const __grid_constant__ Geo g
 template <typename Real>
 __device__ __forceinline__ void pair_of(const Geo& g, int64_t u, int64_t& ra, int64_t& rb, int64_t& bA, int& two) {
   bA = u;
-  const int64_t bB = (g.P - u) % g.P;
-  ra = row_of_base(g, bA);
-  rb = row_of_base(g, bB);
+  const int2 r = __ldg(g.utab + u);
+  ra = r.x;
+  rb = r.y;
   two = ra != rb;
 }
 // mirror element of t (row a) and whether the pair is processed from t
@@ -700,8 +704,9 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
   V* A = reinterpret_cast<V*>(smem_raw);
   V* Bf = A + 2 * lv.pitch;
   const int F = lv.F;
-  for (int64_t t = blockIdx.x; t < g.batch * g.units; t += gridDim.x) {
-    const int64_t b = t / g.units, u = t - b * g.units;
+  const uint32_t units = (uint32_t)g.units;
+  for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.units); t += gridDim.x) {
+    const uint32_t b = t / units, u = t - b * units;
     if (!c.active[b]) continue;
     int64_t ra, rb, bA;
     int two;
@@ -773,8 +778,9 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(const __grid
   V* Bf = A + 2 * lv.pitch;
   const int F = lv.F;
   const double invn = 1.0 / (double)g.n;
-  for (int64_t t = blockIdx.x; t < g.batch * g.units; t += gridDim.x) {
-    const int64_t b = t / g.units, u = t - b * g.units;
+  const uint32_t units = (uint32_t)g.units;
+  for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.units); t += gridDim.x) {
+    const uint32_t b = t / units, u = t - b * units;
     if (!c.active[b]) continue;
     int64_t ra, rb, bA;
     int two;
@@ -868,9 +874,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
   __shared__ int last;
   const int F = g.Frow;
   const double invn = 1.0 / (double)g.n;
-  for (int64_t t = blockIdx.x; t < g.batch * g.nbch; t += gridDim.x) {
-    const int64_t b = t / g.nbch;
-    const int64_t ch = t - b * g.nbch;
+  const uint32_t nbch = (uint32_t)g.nbch;
+  for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.nbch); t += gridDim.x) {
+    const uint32_t b = t / nbch;
+    const uint32_t ch = t - b * nbch;
     if (!c.active[b] || (mode == 1 && !c.search[b])) continue;
     const int L = c.L[b];
     int N0, step;

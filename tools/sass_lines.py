@@ -8,7 +8,7 @@ iA, iS, iW, iE = h.index("Address"), h.index("Source"), h.index("Warp Stall Samp
 cnt, stall, ops = {}, {}, {}
 base = None
 for r in rows[2:]:
-    if len(r) < len(h): continue
+    if len(r) < len(h) or not (r[iA].startswith("0x") or r[iA].isdigit()): continue
     a = int(r[iA], 16) if r[iA].startswith("0x") else int(r[iA])
     if base is None: base = a
     a -= base
@@ -34,7 +34,7 @@ for ln in open(sys.argv[2]):
             byline_ops[line][op.split('.')[0]] += cnt[a]
 tot = sum(byline.values()); tst = sum(byline_st.values())
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-src = open("/root/repo/paper_1802_01359_b200/csrc/fif_resident.cuh").read().split("\n")
+src = open(sys.argv[4] if len(sys.argv) > 4 else "/root/repo/paper_1802_01359_b200/csrc/fif_resident.cuh").read().split("\n")
 for l, c in byline.most_common(top):
     s = src[l - 1].strip()[:70] if l else ""
     print(f"{l:5} {c/tot*100:5.1f}% st {byline_st[l]/tst*100:5.1f}%  {dict(byline_ops[l].most_common(4))}  | {s}")
