@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -222,12 +223,13 @@ fif_status st_setup_t(fif_plan_s* p) {
   const int64_t B = p->batch > 0 ? p->batch : 1;
   if (wave > B) wave = B;
   p->st_wave = wave;
-  const size_t ni = (size_t)B * 10;
+  const size_t ni = (size_t)B * 11;
   const size_t segb = (size_t)B * g.nseg * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t grpb = (size_t)B * g.ngrp * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t redb = (size_t)B * g.nbch * 2 * st::kProbes * sizeof(double);
   const size_t ctl_bytes = ni * sizeof(int32_t) + segb + grpb + redb + 256;
-  if (cudaMalloc(&p->d_X, sizeof(V) * B * g.NC) != cudaSuccess || cudaMalloc(&p->d_Xn, sizeof(V) * B) != cudaSuccess ||
+  // two spectrum buffers (X_in / X_out ping-pong per IMF: the speculative damping keeps X_in intact)
+  if (cudaMalloc(&p->d_X, 2 * sizeof(V) * B * g.NC) != cudaSuccess || cudaMalloc(&p->d_Xn, 2 * sizeof(V) * B) != cudaSuccess ||
       cudaMalloc(&p->d_ctl, ctl_bytes) != cudaSuccess)
     return FIF_ERR_OOM;
   char* q = (char*)p->d_ctl;
@@ -244,7 +246,7 @@ fif_status st_setup_t(fif_plan_s* p) {
   c.gi = (uint32_t*)take((size_t)B * g.ngrp * sizeof(uint32_t));
   int32_t* ip = (int32_t*)take(ni * sizeof(int32_t));
   c.k = ip; c.L = ip + B; c.N = ip + 2 * B; c.M = ip + 3 * B; c.active = ip + 4 * B; c.search = ip + 5 * B;
-  c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B);
+  c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B); c.redo = ip + 10 * B;
   if (cudaMemset(p->d_ctl, 0, ctl_bytes) != cudaSuccess) return FIF_ERR_CUDA;
   // shared memory and grids
   for (int i = 0; i < g.L - 1; ++i) p->st_smem_col[i] = 2 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch;
@@ -260,14 +262,16 @@ fif_status st_setup_t(fif_plan_s* p) {
   attr(st::k_col<Real, 1, st::PASS_MID>);
   attr(st::k_col<Real, 1, st::PASS_INV_LAST>);
   attr(st::k_rows_fwd<Real>);
-  attr(st::k_rows_inv<Real, 0>);
-  attr(st::k_rows_inv<Real, kFastCap>);
+  attr(st::k_rows_inv<Real, 0, 0>);
+  attr(st::k_rows_inv<Real, kFastCap, 0>);
+  attr(st::k_rows_inv<Real, 0, 1>);
+  attr(st::k_rows_inv<Real, kFastCap, 1>);
   if (e != cudaSuccess) {
     fprintf(stderr, "fif: streamed setup failed: %s\n", cudaGetErrorString(e));
     return FIF_ERR_CUDA;
   }
   p->st_grid_col = occ_grid(p, st::k_col<Real, 1, st::PASS_INV_LAST>, smax);
-  p->st_grid_rows = occ_grid(p, st::k_rows_inv<Real, kFastCap>, p->st_smem_rows);
+  p->st_grid_rows = occ_grid(p, st::k_rows_inv<Real, kFastCap, 1>, p->st_smem_rows);
   p->st_grid_probe = occ_grid(p, st::k_probe<Real, kFastCap, 1>, 0);
   p->st_grid = p->st_grid_rows;
   for (int i = 0; i < 2; ++i)
@@ -321,8 +325,11 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     const st::Ctl c = ctl_at(p->ctl, g, boff + b0, sizeof(Real));
     const Real* sg = (const Real*)sig + b0 * g.n;
     Real* out = (Real*)imfs + b0 * g.sig_stride;
-    V* X = (V*)p->d_X + (boff + b0) * g.NC;
+    const int64_t Bp = p->batch > 0 ? p->batch : 1;
+    V* X = (V*)p->d_X + (boff + b0) * g.NC;        // X_0 (forward transform output)
     V* Xn = (V*)p->d_Xn + boff + b0;
+    V* Xalt = (V*)p->d_X + (Bp + boff + b0) * g.NC;  // X_1
+    V* Xnalt = (V*)p->d_Xn + Bp + boff + b0;
     int32_t* ln = lens + b0 * g.max_imfs;
     int32_t* it = its + b0 * g.max_imfs;
     const int Lv = g.L;
@@ -340,14 +347,29 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
       st::k_col<Real, -1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], sg, out, X, tb, c);
     st::k_rows_fwd<Real><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     for (int m = 0; m < g.max_imfs; ++m) {
-      if (fast) {
-        st::k_probe<Real, kFastCap, 0><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
-        for (int r = 0; r < p->st_rounds; ++r) st::k_probe<Real, kFastCap, 1><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
-        st::k_rows_inv<Real, kFastCap><<<grow, TB, p->st_smem_rows, s>>>(g, top, out, X, Xn, tb, c);
+      V* Xi = (m & 1) ? Xalt : X;
+      V* Xo = (m & 1) ? X : Xalt;
+      V* Xni = (m & 1) ? Xnalt : Xn;
+      V* Xno = (m & 1) ? Xn : Xnalt;
+      auto rows = [&](auto spec, auto cap, int redo_only) {
+        st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value>
+            <<<grow, TB, p->st_smem_rows, s>>>(g, top, out, Xi, Xo, Xni, Xno, tb, c, redo_only);
+      };
+      auto probe = [&](auto cap, auto mode) {
+        st::k_probe<Real, decltype(cap)::value, decltype(mode)::value><<<gprobe, TB, 0, s>>>(g, Xi, Xni, tb, c);
+      };
+      using F0 = std::integral_constant<int, 0>;
+      using F1 = std::integral_constant<int, 1>;
+      using FC = std::integral_constant<int, kFastCap>;
+      if (g.stop == 0) {
+        // SD rule: fused cap probe + speculative damping; K-ary search and a redo only if SD(cap) <= delta
+        if (fast) rows(F1{}, FC{}, 0); else rows(F1{}, F0{}, 0);
+        for (int r = 0; r < p->st_rounds; ++r) probe(F0{}, F1{});
+        if (fast) rows(F0{}, FC{}, 1); else rows(F0{}, F0{}, 1);
       } else {
-        st::k_probe<Real, 0, 0><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
-        for (int r = 0; r < p->st_rounds; ++r) st::k_probe<Real, 0, 1><<<gprobe, TB, 0, s>>>(g, X, Xn, tb, c);
-        st::k_rows_inv<Real, 0><<<grow, TB, p->st_smem_rows, s>>>(g, top, out, X, Xn, tb, c);
+        // a-priori N0 rule: one max-reduction probe decides N, then the damping
+        if (fast) probe(FC{}, F0{}); else probe(F0{}, F0{});
+        if (fast) rows(F0{}, FC{}, 0); else rows(F0{}, F0{}, 0);
       }
       for (int i = Lv - 2; i >= 1; --i)
         st::k_col<Real, 1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], sg, out, X, tb, c);
@@ -366,7 +388,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
 int st_kernels_per_call(const fif_plan_s* p) {
   const int L = p->geo.L;
   const int64_t waves = p->batch > 0 ? (p->batch + p->st_wave - 1) / p->st_wave : 0;
-  return (int)(waves * (2 + (L - 1) + 1 + p->max_imfs * (1 + p->st_rounds + L + 1) + 1));
+  const int per_imf = p->stop == 0 ? (p->st_rounds + L + 2) : (L + 2);
+  return (int)(waves * (2 + (L - 1) + 1 + p->max_imfs * per_imf + 1));
 }
 
 fif_status st_setup(fif_plan_s* p) { return p->dtype == FIF_F64 ? st_setup_t<double>(p) : st_setup_t<float>(p); }

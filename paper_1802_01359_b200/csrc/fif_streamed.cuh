@@ -130,6 +130,7 @@ struct Ctl {
   int32_t* lo;      // search bracket: !pass(lo) (lo = 0 virtual), pass(hi)
   int32_t* hi;
   int32_t* bad;     // non-finite input seen
+  int32_t* redo;    // 1: the speculative N = cap damping of this IMF is void (SD(cap) <= delta)
   uint32_t* cnt;    // last-CTA counters
   uint32_t* segi;   // [B][nseg] packed extrema monoid of a segment's internal differences
   void* segv;       // [B][nseg][2] Real: first and last sample of the segment
@@ -506,6 +507,7 @@ static __global__ void k_init(const __grid_constant__ Geo g, const __grid_consta
     c.bad[b] = 0;
     c.active[b] = 1;
     c.search[b] = 0;
+    c.redo[b] = 0;
     c.cnt[b] = 0;
   }
 }
@@ -763,17 +765,24 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
 }
 
 // ------------------------------------------------------------------ a6 damping + pre-processing + row IDFTs
-// d = a^N (a = 1 - w_hat); X <- (1 - d) X; with A = d_k X_k/n, B = d_{NC-k} X_{NC-k}/n:
+// d = a^N (a = 1 - w_hat); X_out = (1 - d) X_in; with A = d_k X_k/n, B = d_{NC-k} X_{NC-k}/n:
 // Z_k = S + T, Z_{NC-k} = conj(S - T), S = A + conj B, T = i e^{2 pi i k/n} (A - conj B)
 // (k = 0 pairs with the Nyquist bin), then the length-F IDFT of each row into the IMF slot.
-template <typename Real, int CAP>
-__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(const __grid_constant__ Geo g, const __grid_constant__ Level lv, Real* __restrict__ imfs,
-                                                       typename Cx<Real>::V* __restrict__ X,
-                                                       typename Cx<Real>::V* __restrict__ Xn,
-                                                       const __grid_constant__ Tabs<Real> tb,
-                                                       const __grid_constant__ Ctl c) {
+// SPEC = 1 (relative SD rule): the a5 cap probe is fused in -- N = cap is assumed (the common case,
+// 70-97% of IMFs), the Parseval sums P, Q at the cap are accumulated from the same a^{cap-1}, and
+// the last CTA of a signal decides; if SD(cap) <= delta the damping was speculative: `redo` is set,
+// the K-ary search reads the untouched X_in, and a SPEC = 0 launch with redo_only recomputes X_out
+// and the IMF slot for those signals.  X_in / X_out (and the Nyquist bins) ping-pong per IMF.
+template <typename Real, int CAP, int SPEC>
+__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
+    const __grid_constant__ Geo g, const __grid_constant__ Level lv, Real* __restrict__ imfs,
+    const typename Cx<Real>::V* __restrict__ Xin, typename Cx<Real>::V* __restrict__ Xout,
+    const typename Cx<Real>::V* __restrict__ Xnin, typename Cx<Real>::V* __restrict__ Xnout,
+    const __grid_constant__ Tabs<Real> tb, const __grid_constant__ Ctl c, int redo_only) {
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
+  __shared__ double sred[kNW][2];
+  __shared__ int last;
   V* A = reinterpret_cast<V*>(smem_raw);
   V* Bf = A + 2 * lv.pitch;
   const int F = lv.F;
@@ -781,12 +790,13 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(const __grid
   const uint32_t units = (uint32_t)g.units;
   for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.units); t += gridDim.x) {
     const uint32_t b = t / units, u = t - b * units;
-    if (!c.active[b]) continue;
+    if (!c.active[b] || (!SPEC && redo_only && !c.redo[b])) continue;
     int64_t ra, rb, bA;
     int two;
     pair_of<Real>(g, u, ra, rb, bA, two);
-    const int L = c.L[b], N = c.N[b];
-    V* Xb = X + b * g.NC;
+    const int L = c.L[b], N = SPEC ? g.max_inner : c.N[b];
+    const V* Xb = Xin + b * g.NC;
+    V* Xo = Xout + b * g.NC;
     {
       constexpr int UR = TileCap<Real>::value / 2 / kThreads;
       V xa[UR], xb[UR];
@@ -809,6 +819,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(const __grid
     }
     __syncthreads();
     const int cb = two ? 1 : 0;
+    double sP = 0.0, sQ = 0.0;
     // L k mod n, advanced by L P blockDim per iteration
     int64_t mk = mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
     const int64_t mstep = mod_n((int64_t)L * ((g.P * blockDim.x) % g.n), g.n, invn);
@@ -817,17 +828,36 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(const __grid
       if (!mirror_t(g, bA, two, F, i, tm)) continue;
       const int64_t k = bA + g.P * i;
       const V xk = A[sidx<V>(0, i, lv.pitch, lv.swz)];
-      const V xm = k == 0 ? Xn[b] : A[sidx<V>(cb, tm, lv.pitch, lv.swz)];
+      const V xm = k == 0 ? Xnin[b] : A[sidx<V>(cb, tm, lv.pitch, lv.swz)];
       double wk, wm;
       double2 Ek;
       what_pair_m(g, tb, L, k, mk, wk, wm, Ek);
+      const double ak = 1.0 - wk, am = 1.0 - wm;
       double dk, dm;
-      if (CAP > 0 && N == CAP) {
-        dk = upow_c<CAP>(1.0 - wk);
-        dm = upow_c<CAP>(1.0 - wm);
+      if (SPEC) {
+        double ek, em;  // a^{cap-1}
+        if (CAP > 0) {
+          ek = upow_c<(CAP > 0 ? CAP - 1 : 1)>(ak);
+          em = upow_c<(CAP > 0 ? CAP - 1 : 1)>(am);
+        } else {
+          ek = upow_rt(ak, N - 1);
+          em = upow_rt(am, N - 1);
+        }
+        // Parseval weights c_k: 1 for k = 0 and the Nyquist bin, 2 otherwise; a self-paired bin once
+        const bool self = !two && i == tm && k != 0;
+        const double ck = k == 0 ? 1.0 : 2.0, cm = self ? 0.0 : (k == 0 ? 1.0 : 2.0);
+        const double pk = ck * ((double)xk.x * (double)xk.x + (double)xk.y * (double)xk.y) * (ek * ek);
+        const double pm = cm * ((double)xm.x * (double)xm.x + (double)xm.y * (double)xm.y) * (em * em);
+        sP += pk + pm;
+        sQ += pk * wk * wk + pm * wm * wm;
+        dk = ek * ak;
+        dm = em * am;
+      } else if (CAP > 0 && N == CAP) {
+        dk = upow_c<(CAP > 0 ? CAP : 1)>(ak);
+        dm = upow_c<(CAP > 0 ? CAP : 1)>(am);
       } else {
-        dk = upow_rt(1.0 - wk, N);
-        dm = upow_rt(1.0 - wm, N);
+        dk = upow_rt(ak, N);
+        dm = upow_rt(am, N);
       }
       if (g.gamma > 0.0) {  // gamma-threshold (A19)
         if (dk >= 1.0 - g.gamma) dk = 1.0;
@@ -839,19 +869,75 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(const __grid
       const double2 E2k = cmul(Ek, Ek);  // e^{2 pi i k/n}
       const V T = mul_i<1>(cmul(V{(Real)E2k.x, (Real)E2k.y}, D));
       Bf[sidx<V>(0, i, lv.pitch, lv.swz)] = cadd(S, T);
-      Xb[ra * F + i] = cscale(xk, (Real)(1.0 - dk));
+      Xo[ra * F + i] = cscale(xk, (Real)(1.0 - dk));
       if (k == 0) {
-        Xn[b] = cscale(xm, (Real)(1.0 - dm));
+        Xnout[b] = cscale(xm, (Real)(1.0 - dm));
       } else {
         Bf[sidx<V>(cb, tm, lv.pitch, lv.swz)] = cconj(csub(S, T));
-        Xb[(two ? rb : ra) * F + tm] = cscale(xm, (Real)(1.0 - dm));
+        Xo[(two ? rb : ra) * F + tm] = cscale(xm, (Real)(1.0 - dm));
       }
     }
-    V* out = cta_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);
+    if (SPEC) {  // unit partial sums -> c.red, last CTA of the signal decides (fixed order)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sP += __shfl_xor_sync(0xffffffffu, sP, o);
+        sQ += __shfl_xor_sync(0xffffffffu, sQ, o);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        sred[threadIdx.x >> 5][0] = sP;
+        sred[threadIdx.x >> 5][1] = sQ;
+      }
+    }
+    V* out = cta_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);  // (its first barrier also publishes sred)
     V* W = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
       W[ra * F + i] = out[sidx<V>(0, i, lv.pitch, lv.swz)];
       if (two) W[rb * F + i] = out[sidx<V>(1, i, lv.pitch, lv.swz)];
+    }
+    if (SPEC) {
+      if (threadIdx.x < 2) {
+        double v = 0.0;
+        for (int w = 0; w < kNW; ++w) v += sred[w][threadIdx.x];
+        c.red[((int64_t)b * g.nbch + u) * (2 * kProbes) + threadIdx.x] = v;
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) last = atomicAdd(c.cnt + b, 1u) == (uint32_t)(g.units - 1);
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        double s2[2] = {0.0, 0.0};
+        const int64_t per = (g.units + blockDim.x - 1) / blockDim.x;
+        const int64_t a0 = (int64_t)threadIdx.x * per, a1 = min(a0 + per, g.units);
+        for (int64_t q = a0; q < a1; ++q)
+#pragma unroll
+          for (int i2 = 0; i2 < 2; ++i2) s2[i2] += __ldcg(c.red + ((int64_t)b * g.nbch + q) * (2 * kProbes) + i2);
+        __syncthreads();
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+          double v = s2[i2];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5][i2] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double Pv = 0.0, Qv = 0.0;
+          for (int w = 0; w < kNW; ++w) {
+            Pv += sred[w][0];
+            Qv += sred[w][1];
+          }
+          c.cnt[b] = 0;
+          c.N[b] = g.max_inner;
+          c.redo[b] = 0;
+          if (Qv <= g.delta2 * Pv && g.max_inner > 1) {  // SD(cap) <= delta: search [1, cap), redo
+            c.lo[b] = 0;
+            c.hi[b] = g.max_inner;
+            c.search[b] = 1;
+            c.redo[b] = 1;
+          }
+        }
+      }
     }
     __syncthreads();
   }
