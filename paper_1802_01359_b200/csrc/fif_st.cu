@@ -249,7 +249,7 @@ fif_status st_setup_t(fif_plan_s* p) {
   c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B); c.redo = ip + 10 * B;
   if (cudaMemset(p->d_ctl, 0, ctl_bytes) != cudaSuccess) return FIF_ERR_CUDA;
   // shared memory and grids
-  for (int i = 0; i < g.L - 1; ++i) p->st_smem_col[i] = 2 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch;
+  for (int i = 0; i < g.L - 1; ++i) p->st_smem_col[i] = 3 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch;
   p->st_smem_rows = 2 * sizeof(V) * 2 * (size_t)g.lv[g.L - 1].pitch;
   size_t smax = p->st_smem_rows;
   for (int i = 0; i < g.L - 1; ++i) smax = smax > p->st_smem_col[i] ? smax : p->st_smem_col[i];
@@ -341,10 +341,10 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     const int gsig = (int)((g.batch + TB - 1) / TB);
     auto col = [&](int i) { return grid_for(g.batch * g.lv[i].tiles, gcol); };
     st::k_init<<<gsig, TB, 0, s>>>(g, c);
-    st::k_col<Real, -1, st::PASS_FWD_FIRST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], sg, out, X, tb, c);
+    st::k_col<Real, -1, st::PASS_FWD_FIRST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
     st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
     for (int i = 1; i < Lv - 1; ++i)
-      st::k_col<Real, -1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], sg, out, X, tb, c);
+      st::k_col<Real, -1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i], sg, out, X, tb, c);
     st::k_rows_fwd<Real><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     for (int m = 0; m < g.max_imfs; ++m) {
       V* Xi = (m & 1) ? Xalt : X;
@@ -353,7 +353,7 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
       V* Xno = (m & 1) ? Xn : Xnalt;
       auto rows = [&](auto spec, auto cap, int redo_only) {
         st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value>
-            <<<grow, TB, p->st_smem_rows, s>>>(g, top, out, Xi, Xo, Xni, Xno, tb, c, redo_only);
+            <<<grow, TB, p->st_smem_rows, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
       };
       auto probe = [&](auto cap, auto mode) {
         st::k_probe<Real, decltype(cap)::value, decltype(mode)::value><<<gprobe, TB, 0, s>>>(g, Xi, Xni, tb, c);
@@ -372,8 +372,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
         if (fast) rows(F0{}, FC{}, 0); else rows(F0{}, F0{}, 0);
       }
       for (int i = Lv - 2; i >= 1; --i)
-        st::k_col<Real, 1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], sg, out, X, tb, c);
-      st::k_col<Real, 1, st::PASS_INV_LAST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], sg, out, X, tb, c);
+        st::k_col<Real, 1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
+      st::k_col<Real, 1, st::PASS_INV_LAST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
       st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 1, ln, it);
     }
     st::k_final<Real><<<grid_for(g.batch, p->num_sms * 4), TB, 0, s>>>(g, out, c, cnt + b0, ln, it);

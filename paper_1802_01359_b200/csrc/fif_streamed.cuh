@@ -434,34 +434,80 @@ __device__ __forceinline__ Mono block_mono(Mono m, Mono* sm) {
 }
 
 // Segment partials of a level-0 tile held in shared memory as complex pairs: segment f consists of
-// the 2C reals of columns c = 0..C-1 (element (c, f) at buf[c*pitch + f]); one warp per segment.
+// the 2C reals of columns c = 0..C-1 (element (c, f) at slot sidx(c, f)); one warp per segment.
+// Fast path (no zero difference in the segment): lane l owns the differences starting at its reals,
+// the last one reaching into lane l+1's first real; sign changes = popc of adjacent sign-bit XORs
+// inside a lane + the lane-boundary transitions, summed with a warp reduction.  A zero difference
+// anywhere in the segment (plateau collapse, reading A4) switches the warp to the exact ordered
+// monoid fold.
 template <typename Real>
 __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, int64_t seg0, int64_t segstep,
                               uint32_t* __restrict__ segi, Real* __restrict__ segv) {
+  using V = typename Cx<Real>::V;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nd = 2 * lv.C - 1;  // internal differences
-  const int q = (nd + 31) / 32;
+  const int nr = 2 * lv.C;           // reals per segment
+  const int per = (nr + 31) / 32;    // reals per lane (the fast path needs <= 64)
+  const int j0 = lane * per, j1 = min(j0 + per, nr);
   for (int f = warp; f < lv.F; f += nw) {
-    Mono m{0, 0, 0};
-    const int d0 = lane * q, d1 = min(d0 + q, nd);
-    if (d0 < d1) {
-      auto x_at = [&](int j) -> Real {
-        const auto v = buf[sidx<typename Cx<Real>::V>(j >> 1, f, lv.pitch, lv.swz)];
-        return (j & 1) ? v.y : v.x;
-      };
-      Real prev = x_at(d0);
-      for (int j = d0; j < d1; ++j) {
-        const Real x = x_at(j + 1);
-        m = mcomb(m, mdiff<Real>(x - prev));
+    auto x_at = [&](int j) -> Real {
+      const V v = buf[sidx<V>(j >> 1, f, lv.pitch, lv.swz)];
+      return (j & 1) ? v.y : v.x;
+    };
+    // this lane's reals and the first real of the next lane
+    Real first = (Real)0, prev = (Real)0;
+    uint64_t bits = 0;
+    int nd = 0;
+    bool zero = per > 64;
+    if (j0 < j1 && !zero) {
+      first = x_at(j0);
+      prev = first;
+      for (int j = j0 + 1; j < j1; ++j) {
+        const Real x = x_at(j);
+        const Real d = x - prev;
+        zero |= (d == (Real)0);
+        bits |= (uint64_t)(d < (Real)0) << nd;
+        ++nd;
         prev = x;
       }
     }
-    m = warp_mono(m);
+    const Real nxt = __shfl_down_sync(0xffffffffu, first, 1);
+    if (j0 < j1 && j1 < nr && per <= 64) {  // the difference into the next lane's first real
+      const Real d = nxt - prev;
+      zero |= (d == (Real)0);
+      bits |= (uint64_t)(d < (Real)0) << nd;
+      ++nd;
+    }
+    Mono m;
+    if (!__any_sync(0xffffffffu, zero)) {
+      const int inner = nd > 1 ? __popcll((bits ^ (bits >> 1)) & ((nd - 1 >= 64) ? ~0ull : ((1ull << (nd - 1)) - 1ull))) : 0;
+      const int fb = nd ? (int)(bits & 1ull) : -1, lb = nd ? (int)((bits >> (nd - 1)) & 1ull) : -1;
+      const int fnext = __shfl_down_sync(0xffffffffu, fb, 1);
+      const int edge = (nd && lane < 31 && fnext >= 0 && fnext != lb) ? 1 : 0;
+      const int total = __reduce_add_sync(0xffffffffu, inner + edge);
+      // first / last nonzero signs of the segment (no zeros: the first and the last difference)
+      const int f0 = __shfl_sync(0xffffffffu, fb, 0);
+      const int lastLane = (nr - 2) / per;  // owner of the last difference (reals nr-2 -> nr-1)
+      const int l0 = __shfl_sync(0xffffffffu, lb, lastLane);
+      m = Mono{f0 < 0 ? 0 : (f0 ? -1 : 1), l0 < 0 ? 0 : (l0 ? -1 : 1), total};
+    } else {
+      m = Mono{0, 0, 0};
+      const int nd2 = nr - 1, q = (nd2 + 31) / 32;
+      const int d0 = lane * q, d1 = min(d0 + q, nd2);
+      if (d0 < d1) {
+        Real pv = x_at(d0);
+        for (int j = d0; j < d1; ++j) {
+          const Real x = x_at(j + 1);
+          m = mcomb(m, mdiff<Real>(x - pv));
+          pv = x;
+        }
+      }
+      m = warp_mono(m);
+    }
     if (lane == 0) {
-      const int64_t s = seg0 + (int64_t)f * segstep;
-      segi[s] = mpack(m);
-      segv[2 * s] = buf[sidx<typename Cx<Real>::V>(0, f, lv.pitch, lv.swz)].x;
-      segv[2 * s + 1] = buf[sidx<typename Cx<Real>::V>(lv.C - 1, f, lv.pitch, lv.swz)].y;
+      const int64_t sg = seg0 + (int64_t)f * segstep;
+      segi[sg] = mpack(m);
+      segv[2 * sg] = buf[sidx<V>(0, f, lv.pitch, lv.swz)].x;
+      segv[2 * sg + 1] = buf[sidx<V>(lv.C - 1, f, lv.pitch, lv.swz)].y;
     }
   }
 }
@@ -515,96 +561,165 @@ static __global__ void k_init(const __grid_constant__ Geo g, const __grid_consta
 // ------------------------------------------------------------------ column passes
 enum { PASS_MID = 0, PASS_FWD_FIRST = 1, PASS_INV_LAST = 2 };
 
+// cp.async (Ampere+ LDGSTS) helpers: global -> shared without registers, completion by groups
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(gsrc), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // Tile = C consecutive lower indices s x the F digit values, of block a.  DIR -1: forward (DFT, then
-// twiddle), +1: inverse (conjugate twiddle, then IDFT).  Buffers: forward passes work on X; inverse
-// passes on the IMF slot M of the signal.  FWD_FIRST reads the signal (copying it to R, flagging
-// non-finite samples, writing extrema partials of s); INV_LAST finishes the IMF in natural order,
-// updates R and writes the extrema partials of the new remainder.
+// the level's twiddle at the store), +1: inverse (IDFT; the input already carries this level's
+// conjugate twiddle, applied by the producer, and the store applies the NEXT coarser level's, lvn).
+// Forward passes work on X; inverse passes on the IMF slot M of the signal.  FWD_FIRST reads the
+// signal (copying it to R, flagging non-finite samples, writing extrema partials of s); INV_LAST
+// finishes the IMF in natural order, updates R and writes the extrema partials of the new remainder.
+// Persistent CTAs, software-pipelined: the next tile streams into a third shared buffer with
+// cp.async while the current one is transformed.
 template <typename Real, int DIR, int KIND>
-__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv, const Real* __restrict__ sig,
-                                                  Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
-                                                  const __grid_constant__ Tabs<Real> tb, const __grid_constant__ Ctl c) {
+__global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv,
+                                                     const __grid_constant__ Level lvn, const Real* __restrict__ sig,
+                                                     Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
+                                                     const __grid_constant__ Tabs<Real> tb,
+                                                     const __grid_constant__ Ctl c) {
   using V = typename Cx<Real>::V;
   extern __shared__ __align__(16) char smem_raw[];
-  V* A = reinterpret_cast<V*>(smem_raw);
-  V* Bf = A + (size_t)lv.C * lv.pitch;
+  const size_t bufsz = (size_t)lv.C * lv.pitch;
+  V* S[3] = {reinterpret_cast<V*>(smem_raw), reinterpret_cast<V*>(smem_raw) + bufsz,
+             reinterpret_cast<V*>(smem_raw) + 2 * bufsz};
   const uint32_t spt = (uint32_t)(lv.S / lv.C), tiles = (uint32_t)lv.tiles;
   const uint32_t total = (uint32_t)(g.batch * lv.tiles);
-  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
-    const uint32_t b = t / tiles, tt = t - b * tiles;
-    if (KIND != PASS_FWD_FIRST && !c.active[b]) continue;
-    const uint32_t a = tt / spt;
-    const int64_t s0 = (int64_t)(tt - a * spt) * lv.C;
-    const int64_t base = a * (int64_t)lv.F * lv.S + s0;
-    Real* Rb = imfs + b * g.sig_stride + (int64_t)g.max_imfs * g.n;
+  const int FC = lv.F * lv.C;
+  constexpr int U = TileCap<Real>::value / kThreads;
+  auto active = [&](uint32_t t) { return KIND == PASS_FWD_FIRST || c.active[t / tiles]; };
+  auto next_tile = [&](uint32_t t) {
+    for (; t < total; t += gridDim.x)
+      if (active(t)) return t;
+    return total;
+  };
+  // tile geometry
+  struct TG {
+    uint32_t b, a;
+    int64_t s0, base;
     V* buf;
-    if (DIR < 0) buf = X + b * g.NC;
-    else buf = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
-    const V* src = KIND == PASS_FWD_FIRST ? reinterpret_cast<const V*>(sig + b * g.n) : buf;
-    const int FC = lv.F * lv.C;
-    constexpr int U = TileCap<Real>::value / kThreads;
-    // all of this thread's tile loads in flight at once
-    V v[U];
+    const V* src;
+  };
+  auto geo = [&](uint32_t t) {
+    TG r;
+    r.b = t / tiles;
+    const uint32_t tt = t - r.b * tiles;
+    r.a = tt / spt;
+    r.s0 = (int64_t)(tt - r.a * spt) * lv.C;
+    r.base = r.a * (int64_t)lv.F * lv.S + r.s0;
+    if (DIR < 0) r.buf = X + r.b * g.NC;
+    else r.buf = reinterpret_cast<V*>(imfs + r.b * g.sig_stride + (int64_t)c.M[r.b] * g.n);
+    r.src = KIND == PASS_FWD_FIRST ? reinterpret_cast<const V*>(sig + r.b * g.n) : r.buf;
+    return r;
+  };
+  auto issue = [&](const TG& q, V* dst) {
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int i = threadIdx.x + j * kThreads;
       if (i < FC) {
         int f, cc;
         tile_fc(lv, i, f, cc);
-        v[j] = src[base + (int64_t)f * lv.S + cc];
+        cp_async<(int)sizeof(V)>(dst + sidx<V>(cc, f, lv.pitch, lv.swz), q.src + q.base + (int64_t)f * lv.S + cc);
       }
     }
-    bool finite = true;
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int i = threadIdx.x + j * kThreads;
-      if (i < FC) {
-        int f, cc;
-        tile_fc(lv, i, f, cc);
-        V x = v[j];
-        if (KIND == PASS_FWD_FIRST) {
-          finite &= isfinite(x.x) && isfinite(x.y);
-          reinterpret_cast<V*>(Rb)[base + (int64_t)f * lv.S + cc] = x;
-        }
-        if (DIR > 0) x = cmul(x, Er(tb, g.eb, lv.E2 * (s0 + cc) * f));
-        A[sidx<V>(cc, f, lv.pitch, lv.swz)] = x;
-      }
+  };
+  uint32_t t = next_tile(blockIdx.x);
+  TG cur{};
+  if (t < total) {
+    cur = geo(t);
+    issue(cur, S[0]);
+  }
+  cp_async_commit();
+  for (int it = 0; t < total; ++it) {
+    const uint32_t tn = next_tile(t + gridDim.x);
+    TG nxt{};
+    if (tn < total) {
+      nxt = geo(tn);
+      issue(nxt, S[(it + 1) % 3]);
     }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    V* In = S[it % 3];
+    V* Sc = S[(it + 2) % 3];
+    Real* Rb = imfs + cur.b * g.sig_stride + (int64_t)g.max_imfs * g.n;
     if (KIND == PASS_FWD_FIRST) {
-      if (!finite) atomicOr(c.bad + b, 1);
-      __syncthreads();
-      tile_segments<Real>(A, lv, b * g.nseg + s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
-    }
-    V* out = cta_fft<DIR>(A, Bf, lv, lv.C, tb.tw);
-    if (KIND == PASS_INV_LAST) {
-      V* stage = out == A ? Bf : A;
-      V r[U];
+      bool finite = true;
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int i = threadIdx.x + j * kThreads;
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
-          r[j] = reinterpret_cast<const V*>(Rb)[base + (int64_t)f * lv.S + cc];
+          const V x = In[sidx<V>(cc, f, lv.pitch, lv.swz)];
+          finite &= isfinite(x.x) && isfinite(x.y);
+          reinterpret_cast<V*>(Rb)[cur.base + (int64_t)f * lv.S + cc] = x;
         }
       }
+      if (!finite) atomicOr(c.bad + cur.b, 1);
+      tile_segments<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+    }
+    V r[KIND == PASS_INV_LAST ? U : 1];
+    if (KIND == PASS_INV_LAST) {  // remainder loads in flight during the transform
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int i = threadIdx.x + j * kThreads;
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
-          const int64_t gi = base + (int64_t)f * lv.S + cc;
+          r[j] = reinterpret_cast<const V*>(Rb)[cur.base + (int64_t)f * lv.S + cc];
+        }
+      }
+    }
+    V* out = cta_fft<DIR>(In, Sc, lv, lv.C, tb.tw);
+    if (KIND == PASS_INV_LAST) {
+      V* stage = out == In ? Sc : In;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = threadIdx.x + j * kThreads;
+        if (i < FC) {
+          int f, cc;
+          tile_fc(lv, i, f, cc);
+          const int64_t gi = cur.base + (int64_t)f * lv.S + cc;
           const V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
-          __stcs(buf + gi, x);
+          __stcs(cur.buf + gi, x);
           const V rn = csub(r[j], x);
           reinterpret_cast<V*>(Rb)[gi] = rn;
           stage[sidx<V>(cc, f, lv.pitch, lv.swz)] = rn;
         }
       }
       __syncthreads();
-      tile_segments<Real>(stage, lv, b * g.nseg + s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+      tile_segments<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     } else {
+      // forward: this level's twiddle e^{-2 pi i s k/(F S)}; inverse: the next coarser level's
+      // e^{+2 pi i s' k'/(F' S')} with s' = f S + s, k' = a mod F'.  When C divides the block size a
+      // thread's column cc is fixed and its digit f advances by kThreads/C per element, so the
+      // twiddles form a geometric sequence: two table products per thread, one multiply per element.
+      const int64_t kn = DIR > 0 ? (int64_t)(cur.a % (uint32_t)lvn.F) : 0;
+      const bool geom = lv.cs >= 0 && lv.C <= kThreads;
+      V w{(Real)1, (Real)0}, ws{(Real)1, (Real)0};
+      if (geom) {
+        int f0, c0;
+        tile_fc(lv, threadIdx.x, f0, c0);
+        const int64_t df = kThreads >> lv.cs;
+        if (DIR < 0) {
+          w = cconj(Er(tb, g.eb, lv.E2 * (cur.s0 + c0) * f0));
+          ws = cconj(Er(tb, g.eb, lv.E2 * ((cur.s0 + c0) * df % ((int64_t)lv.F * lv.S))));
+        } else {
+          w = Er(tb, g.eb, lvn.E2 * (((int64_t)f0 * lv.S + cur.s0 + c0) * kn % ((int64_t)lvn.F * lvn.S)));
+          ws = Er(tb, g.eb, lvn.E2 * ((df * lv.S * kn) % ((int64_t)lvn.F * lvn.S)));
+        }
+      }
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int i = threadIdx.x + j * kThreads;
@@ -612,13 +727,23 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_col(const __grid_cons
           int f, cc;
           tile_fc(lv, i, f, cc);
           V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
-          if (DIR < 0) x = cmul(x, cconj(Er(tb, g.eb, lv.E2 * (s0 + cc) * f)));
-          buf[base + (int64_t)f * lv.S + cc] = x;
+          if (geom) {
+            x = cmul(x, w);
+            w = cmul(w, ws);
+          } else if (DIR < 0) {
+            x = cmul(x, cconj(Er(tb, g.eb, lv.E2 * (cur.s0 + cc) * f)));
+          } else {
+            x = cmul(x, Er(tb, g.eb, lvn.E2 * (((int64_t)f * lv.S + cur.s0 + cc) * kn % ((int64_t)lvn.F * lvn.S))));
+          }
+          cur.buf[cur.base + (int64_t)f * lv.S + cc] = x;
         }
       }
     }
     __syncthreads();
+    t = tn;
+    cur = nxt;
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ a2/a3/a7 fold of extrema partials
@@ -775,7 +900,8 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
 // and the IMF slot for those signals.  X_in / X_out (and the Nyquist bins) ping-pong per IMF.
 template <typename Real, int CAP, int SPEC>
 __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
-    const __grid_constant__ Geo g, const __grid_constant__ Level lv, Real* __restrict__ imfs,
+    const __grid_constant__ Geo g, const __grid_constant__ Level lv, const __grid_constant__ Level lvn,
+    Real* __restrict__ imfs,
     const typename Cx<Real>::V* __restrict__ Xin, typename Cx<Real>::V* __restrict__ Xout,
     const typename Cx<Real>::V* __restrict__ Xnin, typename Cx<Real>::V* __restrict__ Xnout,
     const __grid_constant__ Tabs<Real> tb, const __grid_constant__ Ctl c, int redo_only) {
@@ -890,9 +1016,20 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
     }
     V* out = cta_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);  // (its first barrier also publishes sred)
     V* W = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
+    // the next (coarser) level's conjugate twiddle e^{+2 pi i s k'/(F' S')}: s = element, k' = row mod F'
+    // (geometric in i: two table products per row and thread, one multiply per element)
+    const int64_t ka = ra % lvn.F, kb = rb % lvn.F;
+    const int64_t FSn = (int64_t)lvn.F * lvn.S;
+    V wa = Er(tb, g.eb, lvn.E2 * ((int64_t)threadIdx.x * ka % FSn)), wb = Er(tb, g.eb, lvn.E2 * ((int64_t)threadIdx.x * kb % FSn));
+    const V sa = Er(tb, g.eb, lvn.E2 * ((int64_t)blockDim.x * ka % FSn));
+    const V sb = Er(tb, g.eb, lvn.E2 * ((int64_t)blockDim.x * kb % FSn));
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
-      W[ra * F + i] = out[sidx<V>(0, i, lv.pitch, lv.swz)];
-      if (two) W[rb * F + i] = out[sidx<V>(1, i, lv.pitch, lv.swz)];
+      W[ra * F + i] = cmul(out[sidx<V>(0, i, lv.pitch, lv.swz)], wa);
+      wa = cmul(wa, sa);
+      if (two) {
+        W[rb * F + i] = cmul(out[sidx<V>(1, i, lv.pitch, lv.swz)], wb);
+        wb = cmul(wb, sb);
+      }
     }
     if (SPEC) {
       if (threadIdx.x < 2) {
