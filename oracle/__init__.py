@@ -61,7 +61,9 @@ def lib():
         L.oracle_inner.argtypes = [dp, i64, i64, d, i32, dp, dp, ctypes.c_int]
         L.oracle_inner.restype = i32
         L.oracle_decompose_batch.argtypes = [dp, i64, i64, ctypes.c_int, d, d, i32, i32, dp, ip, ip, ip, ip, dp,
-                                             ctypes.c_int]
+                                             ctypes.c_int, ctypes.c_int]
+        L.oracle_spectral_peak.argtypes = [dp, i64, dp]
+        L.oracle_spectral_peak.restype = i64
         L.oracle_inner_n0.argtypes = [dp, i64, i64, d, i32, dp, dp, ctypes.c_int]
         L.oracle_inner_n0.restype = i32
         L.oracle_dft_inf.argtypes = [dp, i64]
@@ -120,6 +122,15 @@ def inner(r, L, delta, max_inner, parallel=False):
 
 
 STOP_SD, STOP_N0 = 0, 1
+MASK_EXTREMA, MASK_SPECTRAL = 0, 1
+
+
+def spectral_peak(r):
+    """(f*, margin): the highest-frequency significant local maximum of |DFT(r)|^2 (A20)."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    m = np.zeros(1)
+    f = lib().oracle_spectral_peak(_dp(r), r.shape[0], _dp(m))
+    return int(f), float(m[0])
 
 
 def dft_inf(r):
@@ -138,7 +149,8 @@ def inner_n0(r, L, delta, max_inner, parallel=False):
     return imf, int(N)
 
 
-def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, stop=STOP_SD):
+def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, stop=STOP_SD,
+              mask=MASK_EXTREMA):
     """Time-domain oracle decomposition of a batch [B, n] (or one signal [n]).
     stop = STOP_SD: the relative SD rule (reading A5); STOP_N0: the a-priori N0 of Thm DIF_conv_stop with
     the absolute delta (readings A16-A18).
@@ -156,7 +168,7 @@ def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WI
     k = np.zeros((B, max_imfs + 1), dtype=np.int32)
     margins = np.zeros((B, max_imfs + 1, 2))
     lib().oracle_decompose_batch(_dp(s), B, n, int(window), float(xi), float(delta), int(max_inner), int(max_imfs),
-                                 _dp(imfs), _ip(count), _ip(l), _ip(N), _ip(k), _dp(margins), int(stop))
+                                 _dp(imfs), _ip(count), _ip(l), _ip(N), _ip(k), _dp(margins), int(stop), int(mask))
     return {"imfs": imfs, "count": count, "l": l, "N": N, "k": k, "margins": margins}
 
 

@@ -43,6 +43,32 @@ def n0_capped(rhs: float, cap: int) -> int:
     return cap
 
 
+MASK_EXTREMA, MASK_SPECTRAL = 0, 1
+
+
+def spectral_peak(rhat: np.ndarray) -> tuple:
+    """(f*, margin) from the rfft bins (reading A20): the largest f in 1..n/2 that is a local
+    maximum of p = |X|^2 (p_f > p_{f-1} for f > 1, p_f >= p_{f+1} for f < n/2) with p_f >= 1e-4 max p."""
+    p = rhat.real ** 2 + rhat.imag ** 2
+    NC = p.shape[0] - 1
+    M = float(p[1:].max()) if NC >= 1 else 0.0
+    thr, mg = 1e-4 * M, math.inf
+    for f in range(NC, 0, -1):
+        if M <= 0.0:
+            break
+        gap, ok = abs(p[f] - thr), p[f] >= thr
+        if ok and f > 1:
+            ok = p[f] > p[f - 1]
+            gap = min(gap, abs(p[f] - p[f - 1]))
+        if ok and f < NC:
+            ok = p[f] >= p[f + 1]
+            gap = min(gap, abs(p[f] - p[f + 1]))
+        mg = min(mg, gap / M)
+        if ok:
+            return f, mg
+    return 0, mg
+
+
 def threshold_pin(d: np.ndarray, gamma: float) -> np.ndarray:
     """gamma-threshold: whenever (1 - w_hat)^N >= 1 - gamma, w_hat is replaced by
     zero, i.e. the damping factor becomes exactly 1 (the bin passes whole into the IMF)."""
@@ -105,7 +131,8 @@ def sd_curve(rhat: np.ndarray, lam: np.ndarray, n: int, max_inner: int) -> np.nd
     return out
 
 
-def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0, stop=STOP_SD):
+def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0, stop=STOP_SD,
+              mask=MASK_EXTREMA):
     """Full FIF decomposition of one real signal.  Returns dict with imfs [(max_imfs+1), n]
     (trend in slot M), M, l (2L per IMF), N, k (extrema counts), sd (SD_N, SD_{N-1}).
     stop = STOP_N0: N = min(N0, max_inner) from the a-priori bound with the absolute delta (PAPER.md:599,
@@ -126,9 +153,16 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
         margins[M, 0] = (dd.min() / scale) if (dd.size and scale > 0) else np.inf
         if k < 2:
             break
-        L = filter_half_length(xi, n, k, window)
-        lam = eigenvalues(n, L)
         rhat = np.fft.rfft(r)
+        if mask == MASK_SPECTRAL:  # L from k = 2 f* (A20)
+            fs, pm = spectral_peak(rhat)
+            margins[M, 0] = min(margins[M, 0], pm)
+            if fs == 0:
+                break
+            L = filter_half_length(xi, n, 2 * fs, window)
+        else:
+            L = filter_half_length(xi, n, k, window)
+        lam = eigenvalues(n, L)
         curve = sd_curve(rhat, lam, n, max_inner)
         if stop == STOP_N0:
             # ||U^T r||_inf = max_k |X_k| / sqrt(n) (unitary DFT, A16); k = 0 zero eigenvalues (A17)
@@ -168,7 +202,7 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
 
 
 def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0,
-                    stop=STOP_SD):
+                    stop=STOP_SD, mask=MASK_EXTREMA):
     """CPU-DF over a batch, returned in the TD oracle's dict layout (imfs, count, l, N, margins)."""
     S = np.atleast_2d(np.asarray(signals, dtype=np.float64))
     B, n = S.shape
@@ -176,7 +210,7 @@ def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, win
            "l": np.zeros((B, max_imfs), np.int32), "N": np.zeros((B, max_imfs), np.int32),
            "margins": np.full((B, max_imfs + 1, 2), np.nan)}
     for b in range(B):
-        d = decompose(S[b], xi, delta, max_inner, max_imfs, window, gamma, stop)
+        d = decompose(S[b], xi, delta, max_inner, max_imfs, window, gamma, stop, mask)
         M = d["M"]
         out["imfs"][b] = d["imfs"]
         out["count"][b] = M

@@ -173,6 +173,45 @@ double oracle_dft_inf(const double* r, int64_t n) {
   return mx / sqrt((double)n);
 }
 
+/* Spectral-peak filter length ("the identification of its highest frequency peak. The
+ * filter length l can be chosen to be proportional to the reciprocal of this value"; reading A20):
+ * p_f = |X_f|^2 (plain O(n^2) DFT), f = 1..n/2; the peak is the LARGEST f that is a local maximum
+ * (p_f > p_{f-1} for f > 1, p_f >= p_{f+1} for f < n/2) with p_f >= 1e-4 max_f p_f (1% in magnitude,
+ * SPEC.md:112).  Returns f* (0: no such bin -- a flat spectrum); L then follows the extrema rule with
+ * k = 2 f* (a tone of f* periods has 2 f* extrema).  margin_out: the smallest relative gap
+ * (/ max p) among the comparisons that decided f*. */
+int64_t oracle_spectral_peak(const double* r, int64_t n, double* margin_out) {
+  const int64_t NC = n / 2;
+  double* p = (double*)malloc(sizeof(double) * (size_t)(NC + 2));
+  const double tp = 6.283185307179586476925286766559;
+  double M = 0.0;
+  for (int64_t f = 1; f <= NC; ++f) {
+    double re = 0.0, im = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t m = (j * f) % n;
+      const double a = tp * (double)m / (double)n;
+      re += r[j] * cos(a);
+      im -= r[j] * sin(a);
+    }
+    p[f] = re * re + im * im;
+    if (p[f] > M) M = p[f];
+  }
+  const double thr = 1e-4 * M;
+  int64_t fs = 0;
+  double mg = INFINITY;
+  for (int64_t f = NC; f >= 1 && M > 0.0; --f) {
+    double gap = fabs(p[f] - thr);
+    int ok = p[f] >= thr;
+    if (ok && f > 1) { ok = p[f] > p[f - 1]; if (fabs(p[f] - p[f - 1]) < gap) gap = fabs(p[f] - p[f - 1]); }
+    if (ok && f < NC) { ok = p[f] >= p[f + 1]; if (fabs(p[f] - p[f + 1]) < gap) gap = fabs(p[f] - p[f + 1]); }
+    if (gap / M < mg) mg = gap / M;
+    if (ok) { fs = f; break; }
+  }
+  if (margin_out) *margin_out = mg;
+  free(p);
+  return fs;
+}
+
 /* ---------------------------------------------------------------------------
  * A-priori inner loop (Thm DIF_conv_stop; the absolute criterion
  * ||s_{m+1} - s_m||_2 < delta of Eq. Discrete_Abs_StopCond): N0 = the minimum N0 with
@@ -264,7 +303,7 @@ int32_t oracle_inner(const double* r, int64_t n, int64_t L, double delta, int32_
  * ------------------------------------------------------------------------- */
 int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, double delta, int32_t max_inner,
                              int32_t max_imfs, double* imfs, int32_t* l_out, int32_t* N_out, int32_t* k_out,
-                             double* margins, int par, int stop) {
+                             double* margins, int par, int stop, int mask_rule) {
   double* r = (double*)malloc(sizeof(double) * (size_t)n);
   memcpy(r, s, sizeof(double) * (size_t)n);
   memset(imfs, 0, sizeof(double) * (size_t)n * (size_t)(max_imfs + 1));
@@ -281,7 +320,16 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
     if (k_out) k_out[M] = (int32_t)k;
     if (margins) margins[2 * M] = em;
     if (k < 2) break; /* trend: fewer than 2 extrema */
-    int64_t L = oracle_filter_half_length(xi, n, k, window);
+    int64_t L;
+    if (mask_rule) {  /* spectral-peak rule (A20): L from k = 2 f* */
+      double pm;
+      const int64_t fs = oracle_spectral_peak(r, n, &pm);
+      if (margins && pm < margins[2 * M]) margins[2 * M] = pm;
+      if (fs == 0) break;
+      L = oracle_filter_half_length(xi, n, 2 * fs, window);
+    } else {
+      L = oracle_filter_half_length(xi, n, k, window);
+    }
     double sd[4];
     double* imf = imfs + (size_t)M * (size_t)n;
     int32_t N = stop ? oracle_inner_n0(r, n, L, delta, max_inner, imf, sd, par)
@@ -316,7 +364,7 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
  * stencil when batch == 1).  Non-finite input -> count = -1, outputs zeroed. */
 void oracle_decompose_batch(const double* s, int64_t batch, int64_t n, int window, double xi, double delta,
                             int32_t max_inner, int32_t max_imfs, double* imfs, int32_t* counts, int32_t* l_out,
-                            int32_t* N_out, int32_t* k_out, double* margins, int stop) {
+                            int32_t* N_out, int32_t* k_out, double* margins, int stop, int mask_rule) {
   int par_inner = (batch == 1);
 #pragma omp parallel for schedule(dynamic, 1) if (batch > 1)
   for (int64_t b = 0; b < batch; ++b) {
@@ -336,7 +384,7 @@ void oracle_decompose_batch(const double* s, int64_t batch, int64_t n, int windo
       continue;
     }
     counts[b] = oracle_decompose_one(sb, n, window, xi, delta, max_inner, max_imfs, ib, lb, nb, kb, mb, par_inner,
-                                     stop);
+                                     stop, mask_rule);
   }
 }
 

@@ -480,3 +480,50 @@ def test_gamma_to_zero_is_the_plain_method():
     b = df.decompose(s, gamma=1e-300)
     assert a["N"] == b["N"] and a["l"] == b["l"]
     assert np.abs(a["imfs"] - b["imfs"]).max() == 0.0
+
+
+# ------------------------------------------------------------------ NEXT row: spectral-peak filter length
+def test_spectral_peak_spec_examples():
+    """a tone of 8 periods (n=256) -> peak bin 8 -> l = 32 at nu = 1; tones at bins 4 and 32
+    of equal amplitude -> bin 32 -> l = 8; a constant has no peak (flat spectrum).  Our l = 2L with L from
+    the extrema rule at k = 2 f* (reading A20) reproduces SPEC's l on both."""
+    n = 256
+    x = np.arange(n) / n
+    tone = np.sin(2 * np.pi * 8 * x + 0.3)
+    two = np.sin(2 * np.pi * 4 * x) + np.sin(2 * np.pi * 32 * x)
+    for s, f_expect, l_expect in ((tone, 8, 32), (two, 32, 8)):
+        f, _ = oracle.spectral_peak(s)
+        assert f == f_expect
+        assert 2 * oracle.filter_half_length(1.0, n, 2 * f) == l_expect
+        assert df.spectral_peak(np.fft.rfft(s))[0] == f_expect
+    # no AC content at all -> no peak (a constant never reaches the rule: it has no extrema, PAPER.md:405)
+    assert oracle.spectral_peak(np.zeros(n))[0] == 0
+
+
+def test_spectral_peak_definition_brute_force():
+    """The O(n^2) oracle = an independent numpy scan of the definition (rfft powers), random spectra."""
+    rng = np.random.default_rng(11)
+    for t in range(60):
+        n = int(rng.choice([64, 96, 128, 250]))
+        s = rng.standard_normal(n) * rng.uniform(0, 1, n) ** 3 + np.sin(2 * np.pi * rng.integers(1, n // 2) * np.arange(n) / n)
+        p = np.abs(np.fft.rfft(s)) ** 2
+        NC = n // 2
+        thr = 1e-4 * p[1:].max()
+        peaks = [f for f in range(1, NC + 1) if p[f] >= thr and (f == 1 or p[f] > p[f - 1]) and (f == NC or p[f] >= p[f + 1])]
+        f, margin = oracle.spectral_peak(s)
+        if margin > 1e-9:
+            assert f == (max(peaks) if peaks else 0)
+
+
+def test_spectral_rule_td_equals_direct_form():
+    s = np.stack([signals.tones_signal(1024, 61, i, sigma=0.001) for i in range(3)])
+    a = oracle.decompose(s, mask=oracle.MASK_SPECTRAL)
+    b = df.decompose_batch(s, mask=df.MASK_SPECTRAL)
+    np.testing.assert_array_equal(a["count"], b["count"])
+    np.testing.assert_array_equal(a["l"], b["l"])
+    np.testing.assert_array_equal(a["N"], b["N"])
+    assert np.abs(a["imfs"] - b["imfs"]).max() <= 1e-11
+    # l follows each signal's highest tone: 2 floor(xi n / (2 f*)) at the first IMF
+    for b in range(3):
+        f, _ = oracle.spectral_peak(s[b])
+        assert a["l"][b][0] == 2 * oracle.filter_half_length(1.6, 1024, 2 * f)
