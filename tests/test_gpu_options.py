@@ -96,3 +96,40 @@ def test_options_validation():
         with pytest.raises(fif.FifError):
             plan.set_options(stop, gamma)
     plan.close()
+
+
+@pytest.mark.parametrize("name,regime,n", REGIMES)
+def test_spectral_peak_rule_vs_td_oracle(name, regime, n):
+    """Filter length from the highest significant spectral peak (reading A20)."""
+    s = np.stack([signals.tones_signal(n, 53, i, sigma=0.001) for i in range(4)])
+    s[3] = signals.tones_signal(n, 53, 3)  # sigma = 0.05: noise bins above 1% -> small L, many IMFs
+    plan = fif.Plan(n, 4, "f64", regime=regime).set_mask_rule(fif.MASK_SPECTRAL)
+    x = torch.from_numpy(s).cuda()
+    out = plan.alloc_outputs()
+    plan.decompose(x, *out)
+    torch.cuda.synchronize()
+    gpu = [t.cpu().numpy() for t in out]
+    plan.close()
+    ref = oracle.decompose(s, mask=oracle.MASK_SPECTRAL)
+    for b in range(4):
+        assert_parity(s[b], gpu, ref, b, b)
+
+
+def test_spectral_peak_rule_fp32_and_dist_unsupported():
+    n = 1 << 14
+    s32 = np.stack([signals.cfg4_signal(n, i) for i in range(2)])
+    plan = fif.Plan(n, 2, "f32").set_mask_rule(fif.MASK_SPECTRAL)
+    x = torch.from_numpy(s32).cuda()
+    out = plan.alloc_outputs()
+    plan.decompose(x, *out)
+    torch.cuda.synchronize()
+    gpu = [t.cpu().numpy() for t in out]
+    plan.close()
+    s64 = s32.astype(np.float64)
+    ref = df.decompose_batch(s64, mask=df.MASK_SPECTRAL)
+    for b in range(2):
+        assert_parity(s64[b], gpu, ref, b, b, "f32")
+    dp = fif.Plan.dist(4096, 0, 2, emulated=True)
+    with pytest.raises(fif.FifError):
+        dp.set_mask_rule(fif.MASK_SPECTRAL)
+    dp.close()
