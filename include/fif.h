@@ -92,6 +92,17 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
 typedef enum { FIF_STOP_SD = 0, FIF_STOP_N0 = 1 } fif_stop_rule;
 fif_status fif_plan_set_options(fif_plan_t plan, fif_stop_rule stop, double gamma);
 
+/* Filter-length rule (SURVEY.md §8f "next"):
+ *   FIF_MASK_EXTREMA (default): L = floor(xi n / k), k = number of extrema (readings A1-A4);
+ *   FIF_MASK_SPECTRAL: "the identification of its highest frequency peak ... proportional to the reciprocal
+ *   of this value": f* = the largest local maximum of |DFT(r)_f|^2, f = 1..n/2, with
+ *   |DFT(r)_f|^2 >= 1e-4 max (1% in magnitude), and L from the extrema rule at k = 2 f*
+ *   (reading A20); no such bin ends the decomposition (the extrema guard k >= 2 still applies).
+ * Batch plans only (FIF_ERR_UNSUPPORTED_N on a distributed plan: neighbouring bins live on other ranks);
+ * a streamed plan allocates (n/2+1) doubles per signal on first use (FIF_ERR_OOM). */
+typedef enum { FIF_MASK_EXTREMA = 0, FIF_MASK_SPECTRAL = 1 } fif_mask_rule;
+fif_status fif_plan_set_mask_rule(fif_plan_t plan, fif_mask_rule rule);
+
 /* Decompose the batch (device pointers, caller-owned, current device):
  *   d_signals    [batch][n] dtype, read only.
  *   d_imfs       [batch][max_imfs+1][n] dtype: IMF_0..IMF_{M-1} in slots 0..M-1, the

@@ -173,6 +173,17 @@ fif_status fif_plan_set_options(fif_plan_t p, fif_stop_rule stop, double gamma) 
   return FIF_OK;
 }
 
+fif_status fif_plan_set_mask_rule(fif_plan_t p, fif_mask_rule rule) {
+  if (!p || (rule != FIF_MASK_EXTREMA && rule != FIF_MASK_SPECTRAL)) return FIF_ERR_INVALID_ARG;
+  if (rule == FIF_MASK_SPECTRAL && p->regime == 2) return FIF_ERR_UNSUPPORTED_N;  // neighbours span ranks
+  if (rule == FIF_MASK_SPECTRAL && p->regime == 1 && !p->d_pnat) {
+    const int64_t B = p->batch > 0 ? p->batch : 1;
+    if (cudaMalloc(&p->d_pnat, sizeof(double) * (size_t)B * (size_t)(p->n / 2 + 1)) != cudaSuccess) return FIF_ERR_OOM;
+  }
+  p->mask = (int32_t)rule;
+  return FIF_OK;
+}
+
 fif_status fif_nccl_unique_id(void* out128) {
   if (!out128) return FIF_ERR_INVALID_ARG;
   return nccl_unique_id(out128);

@@ -35,6 +35,7 @@ struct fif_plan_s {
   int32_t max_inner = 200, max_imfs = 10;
   int32_t stop = 0;     // fif_stop_rule
   double gamma = 0.0;   // gamma-threshold (0: off)
+  int32_t mask = 0;     // fif_mask_rule
   int device = 0, num_sms = 0;
   int NC = 0;
   void* d_sin = nullptr;   // Real[NC+1]  sin(pi j/n)
@@ -54,6 +55,7 @@ struct fif_plan_s {
   void* d_Xn = nullptr;   // V[B] Nyquist bins
   void* d_ctl = nullptr;  // per-signal control arrays + partials
   void* d_utab = nullptr;   // int2[units] mirror-pair rows
+  void* d_pnat = nullptr;   // double[B][NC+1] natural-order powers (spectral-peak rule, allocated on demand)
   void* d_rbase = nullptr;  // int[rows] row bin bases
   void* d_rmir = nullptr;   // int[rows] mirror rows
   fifgpu::st::Ctl ctl{};

@@ -38,7 +38,7 @@ struct Inst {
   }
   static void decompose(const fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
                         int64_t batch, cudaStream_t s) {
-    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma};
+    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
     const int64_t cap = (int64_t)p->num_sms * p->occ;
     const int grid = (int)(batch < cap ? batch : cap);
     if (p->max_inner == kFastCap)
@@ -71,7 +71,7 @@ struct Inst {
   }
   static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
                          cudaStream_t s) {
-    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma};
+    Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
     const int grid = (int)(batch < 4096 ? batch : 4096);
     if (p->max_inner == kFastCap)
       fif_test_inner_kernel<Real, NC, kFastCap><<<grid, K::T, K::smem_bytes, s>>>(

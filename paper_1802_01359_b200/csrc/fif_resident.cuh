@@ -61,6 +61,7 @@ struct Params {
   int32_t stop;     // 0: relative SD rule (A5); 1: a-priori N0 with the absolute delta (A16-A18)
   double delta;     // delta (absolute, for stop = 1)
   double gamma;     // > 0: gamma-threshold variant (A19)
+  int32_t mask;     // 0: extrema filter-length rule (A1-A3); 1: spectral-peak rule (A20)
 };
 
 // ------------------------------------------------------------------ a5 alternative: a-priori N0
@@ -561,6 +562,64 @@ struct Resident {
   }
 
   // -------------------------------------------------------------- a3 filter length
+  // a3 alternative (reading A20): f* = the largest local maximum of p = |X|^2 over bins
+  // 1..NC with p >= 1e-4 max p (0 when none).  The free exchange buffer becomes a bin-indexed power
+  // array; two block max-reductions.
+  __device__ static int spectral_peak(const V (&X)[R], const V& Xn, const Smem& sm, V*& last, int& slot, int j) {
+    __syncthreads();  // nobody still reads the buffer that becomes the power array
+    V* fb = (last == sm.bufA) ? sm.bufB : sm.bufA;
+    double* pw = reinterpret_cast<double*>(fb);  // bins 0..NC-1 (NC doubles fit in NC complex slots)
+    double* red = sm.red + slot * 4 * NW;
+    slot ^= 1;
+    double mx = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int bin = bin_of(j, q);
+      const double pv = (double)X[q].x * (double)X[q].x + (double)X[q].y * (double)X[q].y;
+      pw[bin] = pv;
+      if (bin >= 1) mx = fmax(mx, pv);
+    }
+    if (j == 0) {  // the Nyquist power lives in the reduction scratch (red[2 NW])
+      const double pn = (double)Xn.x * (double)Xn.x + (double)Xn.y * (double)Xn.y;
+      red[2 * NW] = pn;
+      mx = fmax(mx, pn);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((j & 31) == 0) red[j >> 5] = mx;
+    __syncthreads();  // publishes pw, the Nyquist power and the warp maxima
+    double M = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmax(M, red[w]);
+    const double pnyq = red[2 * NW];
+    const double thr = 1e-4 * M;
+    auto pv_at = [&](int bin) { return bin == NC ? pnyq : pw[bin]; };
+    int best = 0;
+    auto test = [&](int bin) {
+      const double pv = pv_at(bin);
+      bool ok = M > 0.0 && pv >= thr;
+      if (ok && bin > 1) ok = pv > pv_at(bin - 1);
+      if (ok && bin < NC) ok = pv >= pv_at(bin + 1);
+      if (ok && bin > best) best = bin;
+    };
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (bin_of(j, q) >= 1) test(bin_of(j, q));
+    if (j == 0) test(NC);
+    double* red2 = sm.red + slot * 4 * NW;
+    slot ^= 1;
+    double bv = (double)best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bv = fmax(bv, __shfl_xor_sync(0xffffffffu, bv, o));
+    if ((j & 31) == 0) red2[j >> 5] = bv;
+    __syncthreads();
+    double B = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) B = fmax(B, red2[w]);
+    last = fb;
+    return (int)B;
+  }
+
   __device__ static int filter_half_length(const Params& p, int k) {
     const double t = __dmul_rn(p.xi, (double)n);   // fl(xi * n), never contracted (A8)
     const double u = __ddiv_rn(t, (double)k);      // fl(fl(xi n)/k)
@@ -958,7 +1017,14 @@ struct Resident {
     int M = 0;
     const Real invn = (Real)1 / (Real)n;
     while (M < p.max_imfs && k >= 2) {
-      const int L = filter_half_length(p, k);
+      int L;
+      if (p.mask == 1) {  // spectral-peak rule: L from k = 2 f* (A20)
+        const int fs = spectral_peak(X, Xn, sm, last, slot, j);
+        if (fs == 0) break;
+        L = filter_half_length(p, 2 * fs);
+      } else {
+        L = filter_half_length(p, k);
+      }
       const Real invL = (Real)1 / (Real)L;
 #if FIF_SPEC == 0
       V v[R], Dn{0, 0};

@@ -223,7 +223,7 @@ fif_status st_setup_t(fif_plan_s* p) {
   const int64_t B = p->batch > 0 ? p->batch : 1;
   if (wave > B) wave = B;
   p->st_wave = wave;
-  const size_t ni = (size_t)B * 11;
+  const size_t ni = (size_t)B * 11 + 2 * (size_t)B;  // + pmax (B doubles)
   const size_t segb = (size_t)B * g.nseg * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t grpb = (size_t)B * g.ngrp * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t redb = (size_t)B * g.nbch * 2 * st::kProbes * sizeof(double);
@@ -247,6 +247,7 @@ fif_status st_setup_t(fif_plan_s* p) {
   int32_t* ip = (int32_t*)take(ni * sizeof(int32_t));
   c.k = ip; c.L = ip + B; c.N = ip + 2 * B; c.M = ip + 3 * B; c.active = ip + 4 * B; c.search = ip + 5 * B;
   c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B); c.redo = ip + 10 * B;
+  c.pmax = (double*)take((size_t)B * sizeof(double));
   if (cudaMemset(p->d_ctl, 0, ctl_bytes) != cudaSuccess) return FIF_ERR_CUDA;
   // shared memory and grids
   for (int i = 0; i < g.L - 1; ++i) p->st_smem_col[i] = 3 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch;
@@ -322,6 +323,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     g.stop = p->stop;
     g.delta = p->delta;
     g.gamma = p->gamma;
+    g.mask = p->mask;
+    g.pnat = p->d_pnat ? (double*)p->d_pnat + (boff + b0) * (g.NC + 1) : nullptr;
     const st::Ctl c = ctl_at(p->ctl, g, boff + b0, sizeof(Real));
     const Real* sg = (const Real*)sig + b0 * g.n;
     Real* out = (Real*)imfs + b0 * g.sig_stride;
@@ -346,6 +349,12 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     for (int i = 1; i < Lv - 1; ++i)
       st::k_col<Real, -1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i], sg, out, X, tb, c);
     st::k_rows_fwd<Real><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
+    auto peaks = [&](const V* Xs, const V* Xns) {  // spectral-peak rule: L for the next IMF
+      if (!g.mask) return;
+      st::k_peak1<Real><<<grow, TB, 0, s>>>(g, Xs, Xns, c);
+      st::k_peak2<Real><<<grow, TB, 0, s>>>(g, c);
+    };
+    peaks(X, Xn);
     for (int m = 0; m < g.max_imfs; ++m) {
       V* Xi = (m & 1) ? Xalt : X;
       V* Xo = (m & 1) ? X : Xalt;
@@ -375,6 +384,7 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
         st::k_col<Real, 1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
       st::k_col<Real, 1, st::PASS_INV_LAST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
       st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 1, ln, it);
+      peaks(Xo, Xno);
     }
     st::k_final<Real><<<grid_for(g.batch, p->num_sms * 4), TB, 0, s>>>(g, out, c, cnt + b0, ln, it);
   }
@@ -388,8 +398,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
 int st_kernels_per_call(const fif_plan_s* p) {
   const int L = p->geo.L;
   const int64_t waves = p->batch > 0 ? (p->batch + p->st_wave - 1) / p->st_wave : 0;
-  const int per_imf = p->stop == 0 ? (p->st_rounds + L + 2) : (L + 2);
-  return (int)(waves * (2 + (L - 1) + 1 + p->max_imfs * per_imf + 1));
+  const int per_imf = (p->stop == 0 ? (p->st_rounds + L + 2) : (L + 2)) + (p->mask ? 2 : 0);
+  return (int)(waves * (2 + (L - 1) + 1 + (p->mask ? 2 : 0) + p->max_imfs * per_imf + 1));
 }
 
 fif_status st_setup(fif_plan_s* p) { return p->dtype == FIF_F64 ? st_setup_t<double>(p) : st_setup_t<float>(p); }
@@ -408,6 +418,7 @@ void st_free(fif_plan_s* p) {
   cudaFree(p->d_Xn);
   cudaFree(p->d_ctl);
   cudaFree(p->d_utab);
+  cudaFree(p->d_pnat);
   cudaFree(p->d_rbase);
   cudaFree(p->d_rmir);
   for (int i = 0; i < 2; ++i)

@@ -104,6 +104,8 @@ struct Geo {
   int64_t sig_stride;    // reals per signal in d_imfs = (max_imfs + 1) n
   int stop;              // 0: SD rule; 1: a-priori N0 (absolute delta)
   double delta, gamma;   // delta (absolute, stop = 1); gamma-threshold (0: off)
+  int mask;              // 0: extrema filter-length rule; 1: spectral-peak rule (A20)
+  double* pnat;          // [B][NC+1] |X_k|^2 in natural bin order (mask = 1 only)
   const int2* utab;      // [units] rows (ra, rb) of the mirror-pair unit u (bases u and P - u)
   const int* rbase;      // [P] bin base of each row
   const int* rmir;       // [P] row holding the mirror bins of each row
@@ -131,6 +133,7 @@ struct Ctl {
   int32_t* hi;
   int32_t* bad;     // non-finite input seen
   int32_t* redo;    // 1: the speculative N = cap damping of this IMF is void (SD(cap) <= delta)
+  double* pmax;     // [B] max_{k >= 1} |X_k|^2 (spectral-peak rule)
   uint32_t* cnt;    // last-CTA counters
   uint32_t* segi;   // [B][nseg] packed extrema monoid of a segment's internal differences
   void* segv;       // [B][nseg][2] Real: first and last sample of the segment
@@ -789,7 +792,7 @@ __global__ void __launch_bounds__(kThreads) k_fold(const __grid_constant__ Geo g
           c.k[b] = k.c;
           if (k.c < 2 || M >= g.max_imfs) c.active[b] = 0;
           else {
-            c.L[b] = filter_half_length(g, k.c);
+            if (!g.mask) c.L[b] = filter_half_length(g, k.c);  // (mask = 1: k_peak2 sets L)
             c.search[b] = 0;
           }
         }
@@ -1267,6 +1270,112 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
           }
         }
       }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ a3 alternative: spectral-peak rule
+// (reading A20).  k_peak1: |X_k|^2 scattered to natural bin order (one CTA per row pair)
+// + the per-signal max over k >= 1; k_peak2: the largest local maximum >= 1e-4 max (neighbours are
+// contiguous now), folded by the last CTA of the signal into L = rule(k = 2 f*), or the signal stops
+// when there is none.
+template <typename Real>
+__global__ void __launch_bounds__(kThreads) k_peak1(const __grid_constant__ Geo g,
+                                                    const typename Cx<Real>::V* __restrict__ X,
+                                                    const typename Cx<Real>::V* __restrict__ Xn,
+                                                    const __grid_constant__ Ctl c) {
+  using V = typename Cx<Real>::V;
+  __shared__ double sm[kNW];
+  __shared__ int last;
+  const int F = g.Frow;
+  const uint32_t units = (uint32_t)g.units;
+  for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.units); t += gridDim.x) {
+    const uint32_t b = t / units, u = t - b * units;
+    if (!c.active[b]) continue;
+    int64_t ra, rb, bA;
+    int two;
+    pair_of<Real>(g, u, ra, rb, bA, two);
+    const V* Xb = X + b * g.NC;
+    double* pn = g.pnat + b * (g.NC + 1);
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      int tm;
+      if (!mirror_t(g, bA, two, F, i, tm)) continue;
+      const int64_t k = bA + g.P * i;
+      const V xk = Xb[ra * F + i];
+      const V xm = k == 0 ? Xn[b] : Xb[(two ? rb : ra) * F + tm];
+      const double pk = (double)xk.x * (double)xk.x + (double)xk.y * (double)xk.y;
+      const double pm = (double)xm.x * (double)xm.x + (double)xm.y * (double)xm.y;
+      pn[k] = pk;
+      pn[g.NC - k] = pm;  // k = 0: the Nyquist bin NC
+      if (k >= 1) mx = fmax(mx, pk);
+      mx = fmax(mx, pm);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      for (int w = 0; w < kNW; ++w) v = fmax(v, sm[w]);
+      c.red[((int64_t)b * g.nbch + u) * (2 * kProbes)] = v;
+      __threadfence();
+      last = atomicAdd(c.cnt + b, 1u) == (uint32_t)(g.units - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      double v = 0.0;
+      for (int64_t q = 0; q < g.units; ++q) v = fmax(v, __ldcg(c.red + ((int64_t)b * g.nbch + q) * (2 * kProbes)));
+      c.pmax[b] = v;
+      c.cnt[b] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kThreads) k_peak2(const __grid_constant__ Geo g, const __grid_constant__ Ctl c) {
+  __shared__ double sm[kNW];
+  __shared__ int last;
+  const uint32_t units = (uint32_t)g.units;
+  const int64_t chunk = (g.NC + g.units - 1) / g.units;  // bins 1..NC in `units` chunks
+  for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.units); t += gridDim.x) {
+    const uint32_t b = t / units, u = t - b * units;
+    if (!c.active[b]) continue;
+    const double* pn = g.pnat + b * (g.NC + 1);
+    const double M = c.pmax[b], thr = 1e-4 * M;
+    const int64_t k0 = 1 + (int64_t)u * chunk, k1 = min(k0 + chunk, g.NC + 1);
+    int64_t best = 0;
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      const double pv = pn[k];
+      bool ok = M > 0.0 && pv >= thr;
+      if (ok && k > 1) ok = pv > pn[k - 1];
+      if (ok && k < g.NC) ok = pv >= pn[k + 1];
+      if (ok) best = k;
+    }
+    double bv = (double)best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bv = fmax(bv, __shfl_xor_sync(0xffffffffu, bv, o));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = bv;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      for (int w = 0; w < kNW; ++w) v = fmax(v, sm[w]);
+      c.red[((int64_t)b * g.nbch + u) * (2 * kProbes)] = v;
+      __threadfence();
+      last = atomicAdd(c.cnt + b, 1u) == (uint32_t)(g.units - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      double v = 0.0;
+      for (int64_t q = 0; q < g.units; ++q) v = fmax(v, __ldcg(c.red + ((int64_t)b * g.nbch + q) * (2 * kProbes)));
+      c.cnt[b] = 0;
+      const int fs = (int)v;
+      if (fs == 0) c.active[b] = 0;  // no significant peak: the signal stops
+      else c.L[b] = filter_half_length(g, 2 * fs);
     }
     __syncthreads();
   }

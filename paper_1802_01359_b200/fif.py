@@ -23,8 +23,9 @@ REGIME_AUTO, REGIME_RESIDENT, REGIME_STREAMED = 0, 1, 2
 SYMBOLS = ["fif_plan_create", "fif_plan_create_ex", "fif_decompose", "fif_decompose_host", "fif_destroy", "fif_status_string",
            "fif_plan_kernels_per_call", "fif_plan_regime", "fif_plan_launch_config", "fif_test_rfft",
            "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner", "fif_nccl_unique_id",
-           "fif_plan_create_dist", "fif_plan_create_dist_emulated", "fif_plan_set_options"]
+           "fif_plan_create_dist", "fif_plan_create_dist_emulated", "fif_plan_set_options", "fif_plan_set_mask_rule"]
 STOP_SD, STOP_N0 = 0, 1
+MASK_EXTREMA, MASK_SPECTRAL = 0, 1
 
 
 class FifError(RuntimeError):
@@ -65,6 +66,7 @@ def lib():
         L.fif_test_inner.argtypes = [vp, i64, i32, vp, vp, vp, vp]
         L.fif_nccl_unique_id.argtypes = [vp]
         L.fif_plan_set_options.argtypes = [vp, ctypes.c_int, d]
+        L.fif_plan_set_mask_rule.argtypes = [vp, ctypes.c_int]
         L.fif_plan_create_dist.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32, i32, vp,
                                            i32, i32]
         L.fif_plan_create_dist_emulated.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32,
@@ -130,6 +132,11 @@ class Plan:
     def set_options(self, stop=STOP_SD, gamma=0.0):
         """fif_plan_set_options: stopping rule (STOP_SD / STOP_N0) and gamma-threshold (0 = off)."""
         _check(lib().fif_plan_set_options(self._h, int(stop), float(gamma)), "fif_plan_set_options")
+        return self
+
+    def set_mask_rule(self, rule=MASK_EXTREMA):
+        """fif_plan_set_mask_rule: filter length from the extrema count or the highest spectral peak."""
+        _check(lib().fif_plan_set_mask_rule(self._h, int(rule)), "fif_plan_set_mask_rule")
         return self
 
     def decompose(self, signals, imfs, count, lens, iters, stream=None):
