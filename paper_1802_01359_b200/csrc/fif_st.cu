@@ -223,7 +223,7 @@ fif_status st_setup_t(fif_plan_s* p) {
   const int64_t B = p->batch > 0 ? p->batch : 1;
   if (wave > B) wave = B;
   p->st_wave = wave;
-  const size_t ni = (size_t)B * 11 + 2 * (size_t)B;  // + pmax (B doubles)
+  const size_t ni = (size_t)B * 13 + 2 * (size_t)B;  // + slist, scnt, pmax (B doubles)
   const size_t segb = (size_t)B * g.nseg * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t grpb = (size_t)B * g.ngrp * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t redb = (size_t)B * g.nbch * 2 * st::kProbes * sizeof(double);
@@ -247,6 +247,7 @@ fif_status st_setup_t(fif_plan_s* p) {
   int32_t* ip = (int32_t*)take(ni * sizeof(int32_t));
   c.k = ip; c.L = ip + B; c.N = ip + 2 * B; c.M = ip + 3 * B; c.active = ip + 4 * B; c.search = ip + 5 * B;
   c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B); c.redo = ip + 10 * B;
+  c.slist = ip + 11 * B; c.scnt = ip + 12 * B;
   c.pmax = (double*)take((size_t)B * sizeof(double));
   if (cudaMemset(p->d_ctl, 0, ctl_bytes) != cudaSuccess) return FIF_ERR_CUDA;
   // shared memory and grids
@@ -289,7 +290,7 @@ fif_status st_setup_t(fif_plan_s* p) {
 st::Ctl ctl_at(const st::Ctl& c, const st::Geo& g, int64_t b0, size_t rsz) {
   st::Ctl r = c;
   r.k += b0; r.L += b0; r.N += b0; r.M += b0; r.active += b0; r.search += b0; r.lo += b0; r.hi += b0;
-  r.bad += b0; r.cnt += b0;
+  r.bad += b0; r.cnt += b0; r.redo += b0; r.pmax += b0; r.slist += b0; r.scnt += b0;
   r.segi += b0 * g.nseg;
   r.segv = (char*)c.segv + b0 * g.nseg * 2 * rsz;
   r.gi += b0 * g.ngrp;
@@ -360,6 +361,10 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
       V* Xo = (m & 1) ? X : Xalt;
       V* Xni = (m & 1) ? Xnalt : Xn;
       V* Xno = (m & 1) ? Xn : Xnalt;
+      // the K-ary rounds and the redo touch only the few signals whose SD(cap) <= delta: one CTA per
+      // (signal, unit) so that the others cost a flag load and an exit, not a serial skip loop
+      const int gall = (int)(g.batch * g.units < (1LL << 30) ? g.batch * g.units : (1LL << 30));
+      (void)gall;
       auto rows = [&](auto spec, auto cap, int redo_only) {
         st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value>
             <<<grow, TB, p->st_smem_rows, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);

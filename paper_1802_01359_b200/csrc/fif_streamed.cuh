@@ -134,6 +134,8 @@ struct Ctl {
   int32_t* bad;     // non-finite input seen
   int32_t* redo;    // 1: the speculative N = cap damping of this IMF is void (SD(cap) <= delta)
   double* pmax;     // [B] max_{k >= 1} |X_k|^2 (spectral-peak rule)
+  int32_t* slist;   // [B] signals (wave-local) whose SD(cap) <= delta this IMF (K-ary search + redo)
+  int32_t* scnt;    // [1 per wave] length of slist
   uint32_t* cnt;    // last-CTA counters
   uint32_t* segi;   // [B][nseg] packed extrema monoid of a segment's internal differences
   void* segv;       // [B][nseg][2] Real: first and last sample of the segment
@@ -759,6 +761,7 @@ __global__ void __launch_bounds__(kThreads) k_fold(const __grid_constant__ Geo g
   __shared__ int last;
   const Real* segv = reinterpret_cast<const Real*>(c.segv);
   Real* gv = reinterpret_cast<Real*>(c.gv);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *c.scnt = 0;  // the next IMF's search list starts empty
   for (int64_t t = blockIdx.x; t < g.batch * g.ngrp; t += gridDim.x) {
     const int64_t b = t / g.ngrp, j = t - b * g.ngrp;
     if (!c.active[b]) continue;
@@ -917,8 +920,12 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
   const int F = lv.F;
   const double invn = 1.0 / (double)g.n;
   const uint32_t units = (uint32_t)g.units;
-  for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.units); t += gridDim.x) {
-    const uint32_t b = t / units, u = t - b * units;
+  // redo launch: only the listed signals (SD(cap) <= delta)
+  const uint32_t ntile = (!SPEC && redo_only) ? (uint32_t)(*c.scnt) * units : (uint32_t)(g.batch * g.units);
+  for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    uint32_t b = t / units;
+    const uint32_t u = t - b * units;
+    if (!SPEC && redo_only) b = (uint32_t)c.slist[b];
     if (!c.active[b] || (!SPEC && redo_only && !c.redo[b])) continue;
     int64_t ra, rb, bA;
     int two;
@@ -1075,6 +1082,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
             c.hi[b] = g.max_inner;
             c.search[b] = 1;
             c.redo[b] = 1;
+            c.slist[atomicAdd(c.scnt, 1)] = (int32_t)b;
           }
         }
       }
@@ -1101,9 +1109,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
   const int F = g.Frow;
   const double invn = 1.0 / (double)g.n;
   const uint32_t nbch = (uint32_t)g.nbch;
-  for (uint32_t t = blockIdx.x; t < (uint32_t)(g.batch * g.nbch); t += gridDim.x) {
-    const uint32_t b = t / nbch;
+  // K-ary rounds (mode 1) visit only the listed signals
+  const uint32_t ntile = MODE == 1 ? (uint32_t)(*c.scnt) * nbch : (uint32_t)(g.batch * g.nbch);
+  for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    uint32_t b = t / nbch;
     const uint32_t ch = t - b * nbch;
+    if (MODE == 1) b = (uint32_t)c.slist[b];
     if (!c.active[b] || (mode == 1 && !c.search[b])) continue;
     const int L = c.L[b];
     int N0, step;

@@ -151,3 +151,20 @@ def test_streamed_long_single_signal_3level():
     ref = df.decompose_batch(s)
     assert_parity(s[0], gpu, ref, 0, 0)
     assert np.abs(gpu[0][0].sum(axis=0) - s[0]).max() <= 1e-11 * np.abs(s).max()
+
+
+def test_streamed_many_waves_two_streams(monkeypatch):
+    """L2 waves (FIF_WAVE_MB forces ~2 signals per wave, alternating between the plan's two streams) give
+    the same decomposition as the resident regime, including signals that need the K-ary search."""
+    monkeypatch.setenv("FIF_WAVE_MB", "0.2")
+    s = signals.make_batch("cfg1", batch=40, start=900)
+    a = run_gpu(s, regime=fif.REGIME_RESIDENT)
+    b = run_gpu(s, regime=ST)
+    assert (a[3] < 200).any()  # some IMFs stop below the cap (search + redo path)
+    np.testing.assert_array_equal(a[1], b[1])
+    np.testing.assert_array_equal(a[2], b[2])
+    np.testing.assert_array_equal(a[3], b[3])
+    for i in range(40):
+        for m in range(a[1][i] + 1):
+            x, y = a[0][i, m], b[0][i, m]
+            assert np.linalg.norm(x - y) <= 1e-11 * max(np.linalg.norm(x), 1e-5 * np.linalg.norm(s[i]))
