@@ -53,7 +53,10 @@ typedef enum {
 typedef enum {
   FIF_REGIME_AUTO = 0,      /* resident when n fits on chip, streamed otherwise */
   FIF_REGIME_RESIDENT = 1,  /* one CTA per signal, r and r_hat on chip for all IMFs (power-of-two 512 <= n <= 8192) */
-  FIF_REGIME_STREAMED = 2   /* spectrum / work buffers in HBM, four-step FFT, one kernel sequence per IMF */
+  FIF_REGIME_STREAMED = 2,  /* spectrum / work buffers in HBM, multi-level FFT, a short kernel sequence per IMF */
+  FIF_REGIME_ITERATIVE = 3  /* the baseline the paper compares FIF against: Algorithm 2 run
+                               literally, N circular convolutions s <- s - w (*) s per IMF (fp64, n <= 4096);
+                               same decisions and readings; never chosen by AUTO */
 } fif_regime;
 
 /* Create a plan for `batch` independent signals of length n.

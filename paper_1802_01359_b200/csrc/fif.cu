@@ -117,7 +117,8 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
   if (n < 9 || batch < 0 || !(xi > 0.0) || !isfinite(xi) || !(delta > 0.0) || !isfinite(delta) || max_inner < 1 ||
       max_imfs < 1 || (dtype != FIF_F64 && dtype != FIF_F32) ||
       (window != FIF_WINDOW_TRI_SQ && window != FIF_WINDOW_TRI_SQ_WIDE) ||
-      (regime != FIF_REGIME_AUTO && regime != FIF_REGIME_RESIDENT && regime != FIF_REGIME_STREAMED))
+      (regime != FIF_REGIME_AUTO && regime != FIF_REGIME_RESIDENT && regime != FIF_REGIME_STREAMED &&
+       regime != FIF_REGIME_ITERATIVE))
     return FIF_ERR_INVALID_ARG;
   if (n % 2 != 0) return FIF_ERR_UNSUPPORTED_N;
   const int64_t NC = n / 2;
@@ -128,6 +129,9 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
     reg = 0;
   } else if (regime == FIF_REGIME_STREAMED) {
     reg = 1;
+  } else if (regime == FIF_REGIME_ITERATIVE) {
+    if (dtype != FIF_F64 || n > 4096) return FIF_ERR_UNSUPPORTED_N;
+    reg = 3;
   } else {
     reg = resident_ok ? 0 : 1;
   }
@@ -142,6 +146,12 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
       cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
     free_plan(p);
     return FIF_ERR_CUDA;
+  }
+  if (reg == 3) {
+    fif_status st = it_setup(p);
+    if (st != FIF_OK) { free_plan(p); return st; }
+    *out = p;
+    return FIF_OK;
   }
   if (reg == 1) {
     fif_status st = st_setup(p);
@@ -168,6 +178,7 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
 fif_status fif_plan_set_options(fif_plan_t p, fif_stop_rule stop, double gamma) {
   if (!p || (stop != FIF_STOP_SD && stop != FIF_STOP_N0) || !(gamma >= 0.0) || !(gamma < 1.0))
     return FIF_ERR_INVALID_ARG;
+  if (p->regime == 3 && (stop != FIF_STOP_SD || gamma != 0.0)) return FIF_ERR_UNSUPPORTED_N;  // plain Alg. 2 only
   p->stop = (int32_t)stop;
   p->gamma = gamma;
   return FIF_OK;
@@ -175,7 +186,7 @@ fif_status fif_plan_set_options(fif_plan_t p, fif_stop_rule stop, double gamma) 
 
 fif_status fif_plan_set_mask_rule(fif_plan_t p, fif_mask_rule rule) {
   if (!p || (rule != FIF_MASK_EXTREMA && rule != FIF_MASK_SPECTRAL)) return FIF_ERR_INVALID_ARG;
-  if (rule == FIF_MASK_SPECTRAL && p->regime == 2) return FIF_ERR_UNSUPPORTED_N;  // neighbours span ranks
+  if (rule == FIF_MASK_SPECTRAL && (p->regime == 2 || p->regime == 3)) return FIF_ERR_UNSUPPORTED_N;
   if (rule == FIF_MASK_SPECTRAL && p->regime == 1 && !p->d_pnat) {
     const int64_t B = p->batch > 0 ? p->batch : 1;
     if (cudaMalloc(&p->d_pnat, sizeof(double) * (size_t)B * (size_t)(p->n / 2 + 1)) != cudaSuccess) return FIF_ERR_OOM;
@@ -241,6 +252,10 @@ fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int3
     st_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, 0, s);
     return launch_status();
   }
+  if (p->regime == 3) {
+    it_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
+    return launch_status();
+  }
   res_ops(p->dtype, p->NC)->decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
   return launch_status();
 }
@@ -288,6 +303,8 @@ fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs,
     if (p->regime == 1) {
       // disjoint plan work buffers per chunk (chunks run concurrently on the staging streams)
       st_decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, b0, S.stream);
+    } else if (p->regime == 3) {
+      it_decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
     } else {
       res_ops(p->dtype, p->NC)->decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
     }
@@ -324,6 +341,7 @@ int32_t fif_plan_kernels_per_call(fif_plan_t p) {
 
 const char* fif_plan_regime(fif_plan_t p) {
   if (!p) return "none";
+  if (p->regime == 3) return "iterative";
   return p->regime == 2 ? "distributed" : (p->regime == 1 ? "streamed" : "resident");
 }
 

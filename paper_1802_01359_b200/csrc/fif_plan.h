@@ -100,6 +100,11 @@ void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int3
 int st_kernels_per_call(const fif_plan_s* p);
 void st_free(fif_plan_s* p);
 
+// iterative regime (fif_iterative.cu): Algorithm 2 literally (the IF baseline of PAPER.md:693)
+fif_status it_setup(fif_plan_s* p);
+void it_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its, int64_t batch,
+                  cudaStream_t s);
+
 // distributed regime (fif_dist.cu): one signal time-block sharded over nranks GPUs
 fif_status dist_create(fif_plan_s* p, const void* nccl_uid, int rank, int nranks, int emulated);
 fif_status dist_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
