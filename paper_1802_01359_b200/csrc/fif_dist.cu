@@ -930,7 +930,10 @@ fif_status dist_create(fif_plan_s* p, const void* uid, int rank, int nranks, int
   D->P = nranks;
   D->rank = emulated ? 0 : rank;
   D->emulated = emulated != 0;
-  if (!D->emulated && nranks > 1) {
+  // FIF_DIST_FORCE_NCCL: a one-rank plan still goes through NCCL (self all-gathers / self send-recv),
+  // which exercises the NCCL path on a single GPU (tests)
+  const bool force = getenv("FIF_DIST_FORCE_NCCL") != nullptr;
+  if (!D->emulated && (nranks > 1 || force)) {
     if (!nccl().load()) return FIF_ERR_NCCL;
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));

@@ -112,3 +112,25 @@ def test_dist_cfg3_recipe_2p22_vs_direct_form():
     gpu = run_dist(s, 8)
     ref = df.decompose_batch(s[None])
     assert_parity(s, gpu, ref, 0, 0)
+
+
+def test_dist_nccl_one_rank(monkeypatch):
+    """The NCCL path itself (unique id, ncclCommInitRank, ncclAllGather, grouped ncclSend/ncclRecv -- to self)
+    on the one GPU of this box: a one-rank plan forced through NCCL equals the single-GPU streamed plan."""
+    monkeypatch.setenv("FIF_DIST_FORCE_NCCL", "1")
+    n = 1 << 14
+    s = signals.cfg3_signal(2, n=n)
+    uid = fif.nccl_unique_id()
+    assert len(uid) == 128
+    plan = fif.Plan.dist(n, 0, 1, uid=uid)
+    x = torch.from_numpy(s[None]).cuda()
+    out = plan.alloc_outputs()
+    plan.decompose(x, *out)
+    torch.cuda.synchronize()
+    b = [t.cpu().numpy() for t in out]
+    plan.close()
+    a = run_gpu(s[None], regime=fif.REGIME_STREAMED)
+    for i in (1, 2, 3):
+        np.testing.assert_array_equal(a[i], b[i])
+    for m in range(a[1][0] + 1):
+        assert np.linalg.norm(a[0][0, m] - b[0][0, m]) <= 1e-11 * max(np.linalg.norm(a[0][0, m]), 1e-5 * np.linalg.norm(s))
