@@ -1,0 +1,100 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (a plan over the whole
+batch on one GPU), where the oracle cannot run the whole decomposition:
+  * config 3 (one signal, n = 2^26, streamed regime): every decision re-derived by the oracle from the GPU's
+    own remainders -- the extrema count and the filter-length rule exactly (oracle.count_extrema /
+    filter_half_length), N from the SD rule evaluated by Parseval on the oracle side (numpy FFT + the
+    eigenvalues of the filter row, oracle/direct_form.py), the IMF spectrum against (1 - w_hat)^N times the
+    remainder spectrum at every bin, and the trend by telescoping;
+  * config 4 (fp32 sweep, 1 GiB per run): the full batch decomposed, sampled signals against the direct form.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from oracle import direct_form as df  # noqa: E402
+from paper_1802_01359_b200 import fif, signals  # noqa: E402
+from test_gpu_parity import assert_parity  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+
+    ge.build_native()
+    torch.cuda.set_device(0)
+
+
+def test_cfg3_full_size_every_decision():
+    n, delta, cap = 1 << 26, 1e-3, 200
+    s = signals.cfg3_signal(0)
+    plan = fif.Plan(n, 1, "f64", delta=delta)
+    assert plan.launch_config()["regime"] == "streamed"
+    x = torch.from_numpy(s[None]).cuda()
+    imfs, count, lens, iters = plan.alloc_outputs()
+    plan.decompose(x, imfs, count, lens, iters)
+    torch.cuda.synchronize()
+    M, lens, iters = int(count[0]), lens.cpu().numpy()[0], iters.cpu().numpy()[0]
+    assert 1 <= M <= 10
+    r = s.copy()
+    snorm = np.linalg.norm(s)
+    c = np.full(n // 2 + 1, 2.0)
+    c[0] = c[-1] = 1.0
+    for m in range(M):
+        # r here is s minus the GPU's IMFs in the GPU's own order, i.e. the GPU's remainder bit for bit;
+        # the smallest difference among 2^26 noisy samples is ~1e-10 max|s|, far above rounding
+        k, em = oracle.count_extrema(r)
+        assert em > 1e-14, "extremum decision at rounding level"
+        L = oracle.filter_half_length(1.6, n, k)
+        assert lens[m] == 2 * L, (m, lens[m], L)
+        N = int(iters[m])
+        R = np.fft.rfft(r)
+        lam = df.eigenvalues(n, L)
+        a2 = np.clip(1.0 - lam, 0.0, 1.0) ** 2
+        p = c * (R.real ** 2 + R.imag ** 2)
+
+        def sd(NN):
+            e = a2 ** (NN - 1)
+            return math.sqrt(float(np.dot(p * lam * lam, e)) / float(np.dot(p, e)))
+
+        sdN = sd(N)
+        assert sdN <= delta * (1 + 1e-9) or N == cap, (m, N, sdN)
+        if N > 1:
+            assert sd(N - 1) > delta * (1 - 1e-9), (m, N)
+        imf = imfs[0, m].cpu().numpy()
+        I = np.fft.rfft(imf)
+        D = np.clip(1.0 - lam, 0.0, 1.0) ** N * R
+        err = np.linalg.norm(I - D) / max(np.linalg.norm(D), 1e-5 * math.sqrt(n) * snorm)
+        assert err <= 1e-9, (m, err)
+        r = r - imf
+    trend = imfs[0, M].cpu().numpy()
+    assert np.abs(trend - r).max() <= 1e-10 * np.abs(s).max()
+    k, _ = oracle.count_extrema(r)
+    assert M == 10 or k < 2
+    plan.close()
+
+
+@pytest.mark.parametrize("n", [1 << 14, 1 << 17, 1 << 20, 3 << 14, 5 << 14])
+def test_cfg4_full_batch_sampled(n):
+    B = signals.cfg4_batch(n)
+    s32 = signals.make_batch("cfg4", n=n)
+    plan = fif.Plan(n, B, "f32")
+    x = torch.from_numpy(s32).cuda()
+    imfs, count, lens, iters = plan.alloc_outputs()
+    plan.decompose(x, imfs, count, lens, iters)
+    torch.cuda.synchronize()
+    idx = [0, B // 2, B - 1]
+    gpu = [imfs[idx].cpu().numpy(), count[idx].cpu().numpy(), lens[idx].cpu().numpy(), iters[idx].cpu().numpy()]
+    cnt = count.cpu().numpy()
+    assert ((cnt >= 0) & (cnt <= 10)).all()
+    plan.close()
+    s64 = s32[idx].astype(np.float64)
+    ref = df.decompose_batch(s64)
+    for i in range(len(idx)):
+        assert_parity(s64[i], gpu, ref, i, i, "f32")
