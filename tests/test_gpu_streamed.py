@@ -157,14 +157,34 @@ def test_streamed_many_waves_two_streams(monkeypatch):
     """L2 waves (FIF_WAVE_MB forces ~2 signals per wave, alternating between the plan's two streams) give
     the same decomposition as the resident regime, including signals that need the K-ary search."""
     monkeypatch.setenv("FIF_WAVE_MB", "0.2")
-    s = signals.make_batch("cfg1", batch=40, start=900)
+    s = signals.make_batch("cfg1", batch=41, start=900)  # ragged last wave
     a = run_gpu(s, regime=fif.REGIME_RESIDENT)
     b = run_gpu(s, regime=ST)
     assert (a[3] < 200).any()  # some IMFs stop below the cap (search + redo path)
     np.testing.assert_array_equal(a[1], b[1])
     np.testing.assert_array_equal(a[2], b[2])
     np.testing.assert_array_equal(a[3], b[3])
-    for i in range(40):
+    for i in range(41):
         for m in range(a[1][i] + 1):
             x, y = a[0][i, m], b[0][i, m]
             assert np.linalg.norm(x - y) <= 1e-11 * max(np.linalg.norm(x), 1e-5 * np.linalg.norm(s[i]))
+
+
+@pytest.mark.parametrize("n", [16, 24, 40, 96, 250])
+def test_streamed_tiny_lengths_vs_td_oracle(n):
+    """Smallest geometries (two levels of 2..5-point DFTs, self-paired rows only) against the literal oracle."""
+    rng = np.random.default_rng(n)
+    s = rng.standard_normal((5, n))
+    gpu = run_gpu(s, regime=ST)
+    ref = oracle.decompose(s)
+    for b in range(5):
+        assert_parity(s[b], gpu, ref, b, b)
+
+
+def test_streamed_empty_batch():
+    plan = fif.Plan(1 << 14, 0, "f64")
+    x = torch.empty((0, 1 << 14), dtype=torch.float64, device="cuda")
+    out = plan.alloc_outputs()
+    plan.decompose(x, *out)  # a no-op
+    torch.cuda.synchronize()
+    plan.close()
