@@ -251,7 +251,8 @@ fif_status st_setup_t(fif_plan_s* p) {
   c.pmax = (double*)take((size_t)B * sizeof(double));
   if (cudaMemset(p->d_ctl, 0, ctl_bytes) != cudaSuccess) return FIF_ERR_CUDA;
   // shared memory and grids
-  for (int i = 0; i < g.L - 1; ++i) p->st_smem_col[i] = 3 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch;
+  for (int i = 0; i < g.L - 1; ++i)  // three tile buffers + the level's twiddles
+    p->st_smem_col[i] = 3 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch + sizeof(V) * (size_t)g.lv[i].F;
   p->st_smem_rows = 2 * sizeof(V) * 2 * (size_t)g.lv[g.L - 1].pitch;
   size_t smax = p->st_smem_rows;
   for (int i = 0; i < g.L - 1; ++i) smax = smax > p->st_smem_col[i] ? smax : p->st_smem_col[i];
@@ -272,7 +273,11 @@ fif_status st_setup_t(fif_plan_s* p) {
     fprintf(stderr, "fif: streamed setup failed: %s\n", cudaGetErrorString(e));
     return FIF_ERR_CUDA;
   }
-  p->st_grid_col = occ_grid(p, st::k_col<Real, 1, st::PASS_INV_LAST>, smax);
+  {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, st::k_col<Real, 1, st::PASS_INV_LAST>, st::kColThreads, smax);
+    p->st_grid_col = p->num_sms * (occ > 0 ? occ : 1);
+  }
   p->st_grid_rows = occ_grid(p, st::k_rows_inv<Real, kFastCap, 1>, p->st_smem_rows);
   p->st_grid_probe = occ_grid(p, st::k_probe<Real, kFastCap, 1>, 0);
   p->st_grid = p->st_grid_rows;
@@ -345,10 +350,10 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     const int gsig = (int)((g.batch + TB - 1) / TB);
     auto col = [&](int i) { return grid_for(g.batch * g.lv[i].tiles, gcol); };
     st::k_init<<<gsig, TB, 0, s>>>(g, c);
-    st::k_col<Real, -1, st::PASS_FWD_FIRST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+    st::k_col<Real, -1, st::PASS_FWD_FIRST><<<col(0), st::kColThreads, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
     st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
     for (int i = 1; i < Lv - 1; ++i)
-      st::k_col<Real, -1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i], sg, out, X, tb, c);
+      st::k_col<Real, -1, st::PASS_MID><<<col(i), st::kColThreads, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i], sg, out, X, tb, c);
     st::k_rows_fwd<Real><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     auto peaks = [&](const V* Xs, const V* Xns) {  // spectral-peak rule: L for the next IMF
       if (!g.mask) return;
@@ -386,8 +391,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
         if (fast) rows(F0{}, FC{}, 0); else rows(F0{}, F0{}, 0);
       }
       for (int i = Lv - 2; i >= 1; --i)
-        st::k_col<Real, 1, st::PASS_MID><<<col(i), TB, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
-      st::k_col<Real, 1, st::PASS_INV_LAST><<<col(0), TB, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+        st::k_col<Real, 1, st::PASS_MID><<<col(i), st::kColThreads, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
+      st::k_col<Real, 1, st::PASS_INV_LAST><<<col(0), st::kColThreads, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
       st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 1, ln, it);
       peaks(Xo, Xno);
     }

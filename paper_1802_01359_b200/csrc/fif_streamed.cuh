@@ -42,6 +42,10 @@ constexpr int kMaxPass = 16;
 constexpr int kProbes = 15;  // K-ary search: probes per round
 constexpr int kThreads = 256;
 constexpr int kNW = kThreads / 32;
+#ifndef FIF_COL_THREADS
+#define FIF_COL_THREADS 256
+#endif
+constexpr int kColThreads = FIF_COL_THREADS;  // block size of the column passes
 #ifndef FIF_ST_MINB
 #define FIF_ST_MINB 3  // resident CTAs per SM the heavy streamed kernels are register-budgeted for
 #endif
@@ -249,7 +253,7 @@ __device__ void cta_pass_t(const V* src, V* dst, int Ns, int cols, int pitch, in
       const int kt = k * tstride;
 #pragma unroll
       for (int r = 1; r < P; ++r) {
-        V t = __ldg(tw + r * kt);
+        V t = tw[r * kt];  // (global or shared)
         if (DIR > 0) t.y = -t.y;
         x[r] = cmul(x[r], t);
       }
@@ -588,7 +592,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Persistent CTAs, software-pipelined: the next tile streams into a third shared buffer with
 // cp.async while the current one is transformed.
 template <typename Real, int DIR, int KIND>
-__global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv,
+__global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv,
                                                      const __grid_constant__ Level lvn, const Real* __restrict__ sig,
                                                      Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
                                                      const __grid_constant__ Tabs<Real> tb,
@@ -598,10 +602,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo
   const size_t bufsz = (size_t)lv.C * lv.pitch;
   V* S[3] = {reinterpret_cast<V*>(smem_raw), reinterpret_cast<V*>(smem_raw) + bufsz,
              reinterpret_cast<V*>(smem_raw) + 2 * bufsz};
+  // the level's Stockham twiddles e^{-2 pi i j/F} in shared memory (the FFT passes read 1 per point)
+  V* tws = reinterpret_cast<V*>(smem_raw) + 3 * bufsz;
+  for (int j = threadIdx.x; j < lv.F; j += blockDim.x) tws[j] = tb.tw[lv.twoff + j];
+  Level lvs = lv;
+  lvs.twoff = 0;
   const uint32_t spt = (uint32_t)(lv.S / lv.C), tiles = (uint32_t)lv.tiles;
   const uint32_t total = (uint32_t)(g.batch * lv.tiles);
   const int FC = lv.F * lv.C;
-  constexpr int U = TileCap<Real>::value / kThreads;
+  constexpr int U = TileCap<Real>::value / kColThreads;
   auto active = [&](uint32_t t) { return KIND == PASS_FWD_FIRST || c.active[t / tiles]; };
   auto next_tile = [&](uint32_t t) {
     for (; t < total; t += gridDim.x)
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo
   auto issue = [&](const TG& q, V* dst) {
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const int i = threadIdx.x + j * kThreads;
+      const int i = threadIdx.x + j * kColThreads;
       if (i < FC) {
         int f, cc;
         tile_fc(lv, i, f, cc);
@@ -662,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo
       bool finite = true;
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int i = threadIdx.x + j * kThreads;
+        const int i = threadIdx.x + j * kColThreads;
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
@@ -678,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo
     if (KIND == PASS_INV_LAST) {  // remainder loads in flight during the transform
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int i = threadIdx.x + j * kThreads;
+        const int i = threadIdx.x + j * kColThreads;
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
@@ -686,12 +695,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo
         }
       }
     }
-    V* out = cta_fft<DIR>(In, Sc, lv, lv.C, tb.tw);
+    V* out = cta_fft<DIR>(In, Sc, lvs, lv.C, tws);
     if (KIND == PASS_INV_LAST) {
       V* stage = out == In ? Sc : In;
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int i = threadIdx.x + j * kThreads;
+        const int i = threadIdx.x + j * kColThreads;
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
@@ -708,15 +717,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo
     } else {
       // forward: this level's twiddle e^{-2 pi i s k/(F S)}; inverse: the next coarser level's
       // e^{+2 pi i s' k'/(F' S')} with s' = f S + s, k' = a mod F'.  When C divides the block size a
-      // thread's column cc is fixed and its digit f advances by kThreads/C per element, so the
+      // thread's column cc is fixed and its digit f advances by kColThreads/C per element, so the
       // twiddles form a geometric sequence: two table products per thread, one multiply per element.
       const int64_t kn = DIR > 0 ? (int64_t)(cur.a % (uint32_t)lvn.F) : 0;
-      const bool geom = lv.cs >= 0 && lv.C <= kThreads;
+      const bool geom = lv.cs >= 0 && lv.C <= kColThreads;
       V w{(Real)1, (Real)0}, ws{(Real)1, (Real)0};
       if (geom) {
         int f0, c0;
         tile_fc(lv, threadIdx.x, f0, c0);
-        const int64_t df = kThreads >> lv.cs;
+        const int64_t df = kColThreads >> lv.cs;
         if (DIR < 0) {
           w = cconj(Er(tb, g.eb, lv.E2 * (cur.s0 + c0) * f0));
           ws = cconj(Er(tb, g.eb, lv.E2 * ((cur.s0 + c0) * df % ((int64_t)lv.F * lv.S))));
@@ -727,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_col(const __grid_constant__ Geo
       }
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int i = threadIdx.x + j * kThreads;
+        const int i = threadIdx.x + j * kColThreads;
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
