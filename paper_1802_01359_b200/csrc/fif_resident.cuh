@@ -1135,7 +1135,12 @@ struct Resident {
 
 // ------------------------------------------------------------------ kernels
 template <typename Real, int NC, int CAP>
-__global__ void __launch_bounds__(NC / kR, (NC / kR) <= 256 ? FIF_MINB : 1)
+#ifndef FIF_WARPS_TARGET
+#define FIF_WARPS_TARGET 16  // register budget: this many warps per SM (0: FIF_MINB CTAs per SM)
+#endif
+__global__ void __launch_bounds__(NC / kR, FIF_WARPS_TARGET > 0
+                                               ? ((FIF_WARPS_TARGET * 32) / (NC / kR) > 1 ? (FIF_WARPS_TARGET * 32) / (NC / kR) : 1)
+                                               : ((NC / kR) <= 256 ? FIF_MINB : 1))
 fif_resident_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32_t* __restrict__ count,
                     int32_t* __restrict__ lens, int32_t* __restrict__ iters, const Real* __restrict__ sintab,
                     const Real* __restrict__ isintab, const typename Cx<Real>::V* __restrict__ tw, Params p) {
