@@ -52,7 +52,8 @@ typedef enum {
 
 typedef enum {
   FIF_REGIME_AUTO = 0,      /* resident when n fits on chip, streamed otherwise */
-  FIF_REGIME_RESIDENT = 1,  /* one CTA per signal, r and r_hat on chip for all IMFs (power-of-two 512 <= n <= 8192) */
+  FIF_REGIME_RESIDENT = 1,  /* one CTA per signal, r and r_hat on chip for all IMFs (power-of-two 512 <= n <= 8192;
+                               fp32 also n = 16384) */
   FIF_REGIME_STREAMED = 2,  /* spectrum / work buffers in HBM, multi-level FFT, a short kernel sequence per IMF */
   FIF_REGIME_ITERATIVE = 3  /* the baseline the paper compares FIF against: Algorithm 2 run
                                literally, N circular convolutions s <- s - w (*) s per IMF (fp64, n <= 4096);
@@ -60,7 +61,7 @@ typedef enum {
 } fif_regime;
 
 /* Create a plan for `batch` independent signals of length n.
- *   n          : samples per signal, even.  Resident regime: powers of two 512 <= n <= 8192.
+ *   n          : samples per signal, even.  Resident regime: powers of two 512 <= n <= 8192 (fp32: <= 16384).
  *                Streamed regime: n/2 = N1 N2 with N1, N2 of the form 2^a 3^b 5^c, N2 <= 2048 (f64) /
  *                4096 (f32), N1 <= 1024 -- e.g. every 2^a 3^b 5^c up to n = 2^22 (f64) / 2^23 (f32).
  *                Other n -> FIF_ERR_UNSUPPORTED_N.

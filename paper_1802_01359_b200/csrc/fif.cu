@@ -122,7 +122,7 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
     return FIF_ERR_INVALID_ARG;
   if (n % 2 != 0) return FIF_ERR_UNSUPPORTED_N;
   const int64_t NC = n / 2;
-  const bool resident_ok = (NC & (NC - 1)) == 0 && NC >= 256 && NC <= 4096;
+  const bool resident_ok = (NC & (NC - 1)) == 0 && NC >= 256 && (NC <= 4096 || (NC == 8192 && dtype == FIF_F32));
   int reg;
   if (regime == FIF_REGIME_RESIDENT) {
     if (!resident_ok) return FIF_ERR_UNSUPPORTED_N;

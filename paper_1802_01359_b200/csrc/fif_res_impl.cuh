@@ -100,6 +100,9 @@ const ResOps* res_table(int NC) {
     case 1024: return res_entry<Real, 1024>();
     case 2048: return res_entry<Real, 2048>();
     case 4096: return res_entry<Real, 4096>();
+    case 8192:  // fp32 only: 1024 threads, 192 KB of shared memory (n = 16384, config 4)
+      if constexpr (sizeof(Real) == 4) return res_entry<Real, 8192>();
+      else return nullptr;
     default: return nullptr;
   }
 }

@@ -322,3 +322,33 @@ def test_host_path_matches_device_path():
     for a, b in zip(dev, outs):
         np.testing.assert_array_equal(a, b.numpy())
     plan.close()
+
+
+# ------------------------------------------------------------------------------------------ n = 16384 fp32 resident
+def test_resident_fp32_16384_hooks_and_decomposition():
+    """The largest resident kernel (fp32, n/2 = 8192: 1024 threads, 192 KB shared memory; config 4's
+    n = 2^14 point): FFT hooks vs numpy and the extrema hook vs the oracle, then whole decompositions vs
+    the direct form (fp64 oracle on the fp32-rounded input, reading A14)."""
+    n, B = 1 << 14, 9
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((B, n))
+    xg = torch.from_numpy(x).float().cuda()
+    plan = fif.Plan(n, B, "f32")
+    assert plan.launch_config()["regime"] == "resident"
+    X = torch.empty((B, n // 2 + 1, 2), dtype=torch.float32, device="cuda")
+    plan.test_rfft(xg, X)
+    ref = np.fft.rfft(xg.cpu().double().numpy(), axis=1)
+    got = X.cpu().double().numpy()
+    got = got[..., 0] + 1j * got[..., 1]
+    assert np.abs(got - ref).max() <= 2e-6 * np.abs(ref).max() * math.log2(n)
+    k = torch.empty(B, dtype=torch.int32, device="cuda")
+    plan.test_extrema(xg, k)
+    xr = xg.cpu().double().numpy()
+    assert [int(v) for v in k.cpu().numpy()] == [oracle.count_extrema(xr[b])[0] for b in range(B)]
+    plan.close()
+    s32 = np.stack([signals.cfg4_signal(n, i) for i in range(4)])
+    gpu = run_gpu(s32, "f32")
+    s64 = s32.astype(np.float64)
+    refd = df.decompose_batch(s64)
+    for b in range(4):
+        assert_parity(s64[b], gpu, refd, b, b, "f32")
