@@ -109,7 +109,6 @@ bool st_geometry(int64_t n, bool f64, st::Geo& g) {
       g.nseg = NC / g.lv[0].C;
       g.grp = 2048;
       g.ngrp = (g.nseg + g.grp - 1) / g.grp;
-      g.rpc = 2;
       g.nbch = g.units;  // one probe CTA per row-pair unit
       int bits = 0;
       while ((1LL << bits) < 2 * n + 1) ++bits;

@@ -100,7 +100,6 @@ struct Geo {
   int64_t nseg;          // extrema segments per signal = NC / C_0 (each 2 C_0 consecutive samples)
   int64_t grp;           // segments per fold group
   int64_t ngrp;          // fold groups per signal
-  int64_t rpc;           // (unused)
   int64_t nbch;          // probe chunks per signal (= units)
   int eb;                // E table split: E(j) = Eh[j >> eb] * El[j & (2^eb - 1)]
   int max_imfs, max_inner, window;
