@@ -145,6 +145,8 @@ fif_status fif_decompose_host(fif_plan_t plan, const void* h_signals, void* h_im
  * d_imfs [max_imfs+1][n_global/nranks] (this rank's block of every IMF and of the trend);
  * d_imf_count [1], d_filter_len / d_iters [max_imfs]: identical on every rank.  All ranks must
  * call it (collectives inside); it is stream-ordered like the batch regimes.
+ * Environment FIF_DIST_PEER=1 at plan creation: the all-to-alls become peer stores of the producing kernels
+ * into the other ranks' buffers (CUDA IPC over NVLink), with a barrier after each.
  * ------------------------------------------------------------------------- */
 fif_status fif_nccl_unique_id(void* out128);
 fif_status fif_plan_create_dist(fif_plan_t* out, int64_t n_global, fif_dtype dtype, fif_window window, double xi,

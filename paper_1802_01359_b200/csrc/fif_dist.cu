@@ -148,12 +148,15 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_d_pass(const __grid_c
 // ---------------------------------------------------------------- cross-rank digit: length-P DFTs
 // in [m0][s'] (P x Q/P) -> out [k0][s'] = sum_m0 in[m0][s'] e^{DIR 2 pi i m0 k0/P}, forward with the
 // twiddle e^{-2 pi i s k0/NC} (s = rank Q/P + s') applied after.
+// With `peer` (a table of the P ranks' receive buffers), output chunk k0 is stored straight into rank
+// k0's buffer at [rank Q/P + s'] over NVLink -- the all-to-all that follows the DFT fused into it.
 template <typename Real, int DIR>
 __global__ void __launch_bounds__(kThreads) k_d_rankdft(const __grid_constant__ DGeo d,
                                                         const typename Cx<Real>::V* __restrict__ in,
                                                         typename Cx<Real>::V* __restrict__ out,
                                                         const __grid_constant__ Tabs<Real> tb,
-                                                        const int32_t* __restrict__ s) {
+                                                        const int32_t* __restrict__ s,
+                                                        typename Cx<Real>::V* const* __restrict__ peer = nullptr) {
   using V = typename Cx<Real>::V;
   if (DIR > 0 && !s[S_ACT]) return;
   const int64_t W = d.Q / d.P;
@@ -171,9 +174,24 @@ __global__ void __launch_bounds__(kThreads) k_d_rankdft(const __grid_constant__ 
         acc = cadd(acc, cmul(x[m], w));
       }
       if (DIR < 0) acc = cmul(acc, cconj(st::Er(tb, d.g.eb, 4 * sglob * k0)));  // 2n/NC = 4
-      out[(int64_t)k0 * W + sp] = acc;
+      if (peer) peer[k0][(int64_t)d.rank * W + sp] = acc;
+      else out[(int64_t)k0 * W + sp] = acc;
     }
   }
+  if (peer) __threadfence_system();
+}
+
+// signal slices straight into the ranks' receive buffers (the forward all-to-all #1 as peer stores)
+template <typename Real>
+__global__ void __launch_bounds__(kThreads) k_d_scatter(const __grid_constant__ DGeo d,
+                                                        const typename Cx<Real>::V* __restrict__ z,
+                                                        typename Cx<Real>::V* const* __restrict__ peer) {
+  const int64_t W = d.Q / d.P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.Q; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = i / W;
+    peer[q][(int64_t)d.rank * W + (i - q * W)] = z[i];
+  }
+  __threadfence_system();
 }
 
 // inverse level-0 twiddle: out[s] = in[s] e^{+2 pi i s rank/NC}
@@ -186,6 +204,21 @@ __global__ void __launch_bounds__(kThreads) k_d_twiddle_inv(const __grid_constan
   if (!s[S_ACT]) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.Q; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = cmul(in[i], st::Er(tb, d.g.eb, 4 * i * d.rank));
+}
+// ... fused with the all-to-all #3: slice q of the twiddled block into rank q's buffer at [rank Q/P + s']
+template <typename Real>
+__global__ void __launch_bounds__(kThreads) k_d_twiddle_scatter(const __grid_constant__ DGeo d,
+                                                                const typename Cx<Real>::V* __restrict__ in,
+                                                                typename Cx<Real>::V* const* __restrict__ peer,
+                                                                const __grid_constant__ Tabs<Real> tb,
+                                                                const int32_t* __restrict__ s) {
+  if (!s[S_ACT]) return;
+  const int64_t W = d.Q / d.P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.Q; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = i / W;
+    peer[q][(int64_t)d.rank * W + (i - q * W)] = cmul(in[i], st::Er(tb, d.g.eb, 4 * i * d.rank));
+  }
+  __threadfence_system();
 }
 
 // ---------------------------------------------------------------- extrema partials (contiguous segments)
@@ -577,6 +610,7 @@ struct Nccl {
   decltype(&ncclCommInitRank) commInitRank = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclSend) send = nullptr;
   decltype(&ncclRecv) recv = nullptr;
   decltype(&ncclGroupStart) groupStart = nullptr;
@@ -594,6 +628,7 @@ struct Nccl {
     FIF_SYM(commInitRank, "ncclCommInitRank");
     FIF_SYM(commDestroy, "ncclCommDestroy");
     FIF_SYM(allGather, "ncclAllGather");
+    FIF_SYM(allReduce, "ncclAllReduce");
     FIF_SYM(send, "ncclSend");
     FIF_SYM(recv, "ncclRecv");
     FIF_SYM(groupStart, "ncclGroupStart");
@@ -632,6 +667,12 @@ struct DistPlan {
   int grid_pass = 0, grid_elem = 0, grid_probe = 0;
   int rounds = 0;
   int64_t Q = 0;
+  // peer mode (FIF_DIST_PEER=1): the all-to-alls fused into the producing kernels as NVLink peer
+  // stores into the ranks' buffers (CUDA IPC handles in a multi-process plan), a barrier after each
+  bool peer = false;
+  void* dpeer = nullptr;                 // device: [local ranks][2][P] pointers (U table, T table)
+  std::vector<void*> ipc_open;           // IPC-mapped peer buffers to close
+  void* dbar = nullptr;                  // one int for the NCCL barrier
 };
 
 namespace {
@@ -817,6 +858,61 @@ fif_status dist_setup_t(fif_plan_s* p, DistPlan& D) {
   return FIF_OK;
 }
 
+// Peer mode: per local rank a device table [U pointers of the P ranks][T pointers of the P ranks].
+// Emulated: the other ranks' buffers on this device.  NCCL: CUDA IPC handles of U and T all-gathered
+// over the communicator and opened (peer access over NVLink / NVSwitch).
+fif_status peer_setup(DistPlan& D) {
+  const int P = D.P, nl = (int)D.ranks.size();
+  std::vector<void*> tab((size_t)nl * 2 * P, nullptr);
+  if (D.emulated) {
+    for (int li = 0; li < nl; ++li)
+      for (int q = 0; q < P; ++q) {
+        tab[(size_t)li * 2 * P + q] = D.ranks[q].U;
+        tab[(size_t)li * 2 * P + P + q] = D.ranks[q].T;
+      }
+  } else {
+    struct H { cudaIpcMemHandle_t u, t; };
+    H mine;
+    if (cudaIpcGetMemHandle(&mine.u, D.ranks[0].U) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.t, D.ranks[0].T) != cudaSuccess)
+      return FIF_ERR_CUDA;
+    void* dh = nullptr;
+    if (cudaMalloc(&dh, sizeof(H) * (P + 1)) != cudaSuccess) return FIF_ERR_OOM;
+    cudaMemcpy((char*)dh + sizeof(H) * P, &mine, sizeof(H), cudaMemcpyHostToDevice);
+    fif_status st = nccl_check(nccl().allGather((char*)dh + sizeof(H) * P, dh, sizeof(H), ncclUint8, D.comm, 0),
+                               "ncclAllGather(ipc handles)");
+    std::vector<H> all(P);
+    if (st == FIF_OK && (cudaStreamSynchronize(0) != cudaSuccess ||
+                         cudaMemcpy(all.data(), dh, sizeof(H) * P, cudaMemcpyDeviceToHost) != cudaSuccess))
+      st = FIF_ERR_CUDA;
+    cudaFree(dh);
+    if (st != FIF_OK) return st;
+    for (int q = 0; q < P; ++q) {
+      if (q == D.rank) {
+        tab[q] = D.ranks[0].U;
+        tab[P + q] = D.ranks[0].T;
+        continue;
+      }
+      if (cudaIpcOpenMemHandle(&tab[q], all[q].u, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+          cudaIpcOpenMemHandle(&tab[P + q], all[q].t, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return FIF_ERR_CUDA;
+      D.ipc_open.push_back(tab[q]);
+      D.ipc_open.push_back(tab[P + q]);
+    }
+    if (cudaMalloc(&D.dbar, 16) != cudaSuccess) return FIF_ERR_OOM;
+  }
+  if (cudaMalloc(&D.dpeer, sizeof(void*) * tab.size()) != cudaSuccess) return FIF_ERR_OOM;
+  if (cudaMemcpy(D.dpeer, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return FIF_ERR_CUDA;
+  D.peer = true;
+  return FIF_OK;
+}
+// every rank's peer stores issued so far are complete and visible (stream-ordered)
+fif_status peer_barrier(DistPlan& D, cudaStream_t s) {
+  if (D.emulated) return FIF_OK;  // one stream: program order
+  return nccl_check(nccl().allReduce(D.dbar, D.dbar, 1, ncclInt32, ncclSum, D.comm, s), "ncclAllReduce(barrier)");
+}
+
 // The whole decomposition, phase by phase: each phase's kernels for every local rank, then the
 // phase's collective.  Static schedule (every rank issues the same collectives in the same order,
 // active or not).  Inverse buffers: pre -> T, local passes on T, twiddle T -> U, all-to-all U -> T,
@@ -864,18 +960,44 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
   ext_gather();
   all([&](int li, DRank& R) { k_d_decide_ext<<<1, 1, 0, s>>>(R.d, R.c, 0, lens + li * p->max_imfs, its + li * p->max_imfs); });
   // ---- a1 forward transform
-  ok(c_alltoall(D, [&](int li, DRank&) { return (const void*)SIG(li); }, [&](int, DRank& R) { return R.U; }, wb, s));
-  all([&](int, DRank& R) { k_d_rankdft<Real, -1><<<gw, TB, 0, s>>>(R.d, (const V*)R.U, (V*)R.T, tb, R.c.s); });
-  ok(c_alltoall(D, [&](int, DRank& R) { return (const void*)R.T; }, [&](int, DRank& R) { return R.U; }, wb, s));
-  all([&](int, DRank& R) {
-    for (int i = 0; i < R.d.g.L; ++i)
-      k_d_pass<Real, -1><<<gmin(R.d.g.lv[i].tiles, D.grid_pass), TB, D.smem_pass[i], s>>>(R.d, R.d.g.lv[i], (V*)R.U,
-                                                                                          tb, R.c.s);
-  });
-  ok(c_partner(D, [&](int, DRank& R) { return (const void*)R.U; }, [&](int, DRank& R) { return R.T; }, qb, s));
-  all([&](int, DRank& R) {
-    k_d_post<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.U, (const V*)R.T, (V*)R.X, (V*)R.Xm, tb, R.c.s);
-  });
+  // peer tables of local rank li: U pointers, T pointers (device), and the partner's T (host value)
+  auto ptabU = [&](int li) { return (V* const*)((void**)D.dpeer + (size_t)li * 2 * D.P); };
+  auto ptabT = [&](int li) { return (V* const*)((void**)D.dpeer + (size_t)li * 2 * D.P + D.P); };
+  if (D.peer) {
+    std::vector<void*> tab((size_t)nl * 2 * D.P);
+    cudaMemcpy(tab.data(), D.dpeer, sizeof(void*) * tab.size(), cudaMemcpyDeviceToHost);
+    all([&](int li, DRank& R) { k_d_scatter<Real><<<ge, TB, 0, s>>>(R.d, (const V*)SIG(li), ptabU(li)); });
+    ok(peer_barrier(D, s));
+    all([&](int li, DRank& R) {
+      k_d_rankdft<Real, -1><<<gw, TB, 0, s>>>(R.d, (const V*)R.U, nullptr, tb, R.c.s, ptabT(li));
+    });
+    ok(peer_barrier(D, s));
+    all([&](int, DRank& R) {
+      for (int i = 0; i < R.d.g.L; ++i)
+        k_d_pass<Real, -1><<<gmin(R.d.g.lv[i].tiles, D.grid_pass), TB, D.smem_pass[i], s>>>(R.d, R.d.g.lv[i],
+                                                                                            (V*)R.T, tb, R.c.s);
+    });
+    ok(peer_barrier(D, s));
+    all([&](int li, DRank& R) {
+      const int pr = (D.P - R.d.rank) % D.P;
+      const V* Zp = (const V*)tab[(size_t)li * 2 * D.P + D.P + pr];  // the partner's spectrum, read over NVLink
+      k_d_post<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.T, Zp, (V*)R.X, (V*)R.Xm, tb, R.c.s);
+    });
+    ok(peer_barrier(D, s));  // the partner has read our T before our first damping overwrites it
+  } else {
+    ok(c_alltoall(D, [&](int li, DRank&) { return (const void*)SIG(li); }, [&](int, DRank& R) { return R.U; }, wb, s));
+    all([&](int, DRank& R) { k_d_rankdft<Real, -1><<<gw, TB, 0, s>>>(R.d, (const V*)R.U, (V*)R.T, tb, R.c.s); });
+    ok(c_alltoall(D, [&](int, DRank& R) { return (const void*)R.T; }, [&](int, DRank& R) { return R.U; }, wb, s));
+    all([&](int, DRank& R) {
+      for (int i = 0; i < R.d.g.L; ++i)
+        k_d_pass<Real, -1><<<gmin(R.d.g.lv[i].tiles, D.grid_pass), TB, D.smem_pass[i], s>>>(R.d, R.d.g.lv[i],
+                                                                                            (V*)R.U, tb, R.c.s);
+    });
+    ok(c_partner(D, [&](int, DRank& R) { return (const void*)R.U; }, [&](int, DRank& R) { return R.T; }, qb, s));
+    all([&](int, DRank& R) {
+      k_d_post<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.U, (const V*)R.T, (V*)R.X, (V*)R.Xm, tb, R.c.s);
+    });
+  }
   // ---- IMFs
   for (int m = 0; m < p->max_imfs; ++m) {
     // a4/a5: cap probe, then K-ary rounds (device-side early exit when not searching)
@@ -897,11 +1019,20 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
       for (int i = R.d.g.L - 1; i >= 0; --i)
         k_d_pass<Real, 1><<<gmin(R.d.g.lv[i].tiles, D.grid_pass), TB, D.smem_pass[i], s>>>(R.d, R.d.g.lv[i], (V*)R.T,
                                                                                          tb, R.c.s);
-      k_d_twiddle_inv<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.T, (V*)R.U, tb, R.c.s);
+      if (!D.peer) k_d_twiddle_inv<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.T, (V*)R.U, tb, R.c.s);
     });
-    ok(c_alltoall(D, [&](int, DRank& R) { return (const void*)R.U; }, [&](int, DRank& R) { return R.T; }, wb, s));
-    all([&](int, DRank& R) { k_d_rankdft<Real, 1><<<gw, TB, 0, s>>>(R.d, (const V*)R.T, (V*)R.U, tb, R.c.s); });
-    ok(c_alltoall(D, [&](int, DRank& R) { return (const void*)R.U; }, [&](int, DRank& R) { return R.T; }, wb, s));
+    if (D.peer) {  // all-to-alls #3 and #4 as peer stores of the twiddle and rank-DFT kernels
+      all([&](int li, DRank& R) { k_d_twiddle_scatter<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.T, ptabU(li), tb, R.c.s); });
+      ok(peer_barrier(D, s));
+      all([&](int li, DRank& R) {
+        k_d_rankdft<Real, 1><<<gw, TB, 0, s>>>(R.d, (const V*)R.U, nullptr, tb, R.c.s, ptabT(li));
+      });
+      ok(peer_barrier(D, s));
+    } else {
+      ok(c_alltoall(D, [&](int, DRank& R) { return (const void*)R.U; }, [&](int, DRank& R) { return R.T; }, wb, s));
+      all([&](int, DRank& R) { k_d_rankdft<Real, 1><<<gw, TB, 0, s>>>(R.d, (const V*)R.T, (V*)R.U, tb, R.c.s); });
+      ok(c_alltoall(D, [&](int, DRank& R) { return (const void*)R.U; }, [&](int, DRank& R) { return R.T; }, wb, s));
+    }
     all([&](int li, DRank& R) {
       k_d_epi<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.T, OUT(li), R.c);
       k_d_segs<Real><<<gs, TB, 0, s>>>(R.d, OUT(li), R.c);
@@ -942,7 +1073,9 @@ fif_status dist_create(fif_plan_s* p, const void* uid, int rank, int nranks, int
   } else if (!D->emulated) {
     D->emulated = true;  // a one-rank "distributed" plan needs no communicator
   }
-  return dist_setup(p, *D);
+  fif_status st = dist_setup(p, *D);
+  if (st == FIF_OK && getenv("FIF_DIST_PEER")) st = peer_setup(*D);
+  return st;
 }
 fif_status dist_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
                           cudaStream_t s) {
@@ -968,6 +1101,9 @@ void dist_free(fif_plan_s* p) {
   cudaFree(D->utab);
   cudaFree(D->rbase);
   cudaFree(D->rmir);
+  for (void* q : D->ipc_open) cudaIpcCloseMemHandle(q);
+  cudaFree(D->dpeer);
+  cudaFree(D->dbar);
   if (D->comm) nccl().commDestroy(D->comm);
   delete D;
   p->dist = nullptr;

@@ -134,3 +134,43 @@ def test_dist_nccl_one_rank(monkeypatch):
         np.testing.assert_array_equal(a[i], b[i])
     for m in range(a[1][0] + 1):
         assert np.linalg.norm(a[0][0, m] - b[0][0, m]) <= 1e-11 * max(np.linalg.norm(a[0][0, m]), 1e-5 * np.linalg.norm(s))
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_dist_peer_mode_fused_all_to_all(P, monkeypatch):
+    """FIF_DIST_PEER: the four all-to-alls fused into their producing kernels as peer stores into the
+    other ranks' buffers (NVLink in a multi-process plan; here the emulated ranks' buffers) -- same
+    decomposition as the collective path and the oracle."""
+    monkeypatch.setenv("FIF_DIST_PEER", "1")
+    n = 4096
+    for i in range(2):
+        s = signals.tones_signal(n, 35, i)[None]
+        gpu = run_dist(s[0], P)
+        ref = oracle.decompose(s)
+        assert_parity(s[0], gpu, ref, 0, 0)
+    s = signals.cfg3_signal(7, n=1 << 16)
+    monkeypatch.delenv("FIF_DIST_PEER")
+    a = run_dist(s, P)
+    monkeypatch.setenv("FIF_DIST_PEER", "1")
+    b = run_dist(s, P)
+    for i in (1, 2, 3):
+        np.testing.assert_array_equal(a[i], b[i])
+    assert np.abs(a[0] - b[0]).max() == 0.0  # the same arithmetic, only the data movement differs
+
+
+def test_dist_peer_mode_nccl_one_rank(monkeypatch):
+    """Peer mode through NCCL (IPC-handle all-gather + barrier all-reduce) on a one-rank communicator."""
+    monkeypatch.setenv("FIF_DIST_FORCE_NCCL", "1")
+    monkeypatch.setenv("FIF_DIST_PEER", "1")
+    n = 1 << 14
+    s = signals.cfg3_signal(3, n=n)
+    plan = fif.Plan.dist(n, 0, 1, uid=fif.nccl_unique_id())
+    x = torch.from_numpy(s[None]).cuda()
+    out = plan.alloc_outputs()
+    plan.decompose(x, *out)
+    torch.cuda.synchronize()
+    b = [t.cpu().numpy() for t in out]
+    plan.close()
+    a = run_gpu(s[None], regime=fif.REGIME_STREAMED)
+    for i in (1, 2, 3):
+        np.testing.assert_array_equal(a[i], b[i])
