@@ -37,4 +37,4 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 src = open(sys.argv[4] if len(sys.argv) > 4 else "/root/repo/paper_1802_01359_b200/csrc/fif_resident.cuh").read().split("\n")
 for l, c in byline.most_common(top):
     s = src[l - 1].strip()[:70] if l else ""
-    print(f"{l:5} {c/tot*100:5.1f}% st {byline_st[l]/tst*100:5.1f}%  {dict(byline_ops[l].most_common(4))}  | {s}")
+    print(f"{l or 0:5} {c/tot*100:5.1f}% st {byline_st[l]/tst*100:5.1f}%  {dict(byline_ops[l].most_common(4))}  | {s}")
