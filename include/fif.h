@@ -62,9 +62,8 @@ typedef enum {
 
 /* Create a plan for `batch` independent signals of length n.
  *   n          : samples per signal, even.  Resident regime: powers of two 512 <= n <= 8192 (fp32: <= 16384).
- *                Streamed regime: n/2 = N1 N2 with N1, N2 of the form 2^a 3^b 5^c, N2 <= 2048 (f64) /
- *                4096 (f32), N1 <= 1024 -- e.g. every 2^a 3^b 5^c up to n = 2^22 (f64) / 2^23 (f32).
- *                Other n -> FIF_ERR_UNSUPPORTED_N.
+ *                Streamed regime: n/2 of the form 2^a 3^b 5^c, n <= 2^27 (a multi-level FFT of 2-4
+ *                levels in HBM).  Other n -> FIF_ERR_UNSUPPORTED_N.
  *   batch      : number of signals, >= 0 (0 is a valid no-op plan).
  *   dtype      : element type of signals and IMFs.  f32 computes the FFTs in fp32 and
  *                accumulates the stopping sums and takes the floor in fp64 (reading A14).
@@ -73,8 +72,9 @@ typedef enum {
  *   max_inner  : iteration cap (>= 1).
  *   max_imfs   : cap on the number of IMFs (>= 1).
  * Allocates small device tables (sin table and FFT twiddles, O(n) bytes) on the
- * current device and uploads them synchronously; a streamed plan also allocates its work
- * buffers (2 batch n/2 complex + O(batch) control).  On error *out is NULL. */
+ * current device and uploads them synchronously; a streamed plan also allocates its decompose
+ * workspace (2 batch n/2 complex + O(batch) control; see fif_plan_set_workspace to supply it
+ * instead).  On error *out is NULL. */
 fif_status fif_plan_create(fif_plan_t* out, int64_t n, int64_t batch, fif_dtype dtype, fif_window window, double xi,
                            double delta, int32_t max_inner, int32_t max_imfs);
 /* Same, forcing a regime (FIF_REGIME_AUTO = fif_plan_create).  Both regimes compute the same
@@ -102,10 +102,28 @@ fif_status fif_plan_set_options(fif_plan_t plan, fif_stop_rule stop, double gamm
  *   of this value": f* = the largest local maximum of |DFT(r)_f|^2, f = 1..n/2, with
  *   |DFT(r)_f|^2 >= 1e-4 max (1% in magnitude), and L from the extrema rule at k = 2 f*
  *   (reading A20); no such bin ends the decomposition (the extrema guard k >= 2 still applies).
- * Batch plans only (FIF_ERR_UNSUPPORTED_N on a distributed plan: neighbouring bins live on other ranks);
- * a streamed plan allocates (n/2+1) doubles per signal on first use (FIF_ERR_OOM). */
+ * Batch plans only (FIF_ERR_UNSUPPORTED_N on a distributed plan: neighbouring bins live on other ranks).
+ * A streamed plan needs (n/2+1) doubles per signal more workspace under FIF_MASK_SPECTRAL: a plan-owned
+ * workspace is re-allocated (FIF_ERR_OOM), a caller workspace must already be large enough
+ * (FIF_ERR_INVALID_ARG otherwise, the rule unchanged).  No decompose on the plan may be pending. */
 typedef enum { FIF_MASK_EXTREMA = 0, FIF_MASK_SPECTRAL = 1 } fif_mask_rule;
 fif_status fif_plan_set_mask_rule(fif_plan_t plan, fif_mask_rule rule);
+
+/* Decompose workspace (SURVEY.md §8b "ownership": the caller may own every large device buffer).
+ * fif_plan_workspace_bytes: the device scratch the plan's fif_decompose uses beyond the caller's
+ *   inputs and outputs, with the current options -- streamed regime: the spectrum ping-pong
+ *   2 x batch x (n/2) complex, the Nyquist bins, the per-signal control block and (FIF_MASK_SPECTRAL)
+ *   batch x (n/2+1) doubles; 0 for the resident and iterative regimes (their state lives on chip) and
+ *   for distributed plans (whose buffers are plan-owned, peer-mappable).
+ * fif_plan_set_workspace: use d_ws (device memory of the plan's device, 256-byte aligned, >= the
+ *   bytes above) from now on; the plan frees the workspace it owned.  The caller keeps d_ws alive
+ *   until fif_destroy or the next fif_plan_set_workspace; d_ws = NULL returns to a plan-owned
+ *   workspace.  Synchronises the device (no decompose on the plan may be pending) and resets the
+ *   control block.  No-op on resident / iterative plans.  Errors: FIF_ERR_INVALID_ARG (misaligned,
+ *   not device memory of that device, too small, or non-NULL on a distributed plan), FIF_ERR_OOM,
+ *   FIF_ERR_CUDA. */
+fif_status fif_plan_workspace_bytes(fif_plan_t plan, size_t* bytes);
+fif_status fif_plan_set_workspace(fif_plan_t plan, void* d_ws, size_t bytes);
 
 /* Decompose the batch (device pointers, caller-owned, current device):
  *   d_signals    [batch][n] dtype, read only.

@@ -187,12 +187,38 @@ fif_status fif_plan_set_options(fif_plan_t p, fif_stop_rule stop, double gamma) 
 fif_status fif_plan_set_mask_rule(fif_plan_t p, fif_mask_rule rule) {
   if (!p || (rule != FIF_MASK_EXTREMA && rule != FIF_MASK_SPECTRAL)) return FIF_ERR_INVALID_ARG;
   if (rule == FIF_MASK_SPECTRAL && (p->regime == 2 || p->regime == 3)) return FIF_ERR_UNSUPPORTED_N;
-  if (rule == FIF_MASK_SPECTRAL && p->regime == 1 && !p->d_pnat) {
-    const int64_t B = p->batch > 0 ? p->batch : 1;
-    if (cudaMalloc(&p->d_pnat, sizeof(double) * (size_t)B * (size_t)(p->n / 2 + 1)) != cudaSuccess) return FIF_ERR_OOM;
-  }
+  const int32_t old = p->mask;
   p->mask = (int32_t)rule;
+  if (p->regime == 1 && old != p->mask) {  // the power array lives in the workspace: re-carve it
+    fif_status s = FIF_ERR_INVALID_ARG;
+    if (!p->d_ws_user || p->ws_user_bytes >= st_workspace_bytes(p))
+      s = st_bind_workspace(p, p->d_ws_user, p->ws_user_bytes);
+    if (s != FIF_OK) {
+      p->mask = old;
+      return s;
+    }
+  }
   return FIF_OK;
+}
+
+fif_status fif_plan_workspace_bytes(fif_plan_t p, size_t* bytes) {
+  if (!p || !bytes) return FIF_ERR_INVALID_ARG;
+  *bytes = p->regime == 1 ? st_workspace_bytes(p) : 0;
+  return FIF_OK;
+}
+
+fif_status fif_plan_set_workspace(fif_plan_t p, void* d_ws, size_t bytes) {
+  if (!p || ((uintptr_t)d_ws & 255u)) return FIF_ERR_INVALID_ARG;
+  if (p->regime == 2) return d_ws ? FIF_ERR_INVALID_ARG : FIF_OK;  // distributed: plan-owned, peer-mappable
+  if (p->regime != 1) return FIF_OK;                                 // resident / iterative: no workspace
+  if (d_ws) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, d_ws) != cudaSuccess || a.type != cudaMemoryTypeDevice || a.device != p->device) {
+      cudaGetLastError();
+      return FIF_ERR_INVALID_ARG;
+    }
+  }
+  return st_bind_workspace(p, d_ws, bytes);
 }
 
 fif_status fif_nccl_unique_id(void* out128) {

@@ -51,11 +51,18 @@ struct fif_plan_s {
   void* d_Th = nullptr;   // V (Real) copies
   void* d_Tl = nullptr;
   void* d_twl = nullptr;  // V per-level Stockham twiddles
-  void* d_X = nullptr;    // V[B][NC] spectrum (digit-reversed multi-level order)
-  void* d_Xn = nullptr;   // V[B] Nyquist bins
+  // decompose workspace (fif_plan_workspace_bytes): d_X | d_Xn | d_ctl [| d_pnat], carved from one block --
+  // plan-owned (d_ws_own) unless the caller handed its own (fif_plan_set_workspace, d_ws_user)
+  void* d_ws_own = nullptr;
+  void* d_ws_user = nullptr;
+  size_t ws_user_bytes = 0;
+  size_t ws_xn = 0, ws_ctl = 0, ws_pnat = 0, ws_end = 0, ws_end_pnat = 0;  // offsets (bytes)
+  size_t ws_ctl_bytes = 0;
+  void* d_X = nullptr;    // V[2][B][NC] spectrum ping-pong (digit-reversed multi-level order)
+  void* d_Xn = nullptr;   // V[2][B] Nyquist bins
   void* d_ctl = nullptr;  // per-signal control arrays + partials
   void* d_utab = nullptr;   // int2[units] mirror-pair rows
-  void* d_pnat = nullptr;   // double[B][NC+1] natural-order powers (spectral-peak rule, allocated on demand)
+  void* d_pnat = nullptr;   // double[B][NC+1] natural-order powers (spectral-peak rule only; in the workspace)
   void* d_rbase = nullptr;  // int[rows] row bin bases
   void* d_rmir = nullptr;   // int[rows] mirror rows
   fifgpu::st::Ctl ctl{};
@@ -99,6 +106,9 @@ void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int3
                   int64_t batch, int64_t boff, cudaStream_t s);
 int st_kernels_per_call(const fif_plan_s* p);
 void st_free(fif_plan_s* p);
+// workspace: bytes needed with the current options; (re)bind the buffers to `base` (nullptr: plan-owned block)
+size_t st_workspace_bytes(const fif_plan_s* p);
+fif_status st_bind_workspace(fif_plan_s* p, void* base, size_t bytes);
 
 // iterative regime (fif_iterative.cu): Algorithm 2 literally (the IF baseline of PAPER.md:693)
 fif_status it_setup(fif_plan_s* p);

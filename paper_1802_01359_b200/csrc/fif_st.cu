@@ -226,29 +226,16 @@ fif_status st_setup_t(fif_plan_s* p) {
   const size_t segb = (size_t)B * g.nseg * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t grpb = (size_t)B * g.ngrp * (sizeof(uint32_t) + 2 * sizeof(Real));
   const size_t redb = (size_t)B * g.nbch * 2 * st::kProbes * sizeof(double);
-  const size_t ctl_bytes = ni * sizeof(int32_t) + segb + grpb + redb + 256;
-  // two spectrum buffers (X_in / X_out ping-pong per IMF: the speculative damping keeps X_in intact)
-  if (cudaMalloc(&p->d_X, 2 * sizeof(V) * B * g.NC) != cudaSuccess || cudaMalloc(&p->d_Xn, 2 * sizeof(V) * B) != cudaSuccess ||
-      cudaMalloc(&p->d_ctl, ctl_bytes) != cudaSuccess)
-    return FIF_ERR_OOM;
-  char* q = (char*)p->d_ctl;
-  auto take = [&](size_t bytes) {
-    char* r = q;
-    q += (bytes + 15) & ~(size_t)15;
-    return (void*)r;
-  };
-  st::Ctl& c = p->ctl;
-  c.red = (double*)take(redb);
-  c.segv = take((size_t)B * g.nseg * 2 * sizeof(Real));
-  c.gv = take((size_t)B * g.ngrp * 2 * sizeof(Real));
-  c.segi = (uint32_t*)take((size_t)B * g.nseg * sizeof(uint32_t));
-  c.gi = (uint32_t*)take((size_t)B * g.ngrp * sizeof(uint32_t));
-  int32_t* ip = (int32_t*)take(ni * sizeof(int32_t));
-  c.k = ip; c.L = ip + B; c.N = ip + 2 * B; c.M = ip + 3 * B; c.active = ip + 4 * B; c.search = ip + 5 * B;
-  c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B); c.redo = ip + 10 * B;
-  c.slist = ip + 11 * B; c.scnt = ip + 12 * B;
-  c.pmax = (double*)take((size_t)B * sizeof(double));
-  if (cudaMemset(p->d_ctl, 0, ctl_bytes) != cudaSuccess) return FIF_ERR_CUDA;
+  // workspace layout: two spectrum buffers (X_in / X_out ping-pong per IMF: the speculative damping
+  // keeps X_in intact), their Nyquist bins, the control block, and (spectral-peak rule) the power array
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  p->ws_ctl_bytes = ni * sizeof(int32_t) + segb + grpb + redb + 256;
+  p->ws_xn = up(2 * sizeof(V) * B * g.NC);
+  p->ws_ctl = p->ws_xn + up(2 * sizeof(V) * B);
+  p->ws_pnat = p->ws_ctl + up(p->ws_ctl_bytes);
+  p->ws_end = p->ws_pnat;
+  p->ws_end_pnat = p->ws_pnat + up(sizeof(double) * B * (size_t)(g.NC + 1));
+  if ((s = st_bind_workspace(p, nullptr, 0)) != FIF_OK) return s;
   // shared memory and grids
   for (int i = 0; i < g.L - 1; ++i)  // three tile buffers + the level's twiddles
     p->st_smem_col[i] = 3 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch + sizeof(V) * (size_t)g.lv[i].F;
@@ -411,6 +398,54 @@ int st_kernels_per_call(const fif_plan_s* p) {
   return (int)(waves * (2 + (L - 1) + 1 + (p->mask ? 2 : 0) + p->max_imfs * per_imf + 1));
 }
 
+size_t st_workspace_bytes(const fif_plan_s* p) { return p->mask ? p->ws_end_pnat : p->ws_end; }
+
+// Carve d_X, d_Xn, the control block (zeroed: the state a fresh plan starts from) and, with the
+// spectral-peak rule, d_pnat out of one block: the caller's (base != nullptr, >= bytes needed) or a
+// plan-owned allocation.  No decompose on the plan may be pending.
+fif_status st_bind_workspace(fif_plan_s* p, void* base, size_t bytes) {
+  const size_t need = st_workspace_bytes(p);
+  if (base && bytes < need) return FIF_ERR_INVALID_ARG;
+  if (cudaDeviceSynchronize() != cudaSuccess) return FIF_ERR_CUDA;
+  cudaFree(p->d_ws_own);
+  p->d_ws_own = nullptr;
+  p->d_ws_user = base;
+  p->ws_user_bytes = base ? bytes : 0;
+  if (!base) {
+    if (cudaMalloc(&p->d_ws_own, need) != cudaSuccess) return FIF_ERR_OOM;
+    base = p->d_ws_own;
+  }
+  char* w = (char*)base;
+  p->d_X = w;
+  p->d_Xn = w + p->ws_xn;
+  p->d_ctl = w + p->ws_ctl;
+  p->d_pnat = p->mask ? (void*)(w + p->ws_pnat) : nullptr;
+  const st::Geo& g = p->geo;
+  const int64_t B = p->batch > 0 ? p->batch : 1;
+  const size_t rs = p->dtype == FIF_F64 ? sizeof(double) : sizeof(float);
+  const size_t ni = (size_t)B * 13 + 2 * (size_t)B;
+  char* q = (char*)p->d_ctl;
+  auto take = [&](size_t nb) {
+    char* r = q;
+    q += (nb + 15) & ~(size_t)15;
+    return (void*)r;
+  };
+  st::Ctl& c = p->ctl;
+  c.red = (double*)take((size_t)B * g.nbch * 2 * st::kProbes * sizeof(double));
+  c.segv = take((size_t)B * g.nseg * 2 * rs);
+  c.gv = take((size_t)B * g.ngrp * 2 * rs);
+  c.segi = (uint32_t*)take((size_t)B * g.nseg * sizeof(uint32_t));
+  c.gi = (uint32_t*)take((size_t)B * g.ngrp * sizeof(uint32_t));
+  int32_t* ip = (int32_t*)take(ni * sizeof(int32_t));
+  c.k = ip; c.L = ip + B; c.N = ip + 2 * B; c.M = ip + 3 * B; c.active = ip + 4 * B; c.search = ip + 5 * B;
+  c.lo = ip + 6 * B; c.hi = ip + 7 * B; c.bad = ip + 8 * B; c.cnt = (uint32_t*)(ip + 9 * B); c.redo = ip + 10 * B;
+  c.slist = ip + 11 * B; c.scnt = ip + 12 * B;
+  c.pmax = (double*)take((size_t)B * sizeof(double));
+  if (cudaMemset(p->d_ctl, 0, p->ws_ctl_bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return FIF_ERR_CUDA;
+  return FIF_OK;
+}
+
 fif_status st_setup(fif_plan_s* p) { return p->dtype == FIF_F64 ? st_setup_t<double>(p) : st_setup_t<float>(p); }
 void st_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
                   int64_t batch, int64_t boff, cudaStream_t s) {
@@ -423,11 +458,8 @@ void st_free(fif_plan_s* p) {
   cudaFree(p->d_Th);
   cudaFree(p->d_Tl);
   cudaFree(p->d_twl);
-  cudaFree(p->d_X);
-  cudaFree(p->d_Xn);
-  cudaFree(p->d_ctl);
+  cudaFree(p->d_ws_own);  // (a caller workspace stays the caller's)
   cudaFree(p->d_utab);
-  cudaFree(p->d_pnat);
   cudaFree(p->d_rbase);
   cudaFree(p->d_rmir);
   for (int i = 0; i < 2; ++i)

@@ -23,7 +23,8 @@ REGIME_AUTO, REGIME_RESIDENT, REGIME_STREAMED, REGIME_ITERATIVE = 0, 1, 2, 3
 SYMBOLS = ["fif_plan_create", "fif_plan_create_ex", "fif_decompose", "fif_decompose_host", "fif_destroy", "fif_status_string",
            "fif_plan_kernels_per_call", "fif_plan_regime", "fif_plan_launch_config", "fif_test_rfft",
            "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner", "fif_nccl_unique_id",
-           "fif_plan_create_dist", "fif_plan_create_dist_emulated", "fif_plan_set_options", "fif_plan_set_mask_rule"]
+           "fif_plan_create_dist", "fif_plan_create_dist_emulated", "fif_plan_set_options", "fif_plan_set_mask_rule",
+           "fif_plan_workspace_bytes", "fif_plan_set_workspace"]
 STOP_SD, STOP_N0 = 0, 1
 MASK_EXTREMA, MASK_SPECTRAL = 0, 1
 
@@ -67,6 +68,8 @@ def lib():
         L.fif_nccl_unique_id.argtypes = [vp]
         L.fif_plan_set_options.argtypes = [vp, ctypes.c_int, d]
         L.fif_plan_set_mask_rule.argtypes = [vp, ctypes.c_int]
+        L.fif_plan_workspace_bytes.argtypes = [vp, ctypes.POINTER(ctypes.c_size_t)]
+        L.fif_plan_set_workspace.argtypes = [vp, vp, ctypes.c_size_t]
         L.fif_plan_create_dist.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32, i32, vp,
                                            i32, i32]
         L.fif_plan_create_dist_emulated.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32,
@@ -137,6 +140,22 @@ class Plan:
     def set_mask_rule(self, rule=MASK_EXTREMA):
         """fif_plan_set_mask_rule: filter length from the extrema count or the highest spectral peak."""
         _check(lib().fif_plan_set_mask_rule(self._h, int(rule)), "fif_plan_set_mask_rule")
+        return self
+
+    def workspace_bytes(self):
+        """fif_plan_workspace_bytes: device scratch the plan's decompose needs (0: none)."""
+        b = ctypes.c_size_t()
+        _check(lib().fif_plan_workspace_bytes(self._h, ctypes.byref(b)), "fif_plan_workspace_bytes")
+        return int(b.value)
+
+    def set_workspace(self, ws=None):
+        """fif_plan_set_workspace: hand the plan a caller-owned device buffer (a uint8 torch tensor of at
+        least workspace_bytes(), 256-byte aligned); None returns to a plan-owned workspace.  The tensor is
+        kept referenced here so it outlives its use."""
+        _check(lib().fif_plan_set_workspace(self._h, _ptr(ws), ctypes.c_size_t(0 if ws is None else ws.numel()
+                                                                                * ws.element_size())),
+               "fif_plan_set_workspace")
+        self._ws = ws
         return self
 
     def decompose(self, signals, imfs, count, lens, iters, stream=None):
