@@ -32,8 +32,17 @@ def _cuda():
 
 
 def test_cfg3_full_size_every_decision():
-    n, delta, cap = 1 << 26, 1e-3, 200
-    s = signals.cfg3_signal(0)
+    _every_decision(signals.cfg3_signal(0))
+
+
+def test_maximum_length_every_decision():
+    """The largest n a plan accepts (2^27; include/fif.h), cfg3 recipe: the same per-decision checks on the
+    first 3 IMFs (each costs the oracle side two 2^27-point numpy FFTs), telescoping on all."""
+    _every_decision(signals.cfg3_signal(0, n=1 << 27), check=3)
+
+
+def _every_decision(s, check=10):
+    n, delta, cap = s.shape[0], 1e-3, 200
     plan = fif.Plan(n, 1, "f64", delta=delta)
     assert plan.launch_config()["regime"] == "streamed"
     x = torch.from_numpy(s[None]).cuda()
@@ -47,6 +56,9 @@ def test_cfg3_full_size_every_decision():
     c = np.full(n // 2 + 1, 2.0)
     c[0] = c[-1] = 1.0
     for m in range(M):
+        if m >= check:
+            r = r - imfs[0, m].cpu().numpy()
+            continue
         # r here is s minus the GPU's IMFs in the GPU's own order, i.e. the GPU's remainder bit for bit;
         # the smallest difference among 2^26 noisy samples is ~1e-10 max|s|, far above rounding
         k, em = oracle.count_extrema(r)
