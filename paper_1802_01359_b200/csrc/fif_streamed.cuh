@@ -520,6 +520,80 @@ __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, 
   }
 }
 
+// Thread-chunk variant of tile_segments: the tps = blockDim / F threads t = f + F q (q = 0..tps-1) of
+// segment f own its consecutive chunks q of R = 2C / tps reals -- the lanes of a warp read the same
+// column at consecutive rows, conflict-free -- each reduces its chunk (sign bits, one popc; the exact
+// rule when a difference is zero) including the difference into the next chunk, and thread f folds the
+// tps packed monoids in order.  Returns false (nothing written) when the tile shape does not allow it.
+template <typename Real>
+__device__ bool tile_segments_thr(const typename Cx<Real>::V* buf, const Level& lv, int64_t seg0, int64_t segstep,
+                                  uint32_t* __restrict__ segi, Real* __restrict__ segv) {
+  using V = typename Cx<Real>::V;
+  __shared__ uint32_t pks[kColThreads];
+  const int F = lv.F, nr = 2 * lv.C, nt = (int)blockDim.x;
+  if (nt > kColThreads || nt % F) return false;
+  const int tps = nt / F;
+  if (nr % tps) return false;
+  const int R = nr / tps;
+  if (R > 64 || (R & 1)) return false;
+  const int t = threadIdx.x, f = t % F, q = t / F, c0 = q * (R >> 1);
+  const bool last = q == tps - 1;
+  uint64_t bits = 0;
+  int nd = 0;
+  bool zero = false;
+  Real prev;
+  {
+    const V v = buf[sidx<V>(c0, f, lv.pitch, lv.swz)];
+    const Real d = v.y - v.x;
+    zero |= d == (Real)0;
+    bits |= (uint64_t)(d < (Real)0);
+    nd = 1;
+    prev = v.y;
+  }
+  for (int c = c0 + 1; c < c0 + R / 2; ++c) {
+    const V v = buf[sidx<V>(c, f, lv.pitch, lv.swz)];
+    const Real d0 = v.x - prev, d1 = v.y - v.x;
+    zero |= (d0 == (Real)0) | (d1 == (Real)0);
+    bits |= ((uint64_t)(d0 < (Real)0) << nd) | ((uint64_t)(d1 < (Real)0) << (nd + 1));
+    nd += 2;
+    prev = v.y;
+  }
+  Real nxt = (Real)0;
+  if (!last) {  // the difference into the next chunk's first real
+    nxt = buf[sidx<V>(c0 + R / 2, f, lv.pitch, lv.swz)].x;
+    const Real d = nxt - prev;
+    zero |= d == (Real)0;
+    bits |= (uint64_t)(d < (Real)0) << nd;
+    ++nd;
+  }
+  Mono m;
+  if (!zero) {
+    const int cnt = nd > 1 ? __popcll((bits ^ (bits >> 1)) & ((1ull << (nd - 1)) - 1ull)) : 0;
+    m = Mono{(bits & 1ull) ? -1 : 1, ((bits >> (nd - 1)) & 1ull) ? -1 : 1, cnt};
+  } else {  // zero differences are dropped (A4): the exact sequential rule over this chunk
+    m = Mono{0, 0, 0};
+    Real pv = buf[sidx<V>(c0, f, lv.pitch, lv.swz)].x;
+    for (int j = 2 * c0 + 1; j < 2 * c0 + R; ++j) {
+      const V v = buf[sidx<V>(j >> 1, f, lv.pitch, lv.swz)];
+      const Real x = (j & 1) ? v.y : v.x;
+      m = mcomb(m, mdiff<Real>(x - pv));
+      pv = x;
+    }
+    if (!last) m = mcomb(m, mdiff<Real>(nxt - pv));
+  }
+  pks[t] = mpack(m);
+  __syncthreads();
+  if (q == 0) {
+    Mono acc = munpack(pks[f]);
+    for (int qq = 1; qq < tps; ++qq) acc = mcomb(acc, munpack(pks[f + qq * F]));
+    const int64_t sg = seg0 + (int64_t)f * segstep;
+    segi[sg] = mpack(acc);
+    segv[2 * sg] = buf[sidx<V>(0, f, lv.pitch, lv.swz)].x;
+    segv[2 * sg + 1] = buf[sidx<V>(lv.C - 1, f, lv.pitch, lv.swz)].y;
+  }
+  return true;
+}
+
 // Ordered fold of items [i0, i1) (monoid + first/last value), boundary differences between
 // consecutive items included (those before i0 are not).  Result in thread 0: monoid, first, last.
 template <typename Real>
@@ -680,7 +754,8 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         }
       }
       if (!finite) atomicOr(c.bad + cur.b, 1);
-      tile_segments<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+      if (!tile_segments_thr<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
+        tile_segments<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     }
     V r[KIND == PASS_INV_LAST ? U : 1];
     if (KIND == PASS_INV_LAST) {  // remainder loads in flight during the transform
@@ -712,7 +787,8 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         }
       }
       __syncthreads();
-      tile_segments<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+      if (!tile_segments_thr<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
+        tile_segments<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     } else {
       // forward: this level's twiddle e^{-2 pi i s k/(F S)}; inverse: the next coarser level's
       // e^{+2 pi i s' k'/(F' S')} with s' = f S + s, k' = a mod F'.  When C divides the block size a

@@ -1,7 +1,7 @@
 """Attribute ncu per-instruction stall samples / executed instructions of ONE kernel to source lines of
 one file (the outermost inlined frame that lies inside [lo, hi] of that file).  Dev tool.
 usage: sass_by_line.py <ncu-rep> <cubin> <mangled kernel name> <source file> <lo> <hi> [top] [inner|outer]"""
-import csv, io, re, subprocess, sys
+import csv, io, os, re, subprocess, sys
 from collections import Counter
 
 rep, cubin, kern, srcf, lo, hi = sys.argv[1:7]
@@ -10,13 +10,23 @@ top = int(sys.argv[7]) if len(sys.argv) > 7 else 40
 MODE = sys.argv[8] if len(sys.argv) > 8 else "outer"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
-h = rows[1]
+# one block per kernel in the report: pick the one whose name contains $NCU_KSUB (default: the first)
+ksub = os.environ.get("NCU_KSUB", "")
+blocks, name, h = [], None, None
+for r in csv.reader(io.StringIO(raw)):
+    if r and r[0] == "Kernel Name":
+        name = r[1]
+        continue
+    if r and "Address" in r and "Source" in r:
+        h = r
+        blocks.append((name, h, []))
+        continue
+    if blocks and len(r) == len(blocks[-1][1]):
+        blocks[-1][2].append(r)
+name, h, body = next(b for b in blocks if ksub in (b[0] or ""))
 iA, iS, iW, iE = (h.index(k) for k in ("Address", "Source", "Warp Stall Sampling (All Samples)", "Instructions Executed"))
 data, base = [], None
-for r in rows[2:]:
-    if len(r) < len(h):
-        continue
+for r in body:
     a = int(r[iA], 16) if r[iA].startswith("0x") else int(r[iA])
     base = a if base is None else base
     data.append((a - base, r[iS], int(r[iW] or 0), int(r[iE] or 0)))
