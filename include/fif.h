@@ -109,6 +109,16 @@ fif_status fif_plan_set_options(fif_plan_t plan, fif_stop_rule stop, double gamm
 typedef enum { FIF_MASK_EXTREMA = 0, FIF_MASK_SPECTRAL = 1 } fif_mask_rule;
 fif_status fif_plan_set_mask_rule(fif_plan_t plan, fif_mask_rule rule);
 
+/* Per-L eigenvalue table (SURVEY.md §8f "next" 4; "computing in advance the eigenvalues
+ * ... for every scaling reduces even further the computational time"): enable != 0 precomputes, on the
+ * plan's device, w_hat_k (k = 0..n/2) for every filter half-length L = 2..floor((n-1)/4) the rule can
+ * produce ((floor((n-1)/4) - 1) (n/2 + 1) elements of dtype: 16.8 MB at n = 4096 fp64), with the same
+ * device code that otherwise evaluates the closed form per IMF, and the decomposition then reads the
+ * row of its L instead -- bit-identical results.  enable = 0 frees it.  Resident regime only
+ * (FIF_ERR_UNSUPPORTED_N otherwise; enable = 0 is always accepted).  Synchronises the device.
+ * Errors: FIF_ERR_OOM, FIF_ERR_CUDA. */
+fif_status fif_plan_set_eigen_table(fif_plan_t plan, int32_t enable);
+
 /* Decompose workspace (SURVEY.md §8b "ownership": the caller may own every large device buffer).
  * fif_plan_workspace_bytes: the device scratch the plan's fif_decompose uses beyond the caller's
  *   inputs and outputs, with the current options -- streamed regime: the spectrum ping-pong

@@ -77,6 +77,7 @@ void free_plan(fif_plan_s* p) {
   cudaFree(p->d_sin);
   cudaFree(p->d_isin);
   cudaFree(p->d_tw);
+  cudaFree(p->d_wtab);
   st_free(p);
   dist_free(p);
   for (int i = 0; i < p->nstages; ++i) {
@@ -197,6 +198,31 @@ fif_status fif_plan_set_mask_rule(fif_plan_t p, fif_mask_rule rule) {
       p->mask = old;
       return s;
     }
+  }
+  return FIF_OK;
+}
+
+fif_status fif_plan_set_eigen_table(fif_plan_t p, int32_t enable) {
+  if (!p) return FIF_ERR_INVALID_ARG;
+  if (p->regime != 0) return enable ? FIF_ERR_UNSUPPORTED_N : FIF_OK;
+  if (cudaDeviceSynchronize() != cudaSuccess) return FIF_ERR_CUDA;
+  if (!enable) {
+    cudaFree(p->d_wtab);
+    p->d_wtab = nullptr;
+    return FIF_OK;
+  }
+  if (p->d_wtab) return FIF_OK;
+  const int nL = (int)((p->n - 1) / 4) - 1;  // L = 2 .. floor((n-1)/4) (reading A3)
+  const size_t es = p->dtype == FIF_F64 ? sizeof(double) : sizeof(float);
+  if (cudaMalloc(&p->d_wtab, (size_t)nL * (size_t)(p->NC + 1) * es) != cudaSuccess) {
+    p->d_wtab = nullptr;
+    return FIF_ERR_OOM;
+  }
+  res_ops(p->dtype, p->NC)->fill_wtab(p, p->d_wtab, nL, 0);
+  if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFree(p->d_wtab);
+    p->d_wtab = nullptr;
+    return FIF_ERR_CUDA;
   }
   return FIF_OK;
 }

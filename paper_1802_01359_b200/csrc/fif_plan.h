@@ -41,6 +41,7 @@ struct fif_plan_s {
   void* d_sin = nullptr;   // Real[NC+1]  sin(pi j/n)
   void* d_isin = nullptr;  // Real[NC+1]  1/sin(pi j/n) (j >= 1)
   void* d_tw = nullptr;    // V[twtotal]  Stockham twiddles e^{-2 pi i k r/(NS RP)}
+  void* d_wtab = nullptr;  // Real[(n-1)/4 - 1][NC+1] per-L eigenvalue table (fif_plan_set_eigen_table)
   int block = 0, occ = 0;
   size_t smem = 0;
   int regime = 0;  // 0 resident, 1 streamed
@@ -92,6 +93,7 @@ struct ResOps {
   void (*test_extrema)(const fif_plan_s*, const void*, int32_t*, int64_t, cudaStream_t);
   void (*test_window)(const fif_plan_s*, int, void*, cudaStream_t);
   void (*test_inner)(const fif_plan_s*, int, const void*, void*, int32_t*, int64_t, cudaStream_t);
+  void (*fill_wtab)(const fif_plan_s*, void*, int, cudaStream_t);
 };
 const ResOps* res_ops_f64(int NC);
 const ResOps* res_ops_f32(int NC);

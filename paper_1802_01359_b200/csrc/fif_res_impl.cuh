@@ -29,6 +29,8 @@ struct Inst {
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_wtab_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
     return cudaSuccess;
   }
   static int occupancy() {
@@ -39,6 +41,7 @@ struct Inst {
   static void decompose(const fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
                         int64_t batch, cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
+    prm.wtab = p->d_wtab;
     const int64_t cap = (int64_t)p->num_sms * p->occ;
     const int grid = (int)(batch < cap ? batch : cap);
     if (p->max_inner == kFastCap)
@@ -69,6 +72,9 @@ struct Inst {
     fif_test_window_kernel<Real, NC><<<1, K::T, K::smem_bytes, s>>>((Real*)out, L, (const Real*)p->d_sin,
                                                                         (const Real*)p->d_isin);
   }
+  static void fill_wtab(const fif_plan_s* p, void* tab, int nL, cudaStream_t s) {
+    fif_wtab_kernel<Real, NC><<<nL, K::T, K::smem_bytes, s>>>((Real*)tab, (const Real*)p->d_sin, (const Real*)p->d_isin);
+  }
   static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
                          cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
@@ -88,8 +94,8 @@ struct Inst {
 template <typename Real, int NC>
 const ResOps* res_entry() {
   using I = Inst<Real, NC>;
-  static const ResOps ops{&I::prepare, &I::occupancy, I::K::T, I::K::smem_bytes, &I::decompose, &I::test_rfft,
-                          &I::test_irfft, &I::test_extrema, &I::test_window, &I::test_inner};
+  static const ResOps ops{&I::prepare,    &I::occupancy,  I::K::T,        I::K::smem_bytes, &I::decompose, &I::test_rfft,
+                          &I::test_irfft, &I::test_extrema, &I::test_window, &I::test_inner, &I::fill_wtab};
   return &ops;
 }
 template <typename Real>

@@ -62,6 +62,7 @@ struct Params {
   double delta;     // delta (absolute, for stop = 1)
   double gamma;     // > 0: gamma-threshold variant (A19)
   int32_t mask;     // 0: extrema filter-length rule (A1-A3); 1: spectral-peak rule (A20)
+  const void* wtab = nullptr;  // Real[(n-1)/4 - 1][NC+1]: w_hat per L, nullptr: closed form
 };
 
 // ------------------------------------------------------------------ a5 alternative: a-priori N0
@@ -377,6 +378,7 @@ struct Resident {
 
   struct Smem {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
+    const Real* wtab;  // per-L eigenvalue table (row L - 2, bins 0..NC) or nullptr
   };
 
   // group layout: bin index of spectrum register q for thread j
@@ -672,6 +674,13 @@ struct Resident {
   // block-uniform step B = pi L/8: sin(A + qB) = sA cos qB + cA sin qB (group 1) and
   // sin((q+1)B - A) (group 2, g2 = n/8 - j), so only (sA, cA) are per-thread table gathers.
   __device__ static void bin_w_all(const Smem& sm, int L, Real invL, int j, double (&w)[NB]) {
+    if (sm.wtab) {  // precomputed eigenvalues of this scaling, filled by fif_wtab_kernel
+      const Real* row = sm.wtab + (size_t)(L - 2) * (NC + 1);
+#pragma unroll
+      for (int q = 0; q < R; ++q) w[q] = (double)__ldg(row + bin_of(j, q));
+      w[R] = (double)__ldg(row + NC);
+      return;
+    }
     Real cq[5], sq[5];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {  // qB = pi (qL mod 16) (n/8) / n: uniform addresses (broadcasts)
@@ -1123,6 +1132,7 @@ struct Resident {
     sm.red = reinterpret_cast<double*>(base + off_red);
     sm.nbr = reinterpret_cast<V*>(base + off_nbr);
     sm.ired = reinterpret_cast<int*>(base + off_int);
+    sm.wtab = nullptr;
     return sm;
   }
 
@@ -1146,7 +1156,8 @@ fif_resident_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32
                     const Real* __restrict__ isintab, const typename Cx<Real>::V* __restrict__ tw, Params p) {
   using K = Resident<Real, NC, CAP>;
   extern __shared__ __align__(16) char smem_raw[];
-  const typename K::Smem sm = K::carve(smem_raw);
+  typename K::Smem sm = K::carve(smem_raw);
+  sm.wtab = reinterpret_cast<const Real*>(p.wtab);
   const int j = threadIdx.x;
   K::load_tables(sm, sintab, isintab, j);
   int slot = 0;
@@ -1237,6 +1248,26 @@ __global__ void __launch_bounds__(NC / kR) fif_test_window_kernel(Real* __restri
   K::bin_w_all(sm, L, invL, j, w);
   for (int q = 0; q < kR; ++q) out[K::bin_of(j, q)] = (Real)w[q];
   if (j == 0) out[NC] = (Real)w[kR];
+}
+
+// Per-L eigenvalue table ("computing in advance the eigenvalues ... for every scaling"):
+// row L - 2 = w_hat_k, k = 0..NC, for L = 2 + blockIdx.x, by the very code the kernel evaluates
+// (bin_w_all), so a table-driven decomposition is bit-identical to the closed-form one.
+template <typename Real, int NC>
+__global__ void __launch_bounds__(NC / kR) fif_wtab_kernel(Real* __restrict__ tab, const Real* __restrict__ sintab,
+                                                         const Real* __restrict__ isintab) {
+  using K = Resident<Real, NC>;
+  extern __shared__ __align__(16) char smem_raw[];
+  const typename K::Smem sm = K::carve(smem_raw);
+  const int j = threadIdx.x;
+  K::load_tables(sm, sintab, isintab, j);
+  const int L = 2 + (int)blockIdx.x;
+  const Real invL = (Real)1 / (Real)L;
+  double w[K::NB];
+  K::bin_w_all(sm, L, invL, j, w);
+  Real* row = tab + (size_t)blockIdx.x * (NC + 1);
+  for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = (Real)w[q];
+  if (j == 0) row[NC] = (Real)w[kR];
 }
 
 template <typename Real, int NC, int CAP>

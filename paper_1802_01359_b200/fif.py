@@ -24,7 +24,7 @@ SYMBOLS = ["fif_plan_create", "fif_plan_create_ex", "fif_decompose", "fif_decomp
            "fif_plan_kernels_per_call", "fif_plan_regime", "fif_plan_launch_config", "fif_test_rfft",
            "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner", "fif_nccl_unique_id",
            "fif_plan_create_dist", "fif_plan_create_dist_emulated", "fif_plan_set_options", "fif_plan_set_mask_rule",
-           "fif_plan_workspace_bytes", "fif_plan_set_workspace"]
+           "fif_plan_workspace_bytes", "fif_plan_set_workspace", "fif_plan_set_eigen_table"]
 STOP_SD, STOP_N0 = 0, 1
 MASK_EXTREMA, MASK_SPECTRAL = 0, 1
 
@@ -70,6 +70,7 @@ def lib():
         L.fif_plan_set_mask_rule.argtypes = [vp, ctypes.c_int]
         L.fif_plan_workspace_bytes.argtypes = [vp, ctypes.POINTER(ctypes.c_size_t)]
         L.fif_plan_set_workspace.argtypes = [vp, vp, ctypes.c_size_t]
+        L.fif_plan_set_eigen_table.argtypes = [vp, i32]
         L.fif_plan_create_dist.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32, i32, vp,
                                            i32, i32]
         L.fif_plan_create_dist_emulated.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int, ctypes.c_int, d, d, i32,
@@ -140,6 +141,11 @@ class Plan:
     def set_mask_rule(self, rule=MASK_EXTREMA):
         """fif_plan_set_mask_rule: filter length from the extrema count or the highest spectral peak."""
         _check(lib().fif_plan_set_mask_rule(self._h, int(rule)), "fif_plan_set_mask_rule")
+        return self
+
+    def set_eigen_table(self, enable=True):
+        """fif_plan_set_eigen_table: precompute w_hat for every L (resident regime), or free it."""
+        _check(lib().fif_plan_set_eigen_table(self._h, int(bool(enable))), "fif_plan_set_eigen_table")
         return self
 
     def workspace_bytes(self):

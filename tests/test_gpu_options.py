@@ -133,3 +133,62 @@ def test_spectral_peak_rule_fp32_and_dist_unsupported():
     with pytest.raises(fif.FifError):
         dp.set_mask_rule(fif.MASK_SPECTRAL)
     dp.close()
+
+
+# ------------------------------------------------------------------ per-L eigenvalue table
+@pytest.mark.parametrize("n,dtype", [(1024, "f64"), (4096, "f64"), (8192, "f64"), (4096, "f32"), (16384, "f32")])
+def test_eigen_table_bit_identical(n, dtype):
+    """eigenvalues precomputed for every scaling L; the table is filled by the kernel's own
+    window code, so the decomposition must not change by a single bit (64 signals: many distinct L)."""
+    B = 64
+    s = np.stack([signals.tones_signal(n, 41, i) for i in range(B)])
+    td = torch.float64 if dtype == "f64" else torch.float32
+    x = torch.from_numpy(s).to(td).cuda()
+    outs = []
+    for eig in (False, True):
+        plan = fif.Plan(n, B, dtype)
+        assert plan.launch_config()["regime"] == "resident"
+        if eig:
+            plan.set_eigen_table(True)
+        out = plan.alloc_outputs()
+        plan.decompose(x, *out)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in out])
+        plan.close()
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    assert len(set(outs[0][2].ravel().tolist())) > 8  # many filter lengths exercised
+
+
+def test_eigen_table_with_options_and_toggle():
+    n, B = 4096, 32
+    s = signals.make_batch("cfg1", batch=B, start=700)
+    x = torch.from_numpy(s).cuda()
+    for stop, gamma, mask in ((fif.STOP_N0, 0.0, fif.MASK_EXTREMA), (fif.STOP_SD, 0.05, fif.MASK_EXTREMA),
+                              (fif.STOP_SD, 0.0, fif.MASK_SPECTRAL)):
+        res = []
+        for eig in (False, True, False):
+            plan = fif.Plan(n, B, "f64", delta=20.0 if stop == fif.STOP_N0 else 1e-3)
+            plan.set_options(stop=stop, gamma=gamma).set_mask_rule(mask)
+            if eig:
+                plan.set_eigen_table(True)
+            out = plan.alloc_outputs()
+            plan.decompose(x, *out)
+            if eig:  # toggled off again: back to the closed form
+                plan.set_eigen_table(False)
+                out2 = plan.alloc_outputs()
+                plan.decompose(x, *out2)
+                torch.cuda.synchronize()
+                for a, b in zip(out, out2):
+                    assert torch.equal(a, b)
+            torch.cuda.synchronize()
+            res.append([t.cpu().numpy() for t in out])
+            plan.close()
+        for a, b in zip(res[0], res[1]):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_eigen_table_regimes():
+    st = fif.Plan(16384, 2, "f64", regime=fif.REGIME_STREAMED)
+    assert fif.lib().fif_plan_set_eigen_table(st.handle, 1) == 2
+    assert fif.lib().fif_plan_set_eigen_table(st.handle, 0) == 0

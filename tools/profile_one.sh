@@ -14,7 +14,7 @@ case "$1" in
     ncu $LM -s 76 -c 76 --log-file $O/launches_cfg3.csv python tools/run_plan.py --config cfg3 --reps 2 > $O/ncu_l3.log 2>&1 ;;
   full1) python tools/run_plan.py --config cfg1 --reps 1 > $O/plain1.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:fif_resident_kernel -s 1 -c 1 -o $O/full_resident \
-      python tools/run_plan.py --config cfg1 --reps 2 > $O/ncu_f1.log 2>&1 ;;
+      python tools/run_plan.py --config cfg1 --reps 2 --eig > $O/ncu_f1.log 2>&1 ;;
   full2) python tools/run_plan.py --config cfg2 --reps 1 > $O/plain2.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:"k_col|k_rows_inv" -s 3 -c 2 -o $O/full_cfg2 \
       python tools/run_plan.py --config cfg2 --reps 1 > $O/ncu_f2.log 2>&1 ;;

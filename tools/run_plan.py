@@ -19,6 +19,7 @@ ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--regime", type=int, default=0)
+ap.add_argument("--eig", action="store_true", help="per-L eigenvalue table (fif_plan_set_eigen_table)")
 a = ap.parse_args()
 if a.config == "cfg4":
     s = signals.make_batch("cfg4", batch=a.batch or 64, n=a.n)
@@ -31,6 +32,8 @@ else:
         s = np.concatenate([s] * ((B + s.shape[0] - 1) // s.shape[0]))[:B]
     dtype, delta = c["dtype"], c["delta"]
 plan = fif.Plan(s.shape[1], s.shape[0], dtype, delta=delta, regime=a.regime)
+if a.eig:
+    plan.set_eigen_table(True)
 x = torch.from_numpy(np.ascontiguousarray(s)).cuda()
 out = plan.alloc_outputs()
 for r in range(a.reps):
