@@ -32,9 +32,11 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
-def run_gpu(s, dtype="f64", **kw):
+def run_gpu(s, dtype="f64", eig=False, **kw):
     s = np.ascontiguousarray(s)
     plan = fif.Plan(s.shape[1], s.shape[0], dtype, **kw)
+    if eig:  # the per-L eigenvalue table, as bench.py runs resident plans
+        plan.set_eigen_table(True)
     x = torch.from_numpy(s).cuda()
     out = plan.alloc_outputs()
     plan.decompose(x, *out)
@@ -194,10 +196,11 @@ def test_cfg0_noise_free_integers():
 
 
 def test_cfg1_sampled_full_batch():
-    """Config 1 at its full size (4096 x 4096 fp64, the bench launch), 24 sampled signals vs the TD oracle."""
+    """Config 1 at its full size (4096 x 4096 fp64, the bench launch: per-L eigenvalue table on), 24 sampled
+    signals vs the TD oracle."""
     B = 4096
     s = signals.make_batch("cfg1", batch=B)
-    gpu = run_gpu(s)
+    gpu = run_gpu(s, eig=True)
     idx = np.linspace(0, B - 1, 24).astype(int)
     ref = oracle.decompose(s[idx])
     worst = 0.0
