@@ -290,6 +290,52 @@ __device__ V* cta_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict
   return a;
 }
 
+// The same passes with the row length, its radix schedule (radices() in fif_st.cu: 1024 = 4 16 16,
+// 2048 = 8 16 16) and the swizzled pitch known at compile time: identical arithmetic, constant index math.
+template <int P, int DIR, typename V, int F, int NS>
+__device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const V* __restrict__ tw) {
+  constexpr int per = F / P, tstride = F / (NS * P);
+  for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
+    const int f = idx / per, vt = idx % per, k = vt % NS;
+    V x[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) x[r] = src[sidx<V>(f, vt + r * per, F, 1)];
+    if constexpr (NS > 1) {
+      const int kt = k * tstride;
+#pragma unroll
+      for (int r = 1; r < P; ++r) {
+        V t = tw[r * kt];
+        if (DIR > 0) t.y = -t.y;
+        x[r] = cmul(x[r], t);
+      }
+    }
+    dft_small<P, DIR>(x);
+    const int j0 = (vt - k) * P + k;
+#pragma unroll
+    for (int r = 0; r < P; ++r) dst[sidx<V>(f, j0 + r * NS, F, 1)] = x[r];
+  }
+}
+template <int DIR, typename V, int F, int R0>
+__device__ __forceinline__ V* cta_fft_c(V* a, V* b, int cols, const V* __restrict__ tw) {
+  __syncthreads();
+  cta_pass_c<R0, DIR, V, F, 1>(a, b, cols, tw);
+  __syncthreads();
+  cta_pass_c<16, DIR, V, F, R0>(b, a, cols, tw);
+  __syncthreads();
+  cta_pass_c<16, DIR, V, F, R0 * 16>(a, b, cols, tw);
+  __syncthreads();
+  return b;
+}
+// Row transforms: the compile-time path for the full-length rows (every benchmark configuration), the
+// generic passes otherwise.
+template <int DIR, typename V>
+__device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
+  constexpr int FR = sizeof(V) == 16 ? 1024 : 2048, R0 = sizeof(V) == 16 ? 4 : 8;
+  if (lv.F == FR && lv.swz && lv.pitch == FR && lv.np == 3 && lv.rad[0] == R0 && lv.rad[1] == 16 && lv.rad[2] == 16)
+    return cta_fft_c<DIR, V, FR, R0>(a, b, cols, tw + lv.twoff);
+  return cta_fft<DIR>(a, b, lv, cols, tw);
+}
+
 // ------------------------------------------------------------------ tables
 // E(j) = e^{i pi j/n}, 0 <= j <= 2n, from the two-level table (one complex product)
 __device__ __forceinline__ double2 E64(const double2* __restrict__ Eh, const double2* __restrict__ El, int eb,
@@ -949,7 +995,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
         }
       }
     }
-    V* out = cta_fft<-1>(A, Bf, lv, two ? 2 : 1, tb.tw);
+    V* out = row_fft<-1>(A, Bf, lv, two ? 2 : 1, tb.tw);
     V* stage = out == A ? Bf : A;
     const int cb = two ? 1 : 0;
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
@@ -1108,7 +1154,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
         sred[threadIdx.x >> 5][1] = sQ;
       }
     }
-    V* out = cta_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);  // (its first barrier also publishes sred)
+    V* out = row_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);  // (its first barrier also publishes sred)
     V* W = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
     // the next (coarser) level's conjugate twiddle e^{+2 pi i s k'/(F' S')}: s = element, k' = row mod F'
     // (geometric in i: two table products per row and thread, one multiply per element)
