@@ -315,24 +315,47 @@ __device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const
     for (int r = 0; r < P; ++r) dst[sidx<V>(f, j0 + r * NS, F, 1)] = x[r];
   }
 }
-template <int DIR, typename V, int F, int R0>
+template <int DIR, typename V, int F, int NS, int P, int... Rest>
 __device__ __forceinline__ V* cta_fft_c(V* a, V* b, int cols, const V* __restrict__ tw) {
   __syncthreads();
-  cta_pass_c<R0, DIR, V, F, 1>(a, b, cols, tw);
-  __syncthreads();
-  cta_pass_c<16, DIR, V, F, R0>(b, a, cols, tw);
-  __syncthreads();
-  cta_pass_c<16, DIR, V, F, R0 * 16>(a, b, cols, tw);
-  __syncthreads();
-  return b;
+  cta_pass_c<P, DIR, V, F, NS>(a, b, cols, tw);
+  if constexpr (sizeof...(Rest) == 0) {
+    __syncthreads();
+    return b;
+  } else {
+    return cta_fft_c<DIR, V, F, NS * P, Rest...>(b, a, cols, tw);
+  }
+}
+template <int F, int... R>
+__device__ __forceinline__ bool sched_is(const Level& lv) {
+  constexpr int r[] = {R...};
+  if (lv.F != F || !lv.swz || lv.pitch != F || lv.np != (int)sizeof...(R)) return false;
+  for (int i = 0; i < (int)sizeof...(R); ++i)
+    if (lv.rad[i] != r[i]) return false;
+  return true;
 }
 // Row transforms: the compile-time path for the full-length rows (every benchmark configuration), the
 // generic passes otherwise.
 template <int DIR, typename V>
 __device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
-  constexpr int FR = sizeof(V) == 16 ? 1024 : 2048, R0 = sizeof(V) == 16 ? 4 : 8;
-  if (lv.F == FR && lv.swz && lv.pitch == FR && lv.np == 3 && lv.rad[0] == R0 && lv.rad[1] == 16 && lv.rad[2] == 16)
-    return cta_fft_c<DIR, V, FR, R0>(a, b, cols, tw + lv.twoff);
+  if constexpr (sizeof(V) == 16) {
+    if (sched_is<1024, 4, 16, 16>(lv)) return cta_fft_c<DIR, V, 1024, 1, 4, 16, 16>(a, b, cols, tw + lv.twoff);
+  } else {
+    if (sched_is<2048, 8, 16, 16>(lv)) return cta_fft_c<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw + lv.twoff);
+  }
+  return cta_fft<DIR>(a, b, lv, cols, tw);
+}
+// Column transforms: compile-time paths for the fp32 column lengths of the benchmark geometries
+// (radices() order; measured: -2% on config 4, while the fp64 column kernels spill more and lose 5%),
+// the generic passes otherwise.  tw: the level's twiddles (already offset).
+template <int DIR, typename V>
+__device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
+  if constexpr (sizeof(V) == 8) {
+    if (sched_is<32, 8, 4>(lv)) return cta_fft_c<DIR, V, 32, 1, 8, 4>(a, b, cols, tw);
+    if (sched_is<64, 4, 16>(lv)) return cta_fft_c<DIR, V, 64, 1, 4, 16>(a, b, cols, tw);
+    if (sched_is<128, 8, 16>(lv)) return cta_fft_c<DIR, V, 128, 1, 8, 16>(a, b, cols, tw);
+    if (sched_is<256, 16, 16>(lv)) return cta_fft_c<DIR, V, 256, 1, 16, 16>(a, b, cols, tw);
+  }
   return cta_fft<DIR>(a, b, lv, cols, tw);
 }
 
@@ -815,7 +838,7 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         }
       }
     }
-    V* out = cta_fft<DIR>(In, Sc, lvs, lv.C, tws);
+    V* out = col_fft<DIR>(In, Sc, lvs, lv.C, tws);
     if (KIND == PASS_INV_LAST) {
       V* stage = out == In ? Sc : In;
 #pragma unroll
