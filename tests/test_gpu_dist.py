@@ -26,10 +26,12 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
-def run_dist(s, P, dtype="f64", **kw):
+def run_dist(s, P, dtype="f64", stop=fif.STOP_SD, gamma=0.0, **kw):
     """Decompose ONE signal s [n] with the emulated P-rank plan; returns the run_gpu layout for batch 1."""
     n = s.shape[0]
     plan = fif.Plan.dist(n, 0, P, dtype=dtype, emulated=True, **kw)
+    if stop != fif.STOP_SD or gamma != 0.0:
+        plan.set_options(stop, gamma)
     x = torch.from_numpy(np.ascontiguousarray(s.reshape(P, n // P))).cuda()
     imfs, count, lens, iters = plan.alloc_outputs()
     plan.decompose(x, imfs, count, lens, iters)
