@@ -361,9 +361,9 @@ __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, con
 
 // ------------------------------------------------------------------ tables
 // E(j) = e^{i pi j/n}, 0 <= j <= 2n, from the two-level table (one complex product)
-__device__ __forceinline__ double2 E64(const double2* __restrict__ Eh, const double2* __restrict__ El, int eb,
-                                       int64_t j) {
-  return cmul(__ldg(Eh + (j >> eb)), __ldg(El + (j & ((1LL << eb) - 1))));
+template <typename I = int64_t>
+__device__ __forceinline__ double2 E64(const double2* __restrict__ Eh, const double2* __restrict__ El, int eb, I j) {
+  return cmul(__ldg(Eh + (j >> eb)), __ldg(El + (j & (((I)1 << eb) - 1))));
 }
 // sin(pi j/n) for 0 <= j <= n/2: both table angles lie in the first quadrant, so the imaginary part
 // of the product is a sum of two non-negative terms (relative error ~2 ulp)
@@ -401,10 +401,10 @@ __device__ __forceinline__ int64_t mod_n(int64_t x, int64_t n, double invn) {
 // |cos(pi mk/n)| (L odd).  A cosine near zero carries a larger relative error, but it then belongs
 // to a bin whose w_hat is tiny or whose a^N vanishes, so the absolute error of a^N stays at
 // rounding level (|d a^N| <= N a^{N-1} |d w| <= |d w / w| / e).  Returns e^{i pi k/n} in Ek.
-template <typename Real>
-__device__ __forceinline__ void what_pair_m(const Geo& g, const Tabs<Real>& tb, int L, int64_t k, int64_t mk,
+template <typename Real, typename I = int64_t>
+__device__ __forceinline__ void what_pair_m(const Geo& g, const Tabs<Real>& tb, int L, I k, I mk,
                                             double& wk, double& wm, double2& Ek) {
-  const int64_t rk = mk <= g.NC ? mk : g.n - mk;
+  const I rk = mk <= (I)g.NC ? mk : (I)g.n - mk;
   Ek = E64(tb.Eh, tb.El, g.eb, k);                 // (cos, sin)(pi k/n), first quadrant
   const double2 Er_ = E64(tb.Eh, tb.El, g.eb, rk);  // (cos, sin)(pi rk/n), first quadrant
   const double nk = Er_.y, nm = (L & 1) ? fabs(Er_.x) : Er_.y;
@@ -1110,12 +1110,14 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
     const int cb = two ? 1 : 0;
     double sP = 0.0, sQ = 0.0;
     // L k mod n, advanced by L P blockDim per iteration
-    int64_t mk = mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
-    const int64_t mstep = mod_n((int64_t)L * ((g.P * blockDim.x) % g.n), g.n, invn);
-    for (int i = threadIdx.x; i < F; i += blockDim.x, mk = (mk + mstep >= g.n) ? mk + mstep - g.n : mk + mstep) {
+    // 32-bit bin arithmetic (n <= 2^27: k, L k mod n and mk + mstep < 2^31)
+    const int n32 = (int)g.n, P32 = (int)g.P, bA32 = (int)bA;
+    int mk = (int)mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
+    const int mstep = (int)mod_n((int64_t)L * ((g.P * blockDim.x) % g.n), g.n, invn);
+    for (int i = threadIdx.x; i < F; i += blockDim.x, mk = (mk + mstep >= n32) ? mk + mstep - n32 : mk + mstep) {
       int tm;
       if (!mirror_t(g, bA, two, F, i, tm)) continue;
-      const int64_t k = bA + g.P * i;
+      const int k = bA32 + P32 * i;
       const V xk = A[sidx<V>(0, i, lv.pitch, lv.swz)];
       const V xm = k == 0 ? Xnin[b] : A[sidx<V>(cb, tm, lv.pitch, lv.swz)];
       double wk, wm;
@@ -1297,14 +1299,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ G
         xmv[j] = (bA == 0 && i == 0) ? Xn[b] : Xb[(two ? rb : ra) * F + tm];
       }
     }
-    int64_t mk = mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
-    const int64_t mstep = mod_n((int64_t)L * ((g.P * kThreads) % g.n), g.n, invn);
+    const int n32 = (int)g.n, P32 = (int)g.P, bA32 = (int)bA;  // 32-bit bin arithmetic (n <= 2^27)
+    int mk = (int)mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
+    const int mstep = (int)mod_n((int64_t)L * ((g.P * kThreads) % g.n), g.n, invn);
 #pragma unroll
-    for (int j = 0; j < UR; ++j, mk = (mk + mstep >= g.n) ? mk + mstep - g.n : mk + mstep) {
+    for (int j = 0; j < UR; ++j, mk = (mk + mstep >= n32) ? mk + mstep - n32 : mk + mstep) {
       const int i = threadIdx.x + j * kThreads;
       int tm;
       if (i >= F || !mirror_t(g, bA, two, F, i, tm)) continue;
-      const int64_t k = bA + g.P * i;
+      const int k = bA32 + P32 * i;
       const V xk = xkv[j];
       const V xm = xmv[j];
       double wk, wm;
