@@ -46,6 +46,9 @@ constexpr int kNW = kThreads / 32;
 #define FIF_COL_THREADS 256
 #endif
 constexpr int kColThreads = FIF_COL_THREADS;  // block size of the column passes
+#ifndef FIF_PROBE1_MINB
+#define FIF_PROBE1_MINB 2  // K-ary probe kernel: 30 fp64 accumulators per thread -> a 128-register budget
+#endif
 #ifndef FIF_ST_MINB
 #define FIF_ST_MINB 3  // resident CTAs per SM the heavy streamed kernels are register-budgeted for
 #endif
@@ -1253,7 +1256,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
 // One CTA per row-pair unit (both bins of every Hermitian pair share one window evaluation); the
 // last CTA of a signal folds the unit partials (fixed order) and decides.
 template <typename Real, int CAP, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_probe(const __grid_constant__ Geo g,
+__global__ void __launch_bounds__(kThreads, MODE == 1 ? FIF_PROBE1_MINB : 3) k_probe(const __grid_constant__ Geo g,
                                                        const typename Cx<Real>::V* __restrict__ X,
                                                        const typename Cx<Real>::V* __restrict__ Xn,
                                                        const __grid_constant__ Tabs<Real> tb,
