@@ -22,9 +22,17 @@ bool smooth235(int64_t x) {
 }
 // radix schedule: powers of two in radix-16 passes, the remainder as one radix-4 or -8 pass (two 8s
 // instead of 16 x 2), then 3s and 5s
-int radices(int64_t N, int* rad) {
+int radices(int64_t N, int* rad, int maxr) {
   int np = 0, a = 0;
   while (N % 2 == 0) { N /= 2; ++a; }
+  if (maxr == 8) {  // radix 2 or 4 first, then 8s
+    if (a % 3 == 1) { rad[np++] = 2; a -= 1; }
+    if (a % 3 == 2) { rad[np++] = 4; a -= 2; }
+    while (a >= 3) { rad[np++] = 8; a -= 3; }
+    while (N % 3 == 0) { N /= 3; rad[np++] = 3; }
+    while (N % 5 == 0) { N /= 5; rad[np++] = 5; }
+    return np;
+  }
   if (a % 4 == 1 && a >= 5) { rad[np++] = 8; rad[np++] = 4; a -= 5; }
   else if (a % 4 == 1) { rad[np++] = 2; a -= 1; }
   if (a % 4 == 2) { rad[np++] = 4; a -= 2; }
@@ -79,7 +87,7 @@ bool st_geometry(int64_t n, bool f64, st::Geo& g) {
         lv.S = S;
         lv.A = NC / (F[i] * S);
         lv.E2 = 2 * n / (F[i] * S);
-        lv.np = radices(F[i], lv.rad);
+        lv.np = radices(F[i], lv.rad, (f64 && i < L - 1) ? 8 : 16);  // fp64 columns: no radix 16
         lv.twoff = twoff;
         twoff += lv.F;
         if (i < L - 1) {

@@ -266,7 +266,7 @@ __device__ void cta_pass_t(const V* src, V* dst, int Ns, int cols, int pitch, in
     for (int r = 0; r < P; ++r) dst[sidx<V>(f, j0 + r * NS, pitch, swz)] = x[r];
   }
 }
-template <int DIR, typename V>
+template <int DIR, typename V, int MAXR = 16>
 __device__ __forceinline__ void cta_pass(const V* src, V* dst, int Ns, int cols, int pitch, int swz, int p, int NS,
                                          const V* __restrict__ tw) {
   switch (p) {
@@ -275,17 +275,21 @@ __device__ __forceinline__ void cta_pass(const V* src, V* dst, int Ns, int cols,
     case 4: cta_pass_t<4, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
     case 5: cta_pass_t<5, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
     case 8: cta_pass_t<8, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
-    default: cta_pass_t<16, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw); break;
+    default:
+      if constexpr (MAXR >= 16) cta_pass_t<16, DIR>(src, dst, Ns, cols, pitch, swz, NS, tw);
+      break;
   }
 }
 
-// All passes of a level; a holds the input, returns the buffer holding the output (a or b).
-template <int DIR, typename V>
+// All passes of a level; a holds the input, returns the buffer holding the output (a or b).  MAXR = 8:
+// the level's schedule has no radix-16 pass (fp64 column levels, radices(..., 8)), so its 64-register
+// butterfly is not compiled into the caller.
+template <int DIR, typename V, int MAXR = 16>
 __device__ V* cta_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
   int NS = 1;
   for (int ps = 0; ps < lv.np; ++ps) {
     __syncthreads();
-    cta_pass<DIR>(a, b, lv.F, cols, lv.pitch, lv.swz, lv.rad[ps], NS, tw + lv.twoff);
+    cta_pass<DIR, V, MAXR>(a, b, lv.F, cols, lv.pitch, lv.swz, lv.rad[ps], NS, tw + lv.twoff);
     NS *= lv.rad[ps];
     V* t = a; a = b; b = t;
   }
@@ -360,8 +364,10 @@ __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, con
     if (sched_is<64, 4, 16>(lv)) return cta_fft_c<DIR, V, 64, 1, 4, 16>(a, b, cols, tw);
     if (sched_is<128, 8, 16>(lv)) return cta_fft_c<DIR, V, 128, 1, 8, 16>(a, b, cols, tw);
     if (sched_is<256, 16, 16>(lv)) return cta_fft_c<DIR, V, 256, 1, 16, 16>(a, b, cols, tw);
+    return cta_fft<DIR>(a, b, lv, cols, tw);
+  } else {
+    return cta_fft<DIR, V, 8>(a, b, lv, cols, tw);
   }
-  return cta_fft<DIR>(a, b, lv, cols, tw);
 }
 
 // ------------------------------------------------------------------ tables
