@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_d_pass(const __grid_c
         A[st::sidx<V>(cc, f, lv.pitch, lv.swz)] = x;
       }
     }
-    V* out = st::cta_fft<DIR>(A, Bf, lv, lv.C, tb.tw);
+    V* out = st::cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(A, Bf, lv, lv.C, tb.tw);  // fp64 levels: radix <= 8
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int i = threadIdx.x + j * kThreads;

@@ -87,7 +87,7 @@ bool st_geometry(int64_t n, bool f64, st::Geo& g) {
         lv.S = S;
         lv.A = NC / (F[i] * S);
         lv.E2 = 2 * n / (F[i] * S);
-        lv.np = radices(F[i], lv.rad, (f64 && i < L - 1) ? 8 : 16);  // fp64 columns: no radix 16
+        lv.np = radices(F[i], lv.rad, f64 ? 8 : 16);  // fp64: no radix 16 (register budget, see cta_fft)
         lv.twoff = twoff;
         twoff += lv.F;
         if (i < L - 1) {

@@ -282,7 +282,7 @@ __device__ __forceinline__ void cta_pass(const V* src, V* dst, int Ns, int cols,
 }
 
 // All passes of a level; a holds the input, returns the buffer holding the output (a or b).  MAXR = 8:
-// the level's schedule has no radix-16 pass (fp64 column levels, radices(..., 8)), so its 64-register
+// the level's schedule has no radix-16 pass (fp64 geometries, radices(..., 8)), so its 64-register
 // butterfly is not compiled into the caller.
 template <int DIR, typename V, int MAXR = 16>
 __device__ V* cta_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
@@ -346,9 +346,10 @@ __device__ __forceinline__ bool sched_is(const Level& lv) {
 template <int DIR, typename V>
 __device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
   if constexpr (sizeof(V) == 16) {
-    // fp64: 16 8 8 rather than radices()' 4 16 16 -- one radix-16 pass of 64 live doubles instead of two
-    // (fewer spills at the 3-CTA register budget; measured -1.5% on configs 2 and 3)
-    if (lv.F == 1024 && lv.swz && lv.pitch == 1024) return cta_fft_c<DIR, V, 1024, 1, 16, 8, 8>(a, b, cols, tw + lv.twoff);
+    // fp64: radix <= 8 everywhere (radices(..., 8)): the 64-register radix-16 butterfly is never compiled
+    // into an fp64 streamed kernel (spills at the 3-CTA register budget; measured -1.3% on configs 2 and 3)
+    if (sched_is<1024, 2, 8, 8, 8>(lv)) return cta_fft_c<DIR, V, 1024, 1, 2, 8, 8, 8>(a, b, cols, tw + lv.twoff);
+    return cta_fft<DIR, V, 8>(a, b, lv, cols, tw);
   } else {
     if (sched_is<2048, 8, 16, 16>(lv)) return cta_fft_c<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw + lv.twoff);
   }
