@@ -1012,14 +1012,16 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
     V* Xb = X + b * g.NC;
     {
       constexpr int UR = TileCap<Real>::value / 2 / kThreads;
+      // the mirror row is loaded unconditionally (the row itself when there is none): a conditionally
+      // assigned register array is kept in local memory, which serialises the loads behind its spills
+      const int64_t rbb = two ? rb : ra;
       V xa[UR], xb[UR];
 #pragma unroll
       for (int j = 0; j < UR; ++j) {
         const int i = threadIdx.x + j * kThreads;
-        if (i < F) {
-          xa[j] = Xb[ra * F + i];
-          if (two) xb[j] = Xb[rb * F + i];
-        }
+        const int ic = i < F ? i : 0;
+        xa[j] = Xb[ra * F + ic];
+        xb[j] = Xb[rbb * F + ic];
       }
 #pragma unroll
       for (int j = 0; j < UR; ++j) {
@@ -1100,14 +1102,16 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
     V* Xo = Xout + b * g.NC;
     {
       constexpr int UR = TileCap<Real>::value / 2 / kThreads;
+      // the mirror row is loaded unconditionally (the row itself when there is none): a conditionally
+      // assigned register array is kept in local memory, which serialises the loads behind its spills
+      const int64_t rbb = two ? rb : ra;
       V xa[UR], xb[UR];
 #pragma unroll
       for (int j = 0; j < UR; ++j) {
         const int i = threadIdx.x + j * kThreads;
-        if (i < F) {
-          xa[j] = Xb[ra * F + i];
-          if (two) xb[j] = Xb[rb * F + i];
-        }
+        const int ic = i < F ? i : 0;
+        xa[j] = Xb[ra * F + ic];
+        xb[j] = Xb[rbb * F + ic];
       }
 #pragma unroll
       for (int j = 0; j < UR; ++j) {
