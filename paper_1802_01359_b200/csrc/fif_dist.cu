@@ -110,13 +110,11 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_d_pass(const __grid_c
     constexpr int U = st::TileCap<Real>::value / kThreads;
     V v[U];
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
+    for (int j = 0; j < U; ++j) {  // unconditional (clamped) loads keep v[] in registers
       const int i = threadIdx.x + j * kThreads;
-      if (i < FC) {
-        int f, cc;
-        st::tile_fc(lv, i, f, cc);
-        v[j] = buf[base + (int64_t)f * lv.S + cc];
-      }
+      int f, cc;
+      st::tile_fc(lv, i < FC ? i : 0, f, cc);
+      v[j] = buf[base + (int64_t)f * lv.S + cc];
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {

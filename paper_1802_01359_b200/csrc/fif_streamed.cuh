@@ -839,15 +839,13 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         tile_segments<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     }
     V r[KIND == PASS_INV_LAST ? U : 1];
-    if (KIND == PASS_INV_LAST) {  // remainder loads in flight during the transform
+    if (KIND == PASS_INV_LAST) {  // remainder loads in flight during the transform (clamped: no local array)
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int i = threadIdx.x + j * kColThreads;
-        if (i < FC) {
-          int f, cc;
-          tile_fc(lv, i, f, cc);
-          r[j] = reinterpret_cast<const V*>(Rb)[cur.base + (int64_t)f * lv.S + cc];
-        }
+        int f, cc;
+        tile_fc(lv, i < FC ? i : 0, f, cc);
+        r[j] = reinterpret_cast<const V*>(Rb)[cur.base + (int64_t)f * lv.S + cc];
       }
     }
     V* out = col_fft<DIR>(In, Sc, lvs, lv.C, tws);
@@ -1307,13 +1305,14 @@ __global__ void __launch_bounds__(kThreads, MODE == 1 ? FIF_PROBE1_MINB : 3) k_p
     constexpr int UR = TileCap<Real>::value / 2 / kThreads;
     V xkv[UR], xmv[UR];
 #pragma unroll
-    for (int j = 0; j < UR; ++j) {
+    for (int j = 0; j < UR; ++j) {  // unconditional loads (clamped indices): the arrays stay in registers
       const int i = threadIdx.x + j * kThreads;
+      const int ic = i < F ? i : 0;
       int tm;
-      if (i < F && mirror_t(g, bA, two, F, i, tm)) {
-        xkv[j] = Xb[ra * F + i];
-        xmv[j] = (bA == 0 && i == 0) ? Xn[b] : Xb[(two ? rb : ra) * F + tm];
-      }
+      mirror_t(g, bA, two, F, ic, tm);
+      xkv[j] = Xb[ra * F + ic];
+      xmv[j] = Xb[(two ? rb : ra) * F + tm];
+      if (bA == 0 && ic == 0) xmv[j] = Xn[b];
     }
     const int n32 = (int)g.n, P32 = (int)g.P, bA32 = (int)bA;  // 32-bit bin arithmetic (n <= 2^27)
     int mk = (int)mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
