@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kThreads) k_d_post(const __grid_constant__ DGe
 
 // ---------------------------------------------------------------- a5 probes (local sums + rank fold)
 template <typename Real, int CAP, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_d_probe(const __grid_constant__ DGeo d,
+__global__ void __launch_bounds__(kThreads, MODE == 1 ? FIF_PROBE1_MINB : 3) k_d_probe(const __grid_constant__ DGeo d,
                                                          const typename Cx<Real>::V* __restrict__ X,
                                                          const typename Cx<Real>::V* __restrict__ Xm,
                                                          const __grid_constant__ Tabs<Real> tb, DCtl c) {
