@@ -73,6 +73,7 @@ struct fif_plan_s {
   cudaStream_t st_streams[2] = {nullptr, nullptr};  // waves alternate between these
   cudaEvent_t st_ev[3] = {nullptr, nullptr, nullptr};
   size_t st_smem_col[fifgpu::st::kMaxLev] = {}, st_smem_rows = 0;
+  int st_col_cs[fifgpu::st::kMaxLev] = {};  // column transform path per level (st::col_fft CS)
   // host (e2e) path staging
   int64_t chunk = 0;
   int nstages = 0;

@@ -204,6 +204,53 @@ int occ_grid(const fif_plan_s* p, K kern, size_t smem) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, st::kThreads, smem);
   return p->num_sms * (occ > 0 ? occ : 1);
 }
+// the k_col instance for a column level: its compile-time transform path (st::col_fft CS), 0 = generic
+static int col_schedule(const st::Level& lv, bool f64) {
+  auto is = [&](int F, std::initializer_list<int> r) {
+    if (lv.F != F || !lv.swz || lv.pitch != F || lv.np != (int)r.size()) return false;
+    int i = 0;
+    for (int x : r)
+      if (lv.rad[i++] != x) return false;
+    return true;
+  };
+  if (!f64) {
+    if (is(32, {8, 4})) return 1;
+    if (is(64, {4, 16})) return 2;
+    if (is(128, {8, 16})) return 3;
+    if (is(256, {16, 16})) return 4;
+  } else {
+    if (is(128, {2, 8, 8})) return 5;
+    if (is(256, {4, 8, 8})) return 6;
+  }
+  return 0;
+}
+template <typename Real, int DIR, int KIND, typename F>
+static void for_col_instances(F&& f) {
+  f(st::k_col<Real, DIR, KIND, 0>);
+  if constexpr (sizeof(Real) == 4) {
+    f(st::k_col<Real, DIR, KIND, 1>);
+    f(st::k_col<Real, DIR, KIND, 2>);
+    f(st::k_col<Real, DIR, KIND, 3>);
+    f(st::k_col<Real, DIR, KIND, 4>);
+  } else {
+    f(st::k_col<Real, DIR, KIND, 5>);
+    f(st::k_col<Real, DIR, KIND, 6>);
+  }
+}
+template <typename Real, int DIR, int KIND, typename... A>
+static void launch_col(int cs, int grid, size_t smem, cudaStream_t s, A... a) {
+  switch (cs) {
+    case 1: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 1><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 2: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 2><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 3: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 3><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 4: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 4><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 5: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 5><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 6: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 6><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    default: break;
+  }
+  st::k_col<Real, DIR, KIND, 0><<<grid, st::kColThreads, smem, s>>>(a...);
+}
+
 template <typename Real>
 fif_status st_setup_t(fif_plan_s* p) {
   using V = typename Cx<Real>::V;
@@ -254,10 +301,11 @@ fif_status st_setup_t(fif_plan_s* p) {
   auto attr = [&](auto kern) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
   };
-  attr(st::k_col<Real, -1, st::PASS_FWD_FIRST>);
-  attr(st::k_col<Real, -1, st::PASS_MID>);
-  attr(st::k_col<Real, 1, st::PASS_MID>);
-  attr(st::k_col<Real, 1, st::PASS_INV_LAST>);
+  for_col_instances<Real, -1, st::PASS_FWD_FIRST>(attr);
+  for_col_instances<Real, -1, st::PASS_MID>(attr);
+  for_col_instances<Real, 1, st::PASS_MID>(attr);
+  for_col_instances<Real, 1, st::PASS_INV_LAST>(attr);
+  for (int i = 0; i < g.L - 1; ++i) p->st_col_cs[i] = col_schedule(g.lv[i], sizeof(Real) == 8);
   attr(st::k_rows_fwd<Real>);
   attr(st::k_rows_inv<Real, 0, 0>);
   attr(st::k_rows_inv<Real, kFastCap, 0>);
@@ -344,10 +392,10 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     const int gsig = (int)((g.batch + TB - 1) / TB);
     auto col = [&](int i) { return grid_for(g.batch * g.lv[i].tiles, gcol); };
     st::k_init<<<gsig, TB, 0, s>>>(g, c);
-    st::k_col<Real, -1, st::PASS_FWD_FIRST><<<col(0), st::kColThreads, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+    launch_col<Real, -1, st::PASS_FWD_FIRST>(p->st_col_cs[0], col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
     st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
     for (int i = 1; i < Lv - 1; ++i)
-      st::k_col<Real, -1, st::PASS_MID><<<col(i), st::kColThreads, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i], sg, out, X, tb, c);
+      launch_col<Real, -1, st::PASS_MID>(p->st_col_cs[i], col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i], sg, out, X, tb, c);
     st::k_rows_fwd<Real><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     auto peaks = [&](const V* Xs, const V* Xns) {  // spectral-peak rule: L for the next IMF
       if (!g.mask) return;
@@ -385,8 +433,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
         if (fast) rows(F0{}, FC{}, 0); else rows(F0{}, F0{}, 0);
       }
       for (int i = Lv - 2; i >= 1; --i)
-        st::k_col<Real, 1, st::PASS_MID><<<col(i), st::kColThreads, p->st_smem_col[i], s>>>(g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
-      st::k_col<Real, 1, st::PASS_INV_LAST><<<col(0), st::kColThreads, p->st_smem_col[0], s>>>(g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+        launch_col<Real, 1, st::PASS_MID>(p->st_col_cs[i], col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
+      launch_col<Real, 1, st::PASS_INV_LAST>(p->st_col_cs[0], col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
       st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 1, ln, it);
       peaks(Xo, Xno);
     }

@@ -355,20 +355,19 @@ __device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, con
   }
   return cta_fft<DIR>(a, b, lv, cols, tw);
 }
-// Column transforms: compile-time paths for the fp32 column lengths of the benchmark geometries
-// (radices() order; measured: -2% on config 4, while the fp64 column kernels spill more and lose 5%),
-// the generic passes otherwise.  tw: the level's twiddles (already offset).
-template <int DIR, typename V>
+// Column transforms.  CS selects, per kernel instance, ONE transform path (the host picks it from the
+// level: col_schedule() in fif_st.cu), so each k_col instance carries only the code it runs:
+//   0 generic passes (fp64: radix <= 8), 1-4 fp32 F = 32 / 64 / 128 / 256, 5-6 fp64 F = 128 / 256,
+// each with the radices() schedule and the swizzled pitch F at compile time.  tw: the level's twiddles.
+template <int DIR, typename V, int CS>
 __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
-  if constexpr (sizeof(V) == 8) {
-    if (sched_is<32, 8, 4>(lv)) return cta_fft_c<DIR, V, 32, 1, 8, 4>(a, b, cols, tw);
-    if (sched_is<64, 4, 16>(lv)) return cta_fft_c<DIR, V, 64, 1, 4, 16>(a, b, cols, tw);
-    if (sched_is<128, 8, 16>(lv)) return cta_fft_c<DIR, V, 128, 1, 8, 16>(a, b, cols, tw);
-    if (sched_is<256, 16, 16>(lv)) return cta_fft_c<DIR, V, 256, 1, 16, 16>(a, b, cols, tw);
-    return cta_fft<DIR>(a, b, lv, cols, tw);
-  } else {
-    return cta_fft<DIR, V, 8>(a, b, lv, cols, tw);
-  }
+  if constexpr (CS == 1) return cta_fft_c<DIR, V, 32, 1, 8, 4>(a, b, cols, tw);
+  else if constexpr (CS == 2) return cta_fft_c<DIR, V, 64, 1, 4, 16>(a, b, cols, tw);
+  else if constexpr (CS == 3) return cta_fft_c<DIR, V, 128, 1, 8, 16>(a, b, cols, tw);
+  else if constexpr (CS == 4) return cta_fft_c<DIR, V, 256, 1, 16, 16>(a, b, cols, tw);
+  else if constexpr (CS == 5) return cta_fft_c<DIR, V, 128, 1, 2, 8, 8>(a, b, cols, tw);
+  else if constexpr (CS == 6) return cta_fft_c<DIR, V, 256, 1, 4, 8, 8>(a, b, cols, tw);
+  else return cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(a, b, lv, cols, tw);
 }
 
 // ------------------------------------------------------------------ tables
@@ -745,7 +744,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // finishes the IMF in natural order, updates R and writes the extrema partials of the new remainder.
 // Persistent CTAs, software-pipelined: the next tile streams into a third shared buffer with
 // cp.async while the current one is transformed.
-template <typename Real, int DIR, int KIND>
+template <typename Real, int DIR, int KIND, int CS = 0>
 __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ Geo g, const __grid_constant__ Level lv,
                                                      const __grid_constant__ Level lvn, const Real* __restrict__ sig,
                                                      Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
@@ -848,7 +847,7 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         r[j] = reinterpret_cast<const V*>(Rb)[cur.base + (int64_t)f * lv.S + cc];
       }
     }
-    V* out = col_fft<DIR>(In, Sc, lvs, lv.C, tws);
+    V* out = col_fft<DIR, V, CS>(In, Sc, lvs, lv.C, tws);
     if (KIND == PASS_INV_LAST) {
       V* stage = out == In ? Sc : In;
 #pragma unroll
