@@ -224,6 +224,17 @@ static int col_schedule(const st::Level& lv, bool f64) {
   }
   return 0;
 }
+// the row kernels' instance: 1 = the compile-time full-length row (st::row_fft RS)
+static int row_schedule(const st::Level& lv, bool f64) {
+  const int F = f64 ? 1024 : 2048;
+  const int r64[4] = {2, 8, 8, 8}, r32[3] = {8, 16, 16};
+  const int* r = f64 ? r64 : r32;
+  const int np = f64 ? 4 : 3;
+  if (lv.F != F || !lv.swz || lv.pitch != F || lv.np != np) return 0;
+  for (int i = 0; i < np; ++i)
+    if (lv.rad[i] != r[i]) return 0;
+  return 1;
+}
 template <typename Real, int DIR, int KIND, typename F>
 static void for_col_instances(F&& f) {
   f(st::k_col<Real, DIR, KIND, 0>);
@@ -306,11 +317,17 @@ fif_status st_setup_t(fif_plan_s* p) {
   for_col_instances<Real, 1, st::PASS_MID>(attr);
   for_col_instances<Real, 1, st::PASS_INV_LAST>(attr);
   for (int i = 0; i < g.L - 1; ++i) p->st_col_cs[i] = col_schedule(g.lv[i], sizeof(Real) == 8);
-  attr(st::k_rows_fwd<Real>);
-  attr(st::k_rows_inv<Real, 0, 0>);
-  attr(st::k_rows_inv<Real, kFastCap, 0>);
-  attr(st::k_rows_inv<Real, 0, 1>);
-  attr(st::k_rows_inv<Real, kFastCap, 1>);
+  attr(st::k_rows_fwd<Real, 0>);
+  attr(st::k_rows_fwd<Real, 1>);
+  attr(st::k_rows_inv<Real, 0, 0, 0>);
+  attr(st::k_rows_inv<Real, kFastCap, 0, 0>);
+  attr(st::k_rows_inv<Real, 0, 1, 0>);
+  attr(st::k_rows_inv<Real, kFastCap, 1, 0>);
+  attr(st::k_rows_inv<Real, 0, 0, 1>);
+  attr(st::k_rows_inv<Real, kFastCap, 0, 1>);
+  attr(st::k_rows_inv<Real, 0, 1, 1>);
+  attr(st::k_rows_inv<Real, kFastCap, 1, 1>);
+  p->st_row_rs = row_schedule(g.lv[g.L - 1], sizeof(Real) == 8);
   if (e != cudaSuccess) {
     fprintf(stderr, "fif: streamed setup failed: %s\n", cudaGetErrorString(e));
     return FIF_ERR_CUDA;
@@ -320,7 +337,8 @@ fif_status st_setup_t(fif_plan_s* p) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, st::k_col<Real, 1, st::PASS_INV_LAST>, st::kColThreads, smax);
     p->st_grid_col = p->num_sms * (occ > 0 ? occ : 1);
   }
-  p->st_grid_rows = occ_grid(p, st::k_rows_inv<Real, kFastCap, 1>, p->st_smem_rows);
+  p->st_grid_rows = p->st_row_rs ? occ_grid(p, st::k_rows_inv<Real, kFastCap, 1, 1>, p->st_smem_rows)
+                                 : occ_grid(p, st::k_rows_inv<Real, kFastCap, 1, 0>, p->st_smem_rows);
   p->st_grid_probe = occ_grid(p, st::k_probe<Real, kFastCap, 1>, 0);
   p->st_grid = p->st_grid_rows;
   for (int i = 0; i < 2; ++i)
@@ -396,7 +414,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
     for (int i = 1; i < Lv - 1; ++i)
       launch_col<Real, -1, st::PASS_MID>(p->st_col_cs[i], col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i], sg, out, X, tb, c);
-    st::k_rows_fwd<Real><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
+    if (p->st_row_rs) st::k_rows_fwd<Real, 1><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
+    else st::k_rows_fwd<Real, 0><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     auto peaks = [&](const V* Xs, const V* Xns) {  // spectral-peak rule: L for the next IMF
       if (!g.mask) return;
       st::k_peak1<Real><<<grow, TB, 0, s>>>(g, Xs, Xns, c);
@@ -413,8 +432,12 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
       const int gall = (int)(g.batch * g.units < (1LL << 30) ? g.batch * g.units : (1LL << 30));
       (void)gall;
       auto rows = [&](auto spec, auto cap, int redo_only) {
-        st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value>
-            <<<grow, TB, p->st_smem_rows, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
+        if (p->st_row_rs)
+          st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value, 1>
+              <<<grow, TB, p->st_smem_rows, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
+        else
+          st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value, 0>
+              <<<grow, TB, p->st_smem_rows, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
       };
       auto probe = [&](auto cap, auto mode) {
         st::k_probe<Real, decltype(cap)::value, decltype(mode)::value><<<gprobe, TB, 0, s>>>(g, Xi, Xni, tb, c);

@@ -343,17 +343,15 @@ __device__ __forceinline__ bool sched_is(const Level& lv) {
 }
 // Row transforms: the compile-time path for the full-length rows (every benchmark configuration), the
 // generic passes otherwise.
-template <int DIR, typename V>
+// Row transforms.  RS selects, per kernel instance, ONE path (the host picks it: row_schedule() in
+// fif_st.cu): 1 = the full-length rows of every benchmark geometry at compile time (fp64 1024 = 2 8 8 8,
+// radix <= 8 so the 64-register radix-16 butterfly is never compiled into an fp64 kernel; fp32
+// 2048 = 8 16 16), 0 = the generic passes.
+template <int DIR, typename V, int RS>
 __device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
-  if constexpr (sizeof(V) == 16) {
-    // fp64: radix <= 8 everywhere (radices(..., 8)): the 64-register radix-16 butterfly is never compiled
-    // into an fp64 streamed kernel (spills at the 3-CTA register budget; measured -1.3% on configs 2 and 3)
-    if (sched_is<1024, 2, 8, 8, 8>(lv)) return cta_fft_c<DIR, V, 1024, 1, 2, 8, 8, 8>(a, b, cols, tw + lv.twoff);
-    return cta_fft<DIR, V, 8>(a, b, lv, cols, tw);
-  } else {
-    if (sched_is<2048, 8, 16, 16>(lv)) return cta_fft_c<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw + lv.twoff);
-  }
-  return cta_fft<DIR>(a, b, lv, cols, tw);
+  if constexpr (RS == 1 && sizeof(V) == 16) return cta_fft_c<DIR, V, 1024, 1, 2, 8, 8, 8>(a, b, cols, tw + lv.twoff);
+  else if constexpr (RS == 1) return cta_fft_c<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw + lv.twoff);
+  else return cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(a, b, lv, cols, tw);
 }
 // Column transforms.  CS selects, per kernel instance, ONE transform path (the host picks it from the
 // level: col_schedule() in fif_st.cu), so each k_col instance carries only the code it runs:
@@ -989,7 +987,7 @@ __device__ __forceinline__ bool mirror_t(const Geo& g, int64_t bA, int two, int 
   return two || t <= tm;
 }
 
-template <typename Real>
+template <typename Real, int RS = 0>
 __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid_constant__ Geo g, const __grid_constant__ Level lv, typename Cx<Real>::V* __restrict__ X,
                                                        typename Cx<Real>::V* __restrict__ Xn,
                                                        const __grid_constant__ Tabs<Real> tb,
@@ -1029,7 +1027,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
         }
       }
     }
-    V* out = row_fft<-1>(A, Bf, lv, two ? 2 : 1, tb.tw);
+    V* out = row_fft<-1, V, RS>(A, Bf, lv, two ? 2 : 1, tb.tw);
     V* stage = out == A ? Bf : A;
     const int cb = two ? 1 : 0;
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
@@ -1068,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
 // the last CTA of a signal decides; if SD(cap) <= delta the damping was speculative: `redo` is set,
 // the K-ary search reads the untouched X_in, and a SPEC = 0 launch with redo_only recomputes X_out
 // and the IMF slot for those signals.  X_in / X_out (and the Nyquist bins) ping-pong per IMF.
-template <typename Real, int CAP, int SPEC>
+template <typename Real, int CAP, int SPEC, int RS = 0>
 __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
     const __grid_constant__ Geo g, const __grid_constant__ Level lv, const __grid_constant__ Level lvn,
     Real* __restrict__ imfs,
@@ -1192,7 +1190,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
         sred[threadIdx.x >> 5][1] = sQ;
       }
     }
-    V* out = row_fft<1>(Bf, A, lv, two ? 2 : 1, tb.tw);  // (its first barrier also publishes sred)
+    V* out = row_fft<1, V, RS>(Bf, A, lv, two ? 2 : 1, tb.tw);  // (its first barrier also publishes sred)
     V* W = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
     // the next (coarser) level's conjugate twiddle e^{+2 pi i s k'/(F' S')}: s = element, k' = row mod F'
     // (geometric in i: two table products per row and thread, one multiply per element)
