@@ -221,6 +221,8 @@ static int col_schedule(const st::Level& lv, bool f64) {
   } else {
     if (is(128, {2, 8, 8})) return 5;
     if (is(256, {4, 8, 8})) return 6;
+    if (is(32, {4, 8})) return 7;
+    if (is(64, {8, 8})) return 8;
   }
   return 0;
 }
@@ -246,6 +248,8 @@ static void for_col_instances(F&& f) {
   } else {
     f(st::k_col<Real, DIR, KIND, 5>);
     f(st::k_col<Real, DIR, KIND, 6>);
+    f(st::k_col<Real, DIR, KIND, 7>);
+    f(st::k_col<Real, DIR, KIND, 8>);
   }
 }
 template <typename Real, int DIR, int KIND, typename... A>
@@ -257,6 +261,8 @@ static void launch_col(int cs, int grid, size_t smem, cudaStream_t s, A... a) {
     case 4: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 4><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 5: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 5><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 6: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 6><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 7: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 7><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 8: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 8><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     default: break;
   }
   st::k_col<Real, DIR, KIND, 0><<<grid, st::kColThreads, smem, s>>>(a...);
