@@ -600,8 +600,8 @@ __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, 
   }
 }
 
-// Thread-chunk variant of tile_segments: the tps = blockDim / F threads t = f + F q (q = 0..tps-1) of
-// segment f own its consecutive chunks q of R = 2C / tps reals -- the lanes of a warp read the same
+// Thread-chunk variant of tile_segments: the tps threads t = f + F q (q = 0..tps-1; tps the largest power
+// of two dividing 2C with F tps <= blockDim) of segment f own its consecutive chunks q of R = 2C / tps reals -- the lanes of a warp read the same
 // column at consecutive rows, conflict-free -- each reduces its chunk (sign bits, one popc; the exact
 // rule when a difference is zero) including the difference into the next chunk, and thread f folds the
 // tps packed monoids in order.  Returns false (nothing written) when the tile shape does not allow it.
@@ -611,57 +611,60 @@ __device__ bool tile_segments_thr(const typename Cx<Real>::V* buf, const Level& 
   using V = typename Cx<Real>::V;
   __shared__ uint32_t pks[kColThreads];
   const int F = lv.F, nr = 2 * lv.C, nt = (int)blockDim.x;
-  if (nt > kColThreads || nt % F) return false;
-  const int tps = nt / F;
-  if (nr % tps) return false;
+  if (nt > kColThreads || F > nt) return false;
+  int tps = 1;  // chunks per segment: the largest power of two dividing nr with F tps <= blockDim
+  while (2 * tps * F <= nt && nr % (2 * tps) == 0) tps *= 2;
   const int R = nr / tps;
   if (R > 64 || (R & 1)) return false;
   const int t = threadIdx.x, f = t % F, q = t / F, c0 = q * (R >> 1);
+  const bool active = t < F * tps;  // the remaining threads only take part in the barrier
   const bool last = q == tps - 1;
   uint64_t bits = 0;
   int nd = 0;
   bool zero = false;
   Real prev;
-  {
-    const V v = buf[sidx<V>(c0, f, lv.pitch, lv.swz)];
-    const Real d = v.y - v.x;
-    zero |= d == (Real)0;
-    bits |= (uint64_t)(d < (Real)0);
-    nd = 1;
-    prev = v.y;
-  }
-  for (int c = c0 + 1; c < c0 + R / 2; ++c) {
-    const V v = buf[sidx<V>(c, f, lv.pitch, lv.swz)];
-    const Real d0 = v.x - prev, d1 = v.y - v.x;
-    zero |= (d0 == (Real)0) | (d1 == (Real)0);
-    bits |= ((uint64_t)(d0 < (Real)0) << nd) | ((uint64_t)(d1 < (Real)0) << (nd + 1));
-    nd += 2;
-    prev = v.y;
-  }
-  Real nxt = (Real)0;
-  if (!last) {  // the difference into the next chunk's first real
-    nxt = buf[sidx<V>(c0 + R / 2, f, lv.pitch, lv.swz)].x;
-    const Real d = nxt - prev;
-    zero |= d == (Real)0;
-    bits |= (uint64_t)(d < (Real)0) << nd;
-    ++nd;
-  }
-  Mono m;
-  if (!zero) {
-    const int cnt = nd > 1 ? __popcll((bits ^ (bits >> 1)) & ((1ull << (nd - 1)) - 1ull)) : 0;
-    m = Mono{(bits & 1ull) ? -1 : 1, ((bits >> (nd - 1)) & 1ull) ? -1 : 1, cnt};
-  } else {  // zero differences are dropped (A4): the exact sequential rule over this chunk
-    m = Mono{0, 0, 0};
-    Real pv = buf[sidx<V>(c0, f, lv.pitch, lv.swz)].x;
-    for (int j = 2 * c0 + 1; j < 2 * c0 + R; ++j) {
-      const V v = buf[sidx<V>(j >> 1, f, lv.pitch, lv.swz)];
-      const Real x = (j & 1) ? v.y : v.x;
-      m = mcomb(m, mdiff<Real>(x - pv));
-      pv = x;
+  if (active) {
+    {
+      const V v = buf[sidx<V>(c0, f, lv.pitch, lv.swz)];
+      const Real d = v.y - v.x;
+      zero |= d == (Real)0;
+      bits |= (uint64_t)(d < (Real)0);
+      nd = 1;
+      prev = v.y;
     }
-    if (!last) m = mcomb(m, mdiff<Real>(nxt - pv));
+    for (int c = c0 + 1; c < c0 + R / 2; ++c) {
+      const V v = buf[sidx<V>(c, f, lv.pitch, lv.swz)];
+      const Real d0 = v.x - prev, d1 = v.y - v.x;
+      zero |= (d0 == (Real)0) | (d1 == (Real)0);
+      bits |= ((uint64_t)(d0 < (Real)0) << nd) | ((uint64_t)(d1 < (Real)0) << (nd + 1));
+      nd += 2;
+      prev = v.y;
+    }
+    Real nxt = (Real)0;
+    if (!last) {  // the difference into the next chunk's first real
+      nxt = buf[sidx<V>(c0 + R / 2, f, lv.pitch, lv.swz)].x;
+      const Real d = nxt - prev;
+      zero |= d == (Real)0;
+      bits |= (uint64_t)(d < (Real)0) << nd;
+      ++nd;
+    }
+    Mono m;
+    if (!zero) {
+      const int cnt = nd > 1 ? __popcll((bits ^ (bits >> 1)) & ((1ull << (nd - 1)) - 1ull)) : 0;
+      m = Mono{(bits & 1ull) ? -1 : 1, ((bits >> (nd - 1)) & 1ull) ? -1 : 1, cnt};
+    } else {  // zero differences are dropped (A4): the exact sequential rule over this chunk
+      m = Mono{0, 0, 0};
+      Real pv = buf[sidx<V>(c0, f, lv.pitch, lv.swz)].x;
+      for (int j = 2 * c0 + 1; j < 2 * c0 + R; ++j) {
+        const V v = buf[sidx<V>(j >> 1, f, lv.pitch, lv.swz)];
+        const Real x = (j & 1) ? v.y : v.x;
+        m = mcomb(m, mdiff<Real>(x - pv));
+        pv = x;
+      }
+      if (!last) m = mcomb(m, mdiff<Real>(nxt - pv));
+    }
+    pks[t] = mpack(m);
   }
-  pks[t] = mpack(m);
   __syncthreads();
   if (q == 0) {
     Mono acc = munpack(pks[f]);
