@@ -218,6 +218,8 @@ static int col_schedule(const st::Level& lv, bool f64) {
     if (is(64, {4, 16})) return 2;
     if (is(128, {8, 16})) return 3;
     if (is(256, {16, 16})) return 4;
+    if (lv.F == 12 && !lv.swz && lv.pitch == 13 && lv.np == 2 && lv.rad[0] == 4 && lv.rad[1] == 3) return 9;
+    if (lv.F == 20 && !lv.swz && lv.pitch == 21 && lv.np == 2 && lv.rad[0] == 4 && lv.rad[1] == 5) return 10;
   } else {
     if (is(128, {2, 8, 8})) return 5;
     if (is(256, {4, 8, 8})) return 6;
@@ -245,6 +247,8 @@ static void for_col_instances(F&& f) {
     f(st::k_col<Real, DIR, KIND, 2>);
     f(st::k_col<Real, DIR, KIND, 3>);
     f(st::k_col<Real, DIR, KIND, 4>);
+    f(st::k_col<Real, DIR, KIND, 9>);
+    f(st::k_col<Real, DIR, KIND, 10>);
   } else {
     f(st::k_col<Real, DIR, KIND, 5>);
     f(st::k_col<Real, DIR, KIND, 6>);
@@ -259,6 +263,8 @@ static void launch_col(int cs, int grid, size_t smem, cudaStream_t s, A... a) {
     case 2: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 2><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 3: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 3><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 4: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 4><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 9: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 9><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 10: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 10><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 5: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 5><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 6: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 6><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 7: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 7><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;

@@ -299,14 +299,14 @@ __device__ V* cta_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict
 
 // The same passes with the transform length, a radix schedule and the swizzled pitch known at compile
 // time: constant index math.
-template <int P, int DIR, typename V, int F, int NS>
+template <int P, int DIR, typename V, int F, int NS, int PITCH = F, int SWZ = 1>
 __device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const V* __restrict__ tw) {
   constexpr int per = F / P, tstride = F / (NS * P);
   for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
     const int f = idx / per, vt = idx % per, k = vt % NS;
     V x[P];
 #pragma unroll
-    for (int r = 0; r < P; ++r) x[r] = src[sidx<V>(f, vt + r * per, F, 1)];
+    for (int r = 0; r < P; ++r) x[r] = src[sidx<V>(f, vt + r * per, PITCH, SWZ)];
     if constexpr (NS > 1) {
       const int kt = k * tstride;
 #pragma unroll
@@ -319,7 +319,7 @@ __device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const
     dft_small<P, DIR>(x);
     const int j0 = (vt - k) * P + k;
 #pragma unroll
-    for (int r = 0; r < P; ++r) dst[sidx<V>(f, j0 + r * NS, F, 1)] = x[r];
+    for (int r = 0; r < P; ++r) dst[sidx<V>(f, j0 + r * NS, PITCH, SWZ)] = x[r];
   }
 }
 template <int DIR, typename V, int F, int NS, int P, int... Rest>
@@ -331,6 +331,18 @@ __device__ __forceinline__ V* cta_fft_c(V* a, V* b, int cols, const V* __restric
     return b;
   } else {
     return cta_fft_c<DIR, V, F, NS * P, Rest...>(b, a, cols, tw);
+  }
+}
+// the same for an unswizzled (odd-pitch) level: the mixed-radix column lengths
+template <int DIR, typename V, int F, int NS, int P, int... Rest>
+__device__ __forceinline__ V* cta_fft_c_odd(V* a, V* b, int cols, const V* __restrict__ tw) {
+  __syncthreads();
+  cta_pass_c<P, DIR, V, F, NS, F + 1, 0>(a, b, cols, tw);
+  if constexpr (sizeof...(Rest) == 0) {
+    __syncthreads();
+    return b;
+  } else {
+    return cta_fft_c_odd<DIR, V, F, NS * P, Rest...>(b, a, cols, tw);
   }
 }
 template <int F, int... R>
@@ -356,6 +368,7 @@ __device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, con
 // Column transforms.  CS selects, per kernel instance, ONE transform path (the host picks it from the
 // level: col_schedule() in fif_st.cu), so each k_col instance carries only the code it runs:
 //   0 generic passes (fp64: radix <= 8), 1-4 fp32 F = 32 / 64 / 128 / 256, 5-8 fp64 F = 128 / 256 / 32 / 64,
+//   9-10 fp32 F = 12 / 20 (unswizzled, pitch F + 1),
 // each with the radices() schedule and the swizzled pitch F at compile time.  tw: the level's twiddles.
 template <int DIR, typename V, int CS>
 __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
@@ -367,6 +380,8 @@ __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, con
   else if constexpr (CS == 6) return cta_fft_c<DIR, V, 256, 1, 4, 8, 8>(a, b, cols, tw);
   else if constexpr (CS == 7) return cta_fft_c<DIR, V, 32, 1, 4, 8>(a, b, cols, tw);
   else if constexpr (CS == 8) return cta_fft_c<DIR, V, 64, 1, 8, 8>(a, b, cols, tw);
+  else if constexpr (CS == 9) return cta_fft_c_odd<DIR, V, 12, 1, 4, 3>(a, b, cols, tw);
+  else if constexpr (CS == 10) return cta_fft_c_odd<DIR, V, 20, 1, 4, 5>(a, b, cols, tw);
   else return cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(a, b, lv, cols, tw);
 }
 
