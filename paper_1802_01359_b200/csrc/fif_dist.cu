@@ -91,7 +91,7 @@ __device__ __forceinline__ int64_t local_bin(const st::Geo& g, int64_t pos) {
 // ---------------------------------------------------------------- local multi-level passes (in place)
 // Level tile = C consecutive lower indices x F digit values; DIR -1 forward (DFT, twiddle),
 // +1 inverse (conjugate twiddle, IDFT).  Twiddles use the global-n table (E2 = 2n/(F S)).
-template <typename Real, int DIR>
+template <typename Real, int DIR, int CS = 0>
 __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_d_pass(const __grid_constant__ DGeo d,
                                                         const __grid_constant__ Level lv,
                                                         typename Cx<Real>::V* __restrict__ buf,
@@ -127,7 +127,9 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_d_pass(const __grid_c
         A[st::sidx<V>(cc, f, lv.pitch, lv.swz)] = x;
       }
     }
-    V* out = st::cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(A, Bf, lv, lv.C, tb.tw);  // fp64 levels: radix <= 8
+    Level lvs = lv;  // the transform path of this instance (pass_schedule); twiddles pre-offset
+    lvs.twoff = 0;
+    V* out = st::col_fft<DIR, V, CS>(A, Bf, lvs, lv.C, tb.tw + lv.twoff);
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int i = threadIdx.x + j * kThreads;
@@ -662,6 +664,7 @@ struct DistPlan {
   void *Eh = nullptr, *El = nullptr, *Th = nullptr, *Tl = nullptr, *tw = nullptr;
   void *utab = nullptr, *rbase = nullptr, *rmir = nullptr;
   size_t smem_pass[st::kMaxLev] = {};
+  int pass_cs[st::kMaxLev] = {};  // compile-time transform path per level (k_d_pass CS)
   int grid_pass = 0, grid_elem = 0, grid_probe = 0;
   int rounds = 0;
   int64_t Q = 0;
@@ -735,6 +738,37 @@ fif_status c_partner(DistPlan& D, F1 send, F2 recv, size_t bytes, cudaStream_t s
 
 int gmin(int64_t work, int cap) { return (int)(work < cap ? (work > 0 ? work : 1) : cap); }
 
+// k_d_pass instance for a level's transform path (pass_schedule in fif_st.cu)
+template <typename Real, int DIR, typename F>
+static void for_dpass_instances(F&& f) {
+  f(k_d_pass<Real, DIR, 0>);
+  if constexpr (sizeof(Real) == 4) {
+    f(k_d_pass<Real, DIR, 1>); f(k_d_pass<Real, DIR, 2>); f(k_d_pass<Real, DIR, 3>); f(k_d_pass<Real, DIR, 4>);
+    f(k_d_pass<Real, DIR, 9>); f(k_d_pass<Real, DIR, 10>); f(k_d_pass<Real, DIR, 12>);
+  } else {
+    f(k_d_pass<Real, DIR, 5>); f(k_d_pass<Real, DIR, 6>); f(k_d_pass<Real, DIR, 7>); f(k_d_pass<Real, DIR, 8>);
+    f(k_d_pass<Real, DIR, 11>);
+  }
+}
+template <typename Real, int DIR, typename... A>
+static void launch_dpass(int cs, int64_t grid, size_t smem, cudaStream_t s, A... a) {
+#define FIF_DP(C, COND)                                                        \
+  case C:                                                                      \
+    if constexpr (COND) {                                                      \
+      k_d_pass<Real, DIR, C><<<(unsigned)grid, kThreads, smem, s>>>(a...);     \
+      return;                                                                  \
+    }                                                                          \
+    break;
+  constexpr bool f32 = sizeof(Real) == 4, f64 = sizeof(Real) == 8;
+  switch (cs) {
+    FIF_DP(1, f32) FIF_DP(2, f32) FIF_DP(3, f32) FIF_DP(4, f32) FIF_DP(9, f32) FIF_DP(10, f32) FIF_DP(12, f32)
+    FIF_DP(5, f64) FIF_DP(6, f64) FIF_DP(7, f64) FIF_DP(8, f64) FIF_DP(11, f64)
+    default: break;
+  }
+#undef FIF_DP
+  k_d_pass<Real, DIR, 0><<<(unsigned)grid, kThreads, smem, s>>>(a...);
+}
+
 template <typename Real>
 fif_status dist_setup_t(fif_plan_s* p, DistPlan& D) {
   using V = typename Cx<Real>::V;
@@ -805,10 +839,14 @@ fif_status dist_setup_t(fif_plan_s* p, DistPlan& D) {
     D.smem_pass[i] = 2 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch;
     smax = smax > D.smem_pass[i] ? smax : D.smem_pass[i];
   }
-  cudaError_t e = cudaFuncSetAttribute(k_d_pass<Real, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_d_pass<Real, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+  cudaError_t e = cudaSuccess;
+  auto attr = [&](auto kern) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+  };
+  for_dpass_instances<Real, -1>(attr);
+  for_dpass_instances<Real, 1>(attr);
   if (e != cudaSuccess) return FIF_ERR_CUDA;
+  for (int i = 0; i < g.L; ++i) D.pass_cs[i] = pass_schedule(g.lv[i], sizeof(Real) == 8);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_d_pass<Real, 1>, kThreads, smax);
   D.grid_pass = p->num_sms * (occ > 0 ? occ : 1);
@@ -972,8 +1010,8 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
     ok(peer_barrier(D, s));
     all([&](int, DRank& R) {
       for (int i = 0; i < R.d.g.L; ++i)
-        k_d_pass<Real, -1><<<gmin(R.d.g.lv[i].tiles, D.grid_pass), TB, D.smem_pass[i], s>>>(R.d, R.d.g.lv[i],
-                                                                                            (V*)R.T, tb, R.c.s);
+        launch_dpass<Real, -1>(D.pass_cs[i], gmin(R.d.g.lv[i].tiles, D.grid_pass), D.smem_pass[i], s, R.d, R.d.g.lv[i],
+                               (V*)R.T, tb, (const int32_t*)R.c.s);
     });
     ok(peer_barrier(D, s));
     all([&](int li, DRank& R) {
@@ -988,8 +1026,8 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
     ok(c_alltoall(D, [&](int, DRank& R) { return (const void*)R.T; }, [&](int, DRank& R) { return R.U; }, wb, s));
     all([&](int, DRank& R) {
       for (int i = 0; i < R.d.g.L; ++i)
-        k_d_pass<Real, -1><<<gmin(R.d.g.lv[i].tiles, D.grid_pass), TB, D.smem_pass[i], s>>>(R.d, R.d.g.lv[i],
-                                                                                            (V*)R.U, tb, R.c.s);
+        launch_dpass<Real, -1>(D.pass_cs[i], gmin(R.d.g.lv[i].tiles, D.grid_pass), D.smem_pass[i], s, R.d, R.d.g.lv[i],
+                               (V*)R.U, tb, (const int32_t*)R.c.s);
     });
     ok(c_partner(D, [&](int, DRank& R) { return (const void*)R.U; }, [&](int, DRank& R) { return R.T; }, qb, s));
     all([&](int, DRank& R) {
@@ -1015,8 +1053,8 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
       if (fast) k_d_pre<Real, kFastCap><<<ge, TB, 0, s>>>(R.d, (V*)R.X, (V*)R.Xm, (V*)R.T, tb, R.c.s);
       else k_d_pre<Real, 0><<<ge, TB, 0, s>>>(R.d, (V*)R.X, (V*)R.Xm, (V*)R.T, tb, R.c.s);
       for (int i = R.d.g.L - 1; i >= 0; --i)
-        k_d_pass<Real, 1><<<gmin(R.d.g.lv[i].tiles, D.grid_pass), TB, D.smem_pass[i], s>>>(R.d, R.d.g.lv[i], (V*)R.T,
-                                                                                         tb, R.c.s);
+        launch_dpass<Real, 1>(D.pass_cs[i], gmin(R.d.g.lv[i].tiles, D.grid_pass), D.smem_pass[i], s, R.d, R.d.g.lv[i],
+                              (V*)R.T, tb, (const int32_t*)R.c.s);
       if (!D.peer) k_d_twiddle_inv<Real><<<ge, TB, 0, s>>>(R.d, (const V*)R.T, (V*)R.U, tb, R.c.s);
     });
     if (D.peer) {  // all-to-alls #3 and #4 as peer stores of the twiddle and rank-DFT kernels

@@ -113,6 +113,8 @@ void st_free(fif_plan_s* p);
 // workspace: bytes needed with the current options; (re)bind the buffers to `base` (nullptr: plan-owned block)
 size_t st_workspace_bytes(const fif_plan_s* p);
 fif_status st_bind_workspace(fif_plan_s* p, void* base, size_t bytes);
+// compile-time transform path of a C x F tile level (st::col_fft CS; 0 = generic)
+int pass_schedule(const fifgpu::st::Level& lv, bool f64);
 
 // iterative regime (fif_iterative.cu): Algorithm 2 literally (the IF baseline of PAPER.md:693)
 fif_status it_setup(fif_plan_s* p);

@@ -239,6 +239,12 @@ static int row_schedule(const st::Level& lv, bool f64) {
     if (lv.rad[i] != r[i]) return 0;
   return 1;
 }
+// any level processed as C x F tiles (the distributed passes): column shapes, then the row lengths
+int pass_schedule_impl(const st::Level& lv, bool f64) {
+  const int cs = col_schedule(lv, f64);
+  if (cs) return cs;
+  return row_schedule(lv, f64) ? (f64 ? 11 : 12) : 0;
+}
 template <typename Real, int DIR, int KIND, typename F>
 static void for_col_instances(F&& f) {
   f(st::k_col<Real, DIR, KIND, 0>);
@@ -482,6 +488,7 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     }
 }
 }  // namespace
+int pass_schedule(const st::Level& lv, bool f64) { return pass_schedule_impl(lv, f64); }
 int st_kernels_per_call(const fif_plan_s* p) {
   const int L = p->geo.L;
   const int64_t waves = p->batch > 0 ? (p->batch + p->st_wave - 1) / p->st_wave : 0;

@@ -368,7 +368,7 @@ __device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, con
 // Column transforms.  CS selects, per kernel instance, ONE transform path (the host picks it from the
 // level: col_schedule() in fif_st.cu), so each k_col instance carries only the code it runs:
 //   0 generic passes (fp64: radix <= 8), 1-4 fp32 F = 32 / 64 / 128 / 256, 5-8 fp64 F = 128 / 256 / 32 / 64,
-//   9-10 fp32 F = 12 / 20 (unswizzled, pitch F + 1),
+//   9-10 fp32 F = 12 / 20 (unswizzled, pitch F + 1), 11-12 the row lengths (distributed passes),
 // each with the radices() schedule and the swizzled pitch F at compile time.  tw: the level's twiddles.
 template <int DIR, typename V, int CS>
 __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
@@ -382,6 +382,8 @@ __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, con
   else if constexpr (CS == 8) return cta_fft_c<DIR, V, 64, 1, 8, 8>(a, b, cols, tw);
   else if constexpr (CS == 9) return cta_fft_c_odd<DIR, V, 12, 1, 4, 3>(a, b, cols, tw);
   else if constexpr (CS == 10) return cta_fft_c_odd<DIR, V, 20, 1, 4, 5>(a, b, cols, tw);
+  else if constexpr (CS == 11) return cta_fft_c<DIR, V, 1024, 1, 2, 8, 8, 8>(a, b, cols, tw);
+  else if constexpr (CS == 12) return cta_fft_c<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw);
   else return cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(a, b, lv, cols, tw);
 }
 
