@@ -239,10 +239,10 @@ def run_reference(args, world, rank):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         oracle.decompose(s, delta=delta)
-    dt = (time.perf_counter() - t0) / args.steps
-    value = S * n / dt
+    step_s = (time.perf_counter() - t0) / args.steps
+    value = S * n / step_s
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
             "config": {"workload": f"{args.config}: {S}-signal sample of the {B}x{n} {dt} batch per step",
                        "n": n, "batch_per_step": S, "xi": 1.6, "delta": delta, "max_inner": 200, "max_imfs": 10},

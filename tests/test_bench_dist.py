@@ -65,6 +65,11 @@ def test_reference_arm_rank0_only(tmp_path):
 
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    # the line keeps the contract's types: dtype names the arithmetic type, the workload names the batch
+    assert d["dtype"] == "f64" and "f64" in d["config"]["workload"]
+    assert abs(d["ms_per_step"] * 1e-3 * d["value"] - d["config"]["batch_per_step"] * d["config"]["n"]) <= \
+        1e-6 * d["config"]["batch_per_step"] * d["config"]["n"]
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
 
 
 def _worker_cfg3(rank, world, port, out):
