@@ -213,7 +213,8 @@ fif_status fif_plan_set_eigen_table(fif_plan_t p, int32_t enable) {
   }
   if (p->d_wtab) return FIF_OK;
   const int nL = (int)((p->n - 1) / 4) - 1;  // L = 2 .. floor((n-1)/4) (reading A3)
-  const size_t es = p->dtype == FIF_F64 ? sizeof(double) : sizeof(float);
+  // fp64: {w_hat, a^(max_inner-1)} pairs; fp32: w_hat (fif_wtab_kernel)
+  const size_t es = p->dtype == FIF_F64 ? 2 * sizeof(double) : sizeof(float);
   if (cudaMalloc(&p->d_wtab, (size_t)nL * (size_t)(p->NC + 1) * es) != cudaSuccess) {
     p->d_wtab = nullptr;
     return FIF_ERR_OOM;
@@ -301,6 +302,7 @@ fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int3
     return launch_status();
   }
   if (p->regime == 1) {
+    if (!p->d_X || !p->d_ctl) return FIF_ERR_INVALID_ARG;  // no workspace bound
     st_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, 0, s);
     return launch_status();
   }
@@ -318,40 +320,59 @@ fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs,
   if (p->batch == 0) return FIF_OK;
   if (!h_signals || !h_imfs || !h_imf_count || !h_filter_len || !h_iters) return FIF_ERR_INVALID_ARG;
   if (p->regime == 2) return FIF_ERR_INVALID_ARG;  // distributed plans take device buffers
+  if (p->regime == 1 && (!p->d_X || !p->d_ctl)) return FIF_ERR_INVALID_ARG;  // no workspace bound
   const size_t es = elem_size(p->dtype);
   const size_t in_sig = (size_t)p->n * es, out_sig = in_sig * (size_t)(p->max_imfs + 1);
   const size_t meta_sig = (size_t)(1 + 2 * p->max_imfs);
   if (p->nstages == 0) {
-    // chunks of ~1/8 of the batch (>= one full wave of CTAs when possible), 3 stages in flight
+    // chunks of ~1/8 of the batch (>= one full wave of CTAs when possible), 3 stages in flight.
+    // Allocated into locals: p->nstages / p->chunk are committed only when every stage exists.
     int64_t chunk = (p->batch + 7) / 8;
-    const int64_t wave = (int64_t)p->num_sms * p->occ;
+    const int64_t wave = (int64_t)p->num_sms * (p->occ > 0 ? p->occ : 1);
     if (chunk < wave) chunk = wave < p->batch ? wave : p->batch;
-    p->chunk = chunk;
-    p->nstages = (int)((p->batch + chunk - 1) / chunk < FIF_MAX_STAGES ? (p->batch + chunk - 1) / chunk
-                                                                        : FIF_MAX_STAGES);
-    for (int i = 0; i < p->nstages; ++i) {
-      Staging& S = p->st[i];
+    const int ns = (int)((p->batch + chunk - 1) / chunk < FIF_MAX_STAGES ? (p->batch + chunk - 1) / chunk
+                                                                          : FIF_MAX_STAGES);
+    Staging tmp[FIF_MAX_STAGES];
+    fif_status err = FIF_OK;
+    for (int i = 0; i < ns && err == FIF_OK; ++i) {
+      Staging& S = tmp[i];
       if (cudaMalloc(&S.d_in, in_sig * chunk) != cudaSuccess || cudaMalloc(&S.d_out, out_sig * chunk) != cudaSuccess ||
           cudaMalloc(&S.d_meta, sizeof(int32_t) * meta_sig * chunk) != cudaSuccess)
-        return FIF_ERR_OOM;
-      if (cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming) != cudaSuccess)
-        return FIF_ERR_CUDA;
+        err = FIF_ERR_OOM;
+      else if (cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking) != cudaSuccess ||
+               cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming) != cudaSuccess)
+        err = FIF_ERR_CUDA;
     }
+    if (err != FIF_OK) {
+      for (int i = 0; i < ns; ++i) {
+        cudaFree(tmp[i].d_in);
+        cudaFree(tmp[i].d_out);
+        cudaFree(tmp[i].d_meta);
+        if (tmp[i].stream) cudaStreamDestroy(tmp[i].stream);
+        if (tmp[i].done) cudaEventDestroy(tmp[i].done);
+      }
+      cudaGetLastError();
+      return err;
+    }
+    for (int i = 0; i < ns; ++i) p->st[i] = tmp[i];
+    p->chunk = chunk;
+    p->nstages = ns;
   }
   cudaStream_t user = (cudaStream_t)stream;
   cudaEvent_t start;
-  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-  cudaEventRecord(start, user);
-  for (int i = 0; i < p->nstages; ++i) cudaStreamWaitEvent(p->st[i].stream, start, 0);
+  if (cudaEventCreateWithFlags(&start, cudaEventDisableTiming) != cudaSuccess) return FIF_ERR_CUDA;
+  bool ok = cudaEventRecord(start, user) == cudaSuccess;
+  for (int i = 0; i < p->nstages && ok; ++i) ok = cudaStreamWaitEvent(p->st[i].stream, start, 0) == cudaSuccess;
   const int64_t nchunks = (p->batch + p->chunk - 1) / p->chunk;
-  for (int64_t c = 0; c < nchunks; ++c) {
+  for (int64_t c = 0; c < nchunks && ok; ++c) {
     Staging& S = p->st[c % p->nstages];
     const int64_t b0 = c * p->chunk, nb = (b0 + p->chunk <= p->batch) ? p->chunk : p->batch - b0;
     int32_t* d_cnt = S.d_meta;
     int32_t* d_len = S.d_meta + nb;
     int32_t* d_it = d_len + nb * p->max_imfs;
-    cudaMemcpyAsync(S.d_in, (const char*)h_signals + b0 * in_sig, nb * in_sig, cudaMemcpyHostToDevice, S.stream);
+    ok = cudaMemcpyAsync(S.d_in, (const char*)h_signals + b0 * in_sig, nb * in_sig, cudaMemcpyHostToDevice,
+                         S.stream) == cudaSuccess;
+    if (!ok) break;
     if (p->regime == 1) {
       // disjoint plan work buffers per chunk (chunks run concurrently on the staging streams)
       st_decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, b0, S.stream);
@@ -360,18 +381,26 @@ fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs,
     } else {
       res_ops(p->dtype, p->NC)->decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
     }
-    cudaMemcpyAsync((char*)h_imfs + b0 * out_sig, S.d_out, nb * out_sig, cudaMemcpyDeviceToHost, S.stream);
-    cudaMemcpyAsync(h_imf_count + b0, d_cnt, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, S.stream);
-    cudaMemcpyAsync(h_filter_len + b0 * p->max_imfs, d_len, sizeof(int32_t) * nb * p->max_imfs,
-                    cudaMemcpyDeviceToHost, S.stream);
-    cudaMemcpyAsync(h_iters + b0 * p->max_imfs, d_it, sizeof(int32_t) * nb * p->max_imfs, cudaMemcpyDeviceToHost,
-                    S.stream);
+    ok = cudaMemcpyAsync((char*)h_imfs + b0 * out_sig, S.d_out, nb * out_sig, cudaMemcpyDeviceToHost, S.stream) ==
+             cudaSuccess &&
+         cudaMemcpyAsync(h_imf_count + b0, d_cnt, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, S.stream) ==
+             cudaSuccess &&
+         cudaMemcpyAsync(h_filter_len + b0 * p->max_imfs, d_len, sizeof(int32_t) * nb * p->max_imfs,
+                         cudaMemcpyDeviceToHost, S.stream) == cudaSuccess &&
+         cudaMemcpyAsync(h_iters + b0 * p->max_imfs, d_it, sizeof(int32_t) * nb * p->max_imfs, cudaMemcpyDeviceToHost,
+                         S.stream) == cudaSuccess;
   }
+  // the user stream waits for every stage whatever happened, so no staged work outlives the call unseen
   for (int i = 0; i < p->nstages; ++i) {
     cudaEventRecord(p->st[i].done, p->st[i].stream);
     cudaStreamWaitEvent(user, p->st[i].done, 0);
   }
   cudaEventDestroy(start);
+  if (!ok) {
+    fprintf(stderr, "fif: host-path copy or event failed: %s\n", cudaGetErrorString(cudaGetLastError()));
+    cudaStreamSynchronize(user);
+    return FIF_ERR_CUDA;
+  }
   fif_status st = launch_status();
   if (st != FIF_OK) return st;
   if (cudaStreamSynchronize(user) != cudaSuccess) return FIF_ERR_CUDA;

@@ -616,6 +616,7 @@ struct Nccl {
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclCommGetAsyncError) commGetAsyncError = nullptr;
   bool load() {
     if (h) return true;
     h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -634,8 +635,10 @@ struct Nccl {
     FIF_SYM(groupStart, "ncclGroupStart");
     FIF_SYM(groupEnd, "ncclGroupEnd");
     FIF_SYM(errStr, "ncclGetErrorString");
+    FIF_SYM(commGetAsyncError, "ncclCommGetAsyncError");
 #undef FIF_SYM
-    return getUniqueId && commInitRank && commDestroy && allGather && send && recv && groupStart && groupEnd;
+    return getUniqueId && commInitRank && commDestroy && allGather && allReduce && send && recv && groupStart &&
+           groupEnd && commGetAsyncError;
   }
 };
 Nccl& nccl() {
@@ -672,6 +675,7 @@ struct DistPlan {
   // stores into the ranks' buffers (CUDA IPC handles in a multi-process plan), a barrier after each
   bool peer = false;
   void* dpeer = nullptr;                 // device: [local ranks][2][P] pointers (U table, T table)
+  std::vector<void*> hpeer;              // host copy of the same table (read by the host launch code)
   std::vector<void*> ipc_open;           // IPC-mapped peer buffers to close
   void* dbar = nullptr;                  // one int for the NCCL barrier
 };
@@ -682,6 +686,16 @@ fif_status nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return FIF_OK;
   fprintf(stderr, "fif: %s failed: %s\n", what, nccl().errStr ? nccl().errStr(r) : "?");
   return FIF_ERR_NCCL;
+}
+
+// ncclCommGetAsyncError polling (network / peer failures are reported asynchronously by NCCL)
+fif_status async_error(DistPlan& D) {
+  if (D.emulated || !D.comm || !nccl().commGetAsyncError) return FIF_OK;
+  ncclResult_t ae = ncclSuccess;
+  ncclResult_t r = nccl().commGetAsyncError(D.comm, &ae);
+  if (r != ncclSuccess) return nccl_check(r, "ncclCommGetAsyncError");
+  if (ae != ncclSuccess && ae != ncclInProgress) return nccl_check(ae, "NCCL communicator (async error)");
+  return FIF_OK;
 }
 
 // ---------------- collectives (NCCL or emulated copies); `field` selects the per-rank buffer
@@ -940,6 +954,7 @@ fif_status peer_setup(DistPlan& D) {
   if (cudaMalloc(&D.dpeer, sizeof(void*) * tab.size()) != cudaSuccess) return FIF_ERR_OOM;
   if (cudaMemcpy(D.dpeer, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     return FIF_ERR_CUDA;
+  D.hpeer = tab;
   D.peer = true;
   return FIF_OK;
 }
@@ -1000,8 +1015,7 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
   auto ptabU = [&](int li) { return (V* const*)((void**)D.dpeer + (size_t)li * 2 * D.P); };
   auto ptabT = [&](int li) { return (V* const*)((void**)D.dpeer + (size_t)li * 2 * D.P + D.P); };
   if (D.peer) {
-    std::vector<void*> tab((size_t)nl * 2 * D.P);
-    cudaMemcpy(tab.data(), D.dpeer, sizeof(void*) * tab.size(), cudaMemcpyDeviceToHost);
+    const std::vector<void*>& tab = D.hpeer;  // host copy kept by peer_setup: no device read, graph-capturable
     all([&](int li, DRank& R) { k_d_scatter<Real><<<ge, TB, 0, s>>>(R.d, (const V*)SIG(li), ptabU(li)); });
     ok(peer_barrier(D, s));
     all([&](int li, DRank& R) {
@@ -1116,8 +1130,12 @@ fif_status dist_create(fif_plan_s* p, const void* uid, int rank, int nranks, int
 fif_status dist_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
                           cudaStream_t s) {
   DistPlan& D = *p->dist;
-  return p->dtype == FIF_F64 ? dist_decompose_t<double>(p, D, sig, imfs, cnt, lens, its, s)
-                             : dist_decompose_t<float>(p, D, sig, imfs, cnt, lens, its, s);
+  // NCCL failures of earlier (asynchronous) calls surface here: a communicator in error refuses new work
+  if (fif_status a = async_error(D); a != FIF_OK) return a;
+  const fif_status st = p->dtype == FIF_F64 ? dist_decompose_t<double>(p, D, sig, imfs, cnt, lens, its, s)
+                                            : dist_decompose_t<float>(p, D, sig, imfs, cnt, lens, its, s);
+  if (st != FIF_OK) return st;
+  return async_error(D);
 }
 void dist_free(fif_plan_s* p) {
   DistPlan* D = p->dist;

@@ -9,13 +9,26 @@ using namespace fifgpu;
 template <typename Real, int NC>
 struct Inst {
   using K = Resident<Real, NC>;
+  using KT = Resident<Real, NC, 0, true>;  // table-driven instances (smaller shared-memory footprint)
   using V = typename Cx<Real>::V;
+  // dynamic smem limit + a carveout just large enough for the occupancy the registers allow, so the rest
+  // of the SM's 256 KB stays L1 (twiddles, table rows, spills)
+  template <typename Kern>
+  static cudaError_t main_attr(Kern k, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, K::T, smem)) != cudaSuccess) return e;
+    const size_t need = (size_t)(occ > 0 ? occ : 1) * (smem + 1024);
+    const int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+    return cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+  }
   static cudaError_t prepare() {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_resident_kernel<Real, NC, kFastCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = main_attr(fif_resident_kernel<Real, NC, 0, false>, K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = main_attr(fif_resident_kernel<Real, NC, kFastCap, false>, K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = main_attr(fif_resident_kernel<Real, NC, 0, true>, KT::smem_bytes)) != cudaSuccess) return e;
+    if ((e = main_attr(fif_resident_kernel<Real, NC, kFastCap, true>, KT::smem_bytes)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, kFastCap>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem_bytes)) != cudaSuccess)
       return e;
@@ -29,13 +42,15 @@ struct Inst {
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(fif_test_inner_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(fif_wtab_kernel<Real, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(fif_wtab_kernel<Real, NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)K::smem_bytes)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fif_wtab_kernel<Real, NC, kFastCap>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     return cudaSuccess;
   }
   static int occupancy() {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC, kFastCap>, K::T, K::smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC, kFastCap, false>, K::T, K::smem_bytes);
     return occ;
   }
   static void decompose(const fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its,
@@ -44,14 +59,12 @@ struct Inst {
     prm.wtab = p->d_wtab;
     const int64_t cap = (int64_t)p->num_sms * p->occ;
     const int grid = (int)(batch < cap ? batch : cap);
-    if (p->max_inner == kFastCap)
-      fif_resident_kernel<Real, NC, kFastCap><<<grid, K::T, K::smem_bytes, s>>>(
-          (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
-          (const V*)p->d_tw, prm);
-    else
-      fif_resident_kernel<Real, NC, 0><<<grid, K::T, K::smem_bytes, s>>>(
-          (const Real*)sig, (Real*)imfs, cnt, lens, its, (const Real*)p->d_sin, (const Real*)p->d_isin,
-          (const V*)p->d_tw, prm);
+    const bool fast = p->max_inner == kFastCap, tab = p->d_wtab != nullptr;
+    auto kern = fast ? (tab ? fif_resident_kernel<Real, NC, kFastCap, true> : fif_resident_kernel<Real, NC, kFastCap, false>)
+                     : (tab ? fif_resident_kernel<Real, NC, 0, true> : fif_resident_kernel<Real, NC, 0, false>);
+    kern<<<grid, K::T, tab ? KT::smem_bytes : K::smem_bytes, s>>>((const Real*)sig, (Real*)imfs, cnt, lens, its,
+                                                                 (const Real*)p->d_sin, (const Real*)p->d_isin,
+                                                                 (const V*)p->d_tw, prm);
   }
   static void test_rfft(const fif_plan_s* p, const void* in, void* out, int64_t batch, cudaStream_t s) {
     const int grid = (int)(batch < 4096 ? batch : 4096);
@@ -73,7 +86,12 @@ struct Inst {
                                                                         (const Real*)p->d_isin);
   }
   static void fill_wtab(const fif_plan_s* p, void* tab, int nL, cudaStream_t s) {
-    fif_wtab_kernel<Real, NC><<<nL, K::T, K::smem_bytes, s>>>((Real*)tab, (const Real*)p->d_sin, (const Real*)p->d_isin);
+    if (p->max_inner == kFastCap)
+      fif_wtab_kernel<Real, NC, kFastCap><<<nL, K::T, K::smem_bytes, s>>>(tab, (const Real*)p->d_sin,
+                                                                         (const Real*)p->d_isin, p->max_inner);
+    else
+      fif_wtab_kernel<Real, NC, 0><<<nL, K::T, K::smem_bytes, s>>>(tab, (const Real*)p->d_sin, (const Real*)p->d_isin,
+                                                                  p->max_inner);
   }
   static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
                          cudaStream_t s) {

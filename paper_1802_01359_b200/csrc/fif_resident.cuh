@@ -40,9 +40,6 @@
 #ifndef FIF_EXT1
 #define FIF_EXT1 0
 #endif
-#ifndef FIF_SPEC
-#define FIF_SPEC 0
-#endif
 
 namespace fifgpu {
 
@@ -62,7 +59,10 @@ struct Params {
   double delta;     // delta (absolute, for stop = 1)
   double gamma;     // > 0: gamma-threshold variant (A19)
   int32_t mask;     // 0: extrema filter-length rule (A1-A3); 1: spectral-peak rule (A20)
-  const void* wtab = nullptr;  // Real[(n-1)/4 - 1][NC+1]: w_hat per L, nullptr: closed form
+  // per-L eigenvalue table, row L - 2, bins 0..NC; nullptr: closed form per IMF.
+  // fp64 plans: double2 {w_hat_k, a_k^(max_inner-1)} (the cap probe's power chain precomputed by the
+  // kernel's own code, bit-identical); fp32 plans: Real w_hat_k.
+  const void* wtab = nullptr;
 };
 
 // ------------------------------------------------------------------ a5 alternative: a-priori N0
@@ -254,52 +254,48 @@ __device__ __forceinline__ V* fft_passes(V (&v)[kR], V* rd, V* wr, const V* __re
 }
 
 // ------------------------------------------------------------------ block reductions
+__host__ __device__ constexpr int pow2ceil(int m) { return m <= 1 ? 1 : 2 * pow2ceil((m + 1) / 2); }
+__host__ __device__ constexpr int ilog2c(int m) { return m <= 1 ? 0 : 1 + ilog2c(m / 2); }
+
 // Sum M values over the block; every thread gets the same (deterministically ordered) totals.
-// red: NW*M doubles of scratch, not reused until after the next __syncthreads of the caller.
+// Warp level as a reduce-scatter: at each xor level a lane keeps one half of its values and receives
+// the partner's copy of that half (M2 = pow2ceil(M) values: M2 - 1 shuffles instead of 5 M); after
+// log2(M2) levels lane l holds the warp total of value l / (32 / M2), and the remaining levels are a
+// plain butterfly.  Across warps: lane l sums the NW warp totals of value l % M2 in warp order, and
+// value i is broadcast from lane i.  red: NW * M2 values of scratch, not reused until after the
+// caller's next barrier (callers alternate two slots).
 template <int NW, int M, typename S>
 __device__ __forceinline__ void block_sum(S (&v)[M], S* red, int j) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  constexpr int M2 = pow2ceil(M);
+  static_assert(M2 <= 32, "at most 32 values");
   const int lane = j & 31;
-  if (lane == 0)
+  S u[M2];
 #pragma unroll
-    for (int i = 0; i < M; ++i) red[(j >> 5) * M + i] = v[i];
+  for (int i = 0; i < M2; ++i) u[i] = i < M ? v[i] : (S)0;
+#pragma unroll
+  for (int lv = 0; lv < 5; ++lv) {
+    const int o = 16 >> lv;
+    const int c = M2 >> lv;  // values still held per lane at this level (compile time after unrolling)
+    if (c > 1) {
+      const bool hi = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < c / 2; ++i) {
+        const S send = hi ? u[i] : u[i + c / 2];
+        const S keep = hi ? u[i + c / 2] : u[i];
+        u[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    } else {
+      u[0] += __shfl_xor_sync(0xffffffffu, u[0], o);
+    }
+  }
+  constexpr int G = 32 / M2;  // lanes holding the same total
+  if ((lane & (G - 1)) == 0) red[(j >> 5) * M2 + lane / G] = u[0];
   __syncthreads();
+  S t = (S)0;
 #pragma unroll
-  for (int i = 0; i < M; ++i) v[i] = lane < NW ? red[lane * M + i] : (S)0;
+  for (int w = 0; w < NW; ++w) t += red[w * M2 + (lane & (M2 - 1))];
 #pragma unroll
-  for (int o = NW / 2; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-#pragma unroll
-  for (int i = 0; i < M; ++i) v[i] = __shfl_sync(0xffffffffu, v[i], 0);
-}
-
-// The same reduction split in two halves around a barrier the caller already has:
-// warp_sum (all lanes get the warp total; lane 0 publishes it) ... __syncthreads() ... block_collect.
-template <int M, typename S>
-__device__ __forceinline__ void warp_publish(S (&v)[M], S* red, int j) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-  if ((j & 31) == 0)
-#pragma unroll
-    for (int i = 0; i < M; ++i) red[(j >> 5) * M + i] = v[i];
-}
-template <int NW, int M, typename S>
-__device__ __forceinline__ void block_collect(S (&v)[M], const S* red, int j) {
-  const int lane = j & 31;
-#pragma unroll
-  for (int i = 0; i < M; ++i) v[i] = lane < NW ? red[lane * M + i] : (S)0;
-#pragma unroll
-  for (int o = NW / 2; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-#pragma unroll
-  for (int i = 0; i < M; ++i) v[i] = __shfl_sync(0xffffffffu, v[i], 0);
+  for (int i = 0; i < M; ++i) v[i] = __shfl_sync(0xffffffffu, t, i);
 }
 
 // e_i = a_i^E, E a compile-time constant: the addition chain is fixed at compile time.
@@ -353,7 +349,10 @@ __device__ __forceinline__ void upow(S (&e)[M], const S (&a)[M], int ex) {
 // ------------------------------------------------------------------ the kernel body
 // CAP > 0: a compile-time max_inner (the first probe's power chain is fixed at compile time);
 // CAP = 0: runtime max_inner.
-template <typename Real, int NC, int CAP = 0>
+// TAB: the per-L eigenvalue table is set (Params::wtab != nullptr): the window spectrum is read, never
+// evaluated, so the closed-form code and its 1/sin table are compiled out (the smaller shared-memory
+// footprint leaves more of the SM's L1 to the twiddle / table loads and the register spills).
+template <typename Real, int NC, int CAP = 0, bool TAB = false>
 struct Resident {
   using V = typename Cx<Real>::V;
   static constexpr int n = 2 * NC;
@@ -370,16 +369,18 @@ struct Resident {
   static constexpr size_t off_bufA = 0;
   static constexpr size_t off_bufB = off_bufA + sizeof(V) * PADN;
   static constexpr size_t off_sin = off_bufB + sizeof(V) * PADN;
-  static constexpr size_t off_isin = off_sin + sizeof(Real) * ((NC + 2) & ~1);
-  static constexpr size_t off_red = off_isin + sizeof(Real) * ((NC + 2) & ~1);  // 2 slots x 4*NW doubles
+  static constexpr size_t off_red = off_sin + sizeof(Real) * ((NC + 2) & ~1);   // 2 slots x 4*NW doubles
   static constexpr size_t off_nbr = off_red + sizeof(double) * 8 * NW;         // NW*R V
   static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // 2 NW + 8 ints
-  static constexpr size_t smem_bytes = off_int + sizeof(int) * (4 * NW + 8);
+  static constexpr size_t off_isin = (off_int + sizeof(int) * (4 * NW + 8) + 15) & ~(size_t)15;  // last: absent if TAB
+  static constexpr size_t smem_bytes = TAB ? off_isin : off_isin + sizeof(Real) * ((NC + 2) & ~1);
 
   struct Smem {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
-    const Real* wtab;  // per-L eigenvalue table (row L - 2, bins 0..NC) or nullptr
+    const void* wtab;  // per-L eigenvalue table (Params::wtab) or nullptr
   };
+  // fp64: the table rows hold {w_hat, a^(cap-1)} pairs (TabE); fp32: w_hat only
+  static constexpr bool kWE = sizeof(Real) == 8;
 
   // group layout: bin index of spectrum register q for thread j
   __device__ static int g2_of(int j) { return j == 0 ? NC / 8 : G - j; }
@@ -674,45 +675,65 @@ struct Resident {
   // block-uniform step B = pi L/8: sin(A + qB) = sA cos qB + cA sin qB (group 1) and
   // sin((q+1)B - A) (group 2, g2 = n/8 - j), so only (sA, cA) are per-thread table gathers.
   __device__ static void bin_w_all(const Smem& sm, int L, Real invL, int j, double (&w)[NB]) {
-    if (sm.wtab) {  // precomputed eigenvalues of this scaling, filled by fif_wtab_kernel
-      const Real* row = sm.wtab + (size_t)(L - 2) * (NC + 1);
+    if constexpr (TAB) {  // precomputed eigenvalues of this scaling, filled by fif_wtab_kernel
+      if constexpr (kWE) {
+        const double* row = reinterpret_cast<const double*>(wtab_row(sm, L));  // .x of the {w, e} pairs
 #pragma unroll
-      for (int q = 0; q < R; ++q) w[q] = (double)__ldg(row + bin_of(j, q));
-      w[R] = (double)__ldg(row + NC);
+        for (int q = 0; q < R; ++q) w[q] = __ldg(row + 2 * bin_of(j, q));
+        w[R] = __ldg(row + 2 * NC);
+      } else {
+        const Real* row = reinterpret_cast<const Real*>(sm.wtab) + (size_t)(L - 2) * (NC + 1);
+#pragma unroll
+        for (int q = 0; q < R; ++q) w[q] = (double)__ldg(row + bin_of(j, q));
+        w[R] = (double)__ldg(row + NC);
+      }
       return;
-    }
-    Real cq[5], sq[5];
+    } else {
+      Real cq[5], sq[5];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) {  // qB = pi (qL mod 16) (n/8) / n: uniform addresses (broadcasts)
-      const unsigned m = ((unsigned)(q * L) & 15u) * (unsigned)(n / 8);
-      sq[q] = ssin(sm, m);
-      cq[q] = scos(sm, m);
-    }
-    const unsigned mA = (unsigned)L * (unsigned)j;
-    const Real sA = ssin(sm, mA), cA = scos(sm, mA);
-    Real sA2 = sA, cA2 = cA;
-    if (j == 0) {  // g2 = n/16: angle (q + 1/2) B = (q+1)B - B/2
-      const unsigned mh = ((unsigned)L & 31u) * (unsigned)(n / 16);
-      sA2 = ssin(sm, mh);
-      cA2 = scos(sm, mh);
-    }
+      for (int q = 0; q < 5; ++q) {  // qB = pi (qL mod 16) (n/8) / n: uniform addresses (broadcasts)
+        const unsigned m = ((unsigned)(q * L) & 15u) * (unsigned)(n / 8);
+        sq[q] = ssin(sm, m);
+        cq[q] = scos(sm, m);
+      }
+      const unsigned mA = (unsigned)L * (unsigned)j;
+      const Real sA = ssin(sm, mA), cA = scos(sm, mA);
+      Real sA2 = sA, cA2 = cA;
+      if (j == 0) {  // g2 = n/16: angle (q + 1/2) B = (q+1)B - B/2
+        const unsigned mh = ((unsigned)L & 31u) * (unsigned)(n / 16);
+        sA2 = ssin(sm, mh);
+        cA2 = scos(sm, mh);
+      }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const Real n1 = sA * cq[q] + cA * sq[q];              // sin(A + qB)
-      const Real n2 = sq[q + 1] * cA2 - cq[q + 1] * sA2;    // sin((q+1)B - A2)
-      const Real s1 = n1 * sm.isin[bin_of(j, q)] * invL;
-      const Real s2 = n2 * sm.isin[bin_of(j, q + 4)] * invL;
-      const Real t1 = s1 * s1, t2 = s2 * s2;
-      w[q] = (double)(t1 * t1);
-      w[q + 4] = (double)(t2 * t2);
+      for (int q = 0; q < 4; ++q) {
+        const Real n1 = sA * cq[q] + cA * sq[q];              // sin(A + qB)
+        const Real n2 = sq[q + 1] * cA2 - cq[q + 1] * sA2;    // sin((q+1)B - A2)
+        const Real s1 = n1 * sm.isin[bin_of(j, q)] * invL;
+        const Real s2 = n2 * sm.isin[bin_of(j, q + 4)] * invL;
+        const Real t1 = s1 * s1, t2 = s2 * s2;
+        w[q] = (double)(t1 * t1);
+        w[q + 4] = (double)(t2 * t2);
+      }
+      if (j == 0) w[0] = 1.0;  // bin 0: w_hat_0 = 1 (rows sum to 1)
+      w[R] = (double)what(sm, L, invL, NC);
     }
-    if (j == 0) w[0] = 1.0;  // bin 0: w_hat_0 = 1 (rows sum to 1)
-    w[R] = (double)what(sm, L, invL, NC);
   }
+  __device__ static const double2* wtab_row(const Smem& sm, int L) {
+    return reinterpret_cast<const double2*>(sm.wtab) + (size_t)(L - 2) * (NC + 1);
+  }
+  // |X_k|^2 c_k / 2 (the factor 2 is applied to the thread's sums); explicit roundings so that every
+  // code path (closed form, table, test hooks) accumulates bit-identical values
   __device__ static double bin_p1(const V (&X)[R], const V& Xn, int j, int q) {
-    if (q == R) return (j == 0) ? 0.5 * ((double)Xn.x * (double)Xn.x) : 0.0;  // X_NC real, weight 1
-    const double p = (double)X[q].x * (double)X[q].x + (double)X[q].y * (double)X[q].y;
-    return (q == 0 && j == 0) ? 0.5 * p : p;                                   // X_0 weight 1
+    if (q == R) return (j == 0) ? 0.5 * __dmul_rn((double)Xn.x, (double)Xn.x) : 0.0;  // X_NC real, weight 1
+    const double p = __fma_rn((double)X[q].x, (double)X[q].x, __dmul_rn((double)X[q].y, (double)X[q].y));
+    return (q == 0 && j == 0) ? 0.5 * p : p;                                          // X_0 weight 1
+  }
+  // one bin of a probe: e = a^(N-1) -> P += p e^2, Q += p e^2 w^2, d = e a = a^N
+  __device__ static void accum_bin(double p1, double w, double e, double& P, double& Q, double& d) {
+    const double px = __dmul_rn(p1, __dmul_rn(e, e));
+    P = __dadd_rn(P, px);
+    Q = __fma_rn(px, __dmul_rn(w, w), Q);
+    d = __dmul_rn(e, __dsub_rn(1.0, w));
   }
 
   // One fp64 probe at N: (P, Q) block totals and d_k = a_k^N.  ECT >= 0: N - 1 == ECT at compile time.
@@ -724,7 +745,8 @@ struct Resident {
     block_sum<NW, 2>(v, red, j);
     P = v[0]; Q = v[1];
   }
-  // the thread's share of (P, Q) (not reduced) and d_k = a_k^N
+  // the thread's share of (P, Q) (not reduced) and d_k = a_k^N.  Bins q = 0..7 in two groups of 4
+  // (register pressure), then the Nyquist bin on thread 0 only; d[R] = 0 elsewhere.
   template <int ECT = -1>
   __device__ static void probe_part(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N,
                                     double (&v)[2], double (&d)[NB], int j) {
@@ -733,94 +755,123 @@ struct Resident {
     bin_w_all(sm, L, invL, j, wall);
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
-      constexpr int M = 5;
-      double w[M], a[M], e[M];
+      constexpr int M = 4;
+      double a[M], e[M];
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const int q = glo(g) + i;
-        w[i] = q < ghi(g) ? wall[q] : 1.0;
-        a[i] = 1.0 - w[i];
-      }
+      for (int i = 0; i < M; ++i) a[i] = 1.0 - wall[4 * g + i];
       if constexpr (ECT >= 0) upow_ct<ECT>(e, a); else upow<M>(e, a, N - 1);
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const int q = glo(g) + i;
-        if (q < ghi(g)) {
-          const double px = bin_p1(X, Xn, j, q) * (e[i] * e[i]);
-          v[0] += px;
-          v[1] += px * (w[i] * w[i]);
-          d[q] = e[i] * a[i];
-        }
-      }
+      for (int i = 0; i < M; ++i) accum_bin(bin_p1(X, Xn, j, 4 * g + i), wall[4 * g + i], e[i], v[0], v[1], d[4 * g + i]);
+    }
+    d[R] = 0.0;
+    if (j == 0) {
+      double a[1] = {1.0 - wall[R]}, e[1];
+      if constexpr (ECT >= 0) upow_ct<ECT>(e, a); else upow<1>(e, a, N - 1);
+      accum_bin(bin_p1(X, Xn, 0, R), wall[R], e[0], v[0], v[1], d[R]);
+    }
+    v[0] *= 2.0; v[1] *= 2.0;
+  }
+  // The cap probe from the per-L table (fp64): e = a^(cap-1) is read, not computed;
+  // the same accumulation as probe_part<cap-1>, so the result is bit-identical.
+  __device__ static void probe_cap_tab(const V (&X)[R], const V& Xn, const Smem& sm, int L, double (&v)[2],
+                                       double (&d)[NB], int j) {
+    const double2* row = wtab_row(sm, L);
+    double2 we[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) we[q] = __ldg(row + bin_of(j, q));
+    v[0] = 0.0; v[1] = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) accum_bin(bin_p1(X, Xn, j, q), we[q].x, we[q].y, v[0], v[1], d[q]);
+    d[R] = 0.0;
+    if (j == 0) {
+      const double2 wn = __ldg(row + NC);
+      accum_bin(bin_p1(X, Xn, 0, R), wn.x, wn.y, v[0], v[1], d[R]);
     }
     v[0] *= 2.0; v[1] *= 2.0;
   }
 
-  // fp32 hint for the minimal passing N in [1, hi] (bisection on fp32 sums, powers through the SFU:
-  // a^(2(N-1)) = ex2(2(N-1) lg2 a)); only a hint: the caller verifies it in fp64.
+  // fp32 hint for the minimal passing N in [1, hi] (pass(hi) known): a 4-ary search on fp32 sums, three
+  // probes lo + D, lo + 2D, lo + 3D per round (4 rounds for hi = 200 instead of 8 bisection rounds: half
+  // the block reductions); powers through the SFU, a^(2(m-1)) = ex2(2(m-1) lg2 a), the next two probes
+  // by multiplying with a^(2D).  Only a hint: the caller verifies it in fp64 (and falls back to an fp64
+  // bisection), so neither its rounding nor its order decides N.
   __device__ static float lg2f(float x) { float y; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
   __device__ static float ex2f(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
   __device__ static int hint_fp32(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int hi,
-                                  float delta2, float* red, int j) {
+                                  float delta2, int& slot, int j) {
     float l2[NB], pk[NB], pw[NB];
     double wall[NB];
     bin_w_all(sm, L, invL, j, wall);
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
       const double w = wall[q], p64 = bin_p1(X, Xn, j, q);
-      l2[q] = fmaxf(2.0f * lg2f(fmaxf((float)(1.0 - w), 0.0f)), -1e30f);  // finite: 0 * l2 = 0 at N = 1
+      l2[q] = fmaxf(2.0f * lg2f(fmaxf((float)(1.0 - w), 0.0f)), -1e30f);  // finite: 0 * l2 = 0 at m = 1
       pk[q] = (float)p64;
       pw[q] = (float)(p64 * w * w);
     }
     int lo = 0;
     while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      const float t = (float)(mid - 1);
-      float v[2] = {0.f, 0.f};
+      const int D = (hi - lo + 3) >> 2;
+      const float t1 = (float)(lo + D - 1), tD = (float)D;
+      float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        const float x = ex2f(t * l2[i]);
-        v[0] += pk[i] * x;
-        v[1] += pw[i] * x;
+        if (i == R && j != 0) break;  // the Nyquist bin lives on thread 0
+        const float x1 = ex2f(t1 * l2[i]), st = ex2f(tD * l2[i]);
+        const float x2 = x1 * st, x3 = x2 * st;
+        v[0] += pk[i] * x1; v[1] += pw[i] * x1;
+        v[2] += pk[i] * x2; v[3] += pw[i] * x2;
+        v[4] += pk[i] * x3; v[5] += pw[i] * x3;
       }
-      block_sum<NW, 2>(v, red, j);
-      if (v[1] <= delta2 * v[0]) hi = mid; else lo = mid;
+      float* red = reinterpret_cast<float*>(sm.red + slot * 4 * NW);
+      slot ^= 1;
+      block_sum<NW, 6>(v, red, j);
+      int nlo = lo, nhi = hi;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int m = lo + (i + 1) * D;
+        if (m >= hi) break;
+        if (v[2 * i + 1] <= delta2 * v[2 * i]) { nhi = m; break; }
+        nlo = m;
+      }
+      lo = nlo; hi = nhi;
     }
     return hi;
   }
 
   // fp64 check of pass(N-1) (N > 1) and pass(N) in one pass; d_k = a_k^N.
+  __device__ static void verify_bin(double p1, double w, double a, double e, int N, double (&v)[4], double& d) {
+    // e = a^(N-2) (N > 1) or 1 (N = 1)
+    const double w2 = __dmul_rn(w, w);
+    const double e1 = N > 1 ? __dmul_rn(e, a) : e;  // a^(N-1)
+    const double x0 = __dmul_rn(p1, __dmul_rn(e, e)), x1 = __dmul_rn(p1, __dmul_rn(e1, e1));
+    v[0] = __dadd_rn(v[0], x0);
+    v[1] = __fma_rn(x0, w2, v[1]);
+    v[2] = __dadd_rn(v[2], x1);
+    v[3] = __fma_rn(x1, w2, v[3]);
+    d = __dmul_rn(e1, a);
+  }
   __device__ static void verify(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N,
                                 double delta2, bool& pass_lo, bool& pass_hi, double (&d)[NB], double* red, int j) {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     double wall[NB];
     bin_w_all(sm, L, invL, j, wall);
+    const int ex = N > 1 ? N - 2 : 0;
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
-      constexpr int M = 5;
-      double w[M], a[M], e[M];
+      constexpr int M = 4;
+      double a[M], e[M];
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const int q = glo(g) + i;
-        w[i] = q < ghi(g) ? wall[q] : 1.0;
-        a[i] = 1.0 - w[i];
-      }
-      upow<M>(e, a, N > 1 ? N - 2 : 0);  // a^(N-2)
+      for (int i = 0; i < M; ++i) a[i] = 1.0 - wall[4 * g + i];
+      upow<M>(e, a, ex);  // a^(N-2)
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const int q = glo(g) + i;
-        if (q < ghi(g)) {
-          const double pk = bin_p1(X, Xn, j, q);
-          const double w2 = w[i] * w[i];
-          const double e1 = N > 1 ? e[i] * a[i] : e[i];  // a^(N-1)
-          const double x0 = pk * (e[i] * e[i]), x1 = pk * (e1 * e1);
-          v[0] += x0;
-          v[1] += x0 * w2;
-          v[2] += x1;
-          v[3] += x1 * w2;
-          d[q] = e1 * a[i];
-        }
-      }
+      for (int i = 0; i < M; ++i) verify_bin(bin_p1(X, Xn, j, 4 * g + i), wall[4 * g + i], a[i], e[i], N, v, d[4 * g + i]);
+    }
+    d[R] = 0.0;
+    if (j == 0) {
+      double a[1] = {1.0 - wall[R]}, e[1];
+      upow<1>(e, a, ex);
+      verify_bin(bin_p1(X, Xn, 0, R), wall[R], a[0], e[0], N, v, d[R]);
     }
     block_sum<NW, 4>(v, red, j);
     pass_lo = (N > 1) && (v[1] <= delta2 * v[0]);
@@ -832,10 +883,8 @@ struct Resident {
   __device__ static int search_below_cap(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL,
                                          const Params& p, double (&dd)[NB], int& slot, int j) {
     const int cap = p.max_inner;
+    const int Nh = hint_fp32(X, Xn, sm, L, invL, cap, (float)p.delta2, slot, j);
     double* red = sm.red + slot * 4 * NW;
-    slot ^= 1;
-    const int Nh = hint_fp32(X, Xn, sm, L, invL, cap, (float)p.delta2, reinterpret_cast<float*>(red), j);
-    red = sm.red + slot * 4 * NW;
     slot ^= 1;
     bool plo, phi;
     verify(X, Xn, sm, L, invL, Nh, p.delta2, plo, phi, dd, red, j);
@@ -885,8 +934,16 @@ struct Resident {
       slot ^= 1;
       verify(X, Xn, sm, L, invL, N, p.delta2, lo, hi, dd, red2, j);
     } else {
-      if constexpr (CAP > 0) probe<CAP - 1>(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
-      else probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+      if constexpr (kWE && TAB) {
+        double v[2];
+        probe_cap_tab(X, Xn, sm, L, v, dd, j);
+        block_sum<NW, 2>(v, red, j);
+        Pv = v[0]; Qv = v[1];
+      } else if constexpr (CAP > 0) {
+        probe<CAP - 1>(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+      } else {
+        probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
+      }
       if (Qv <= p.delta2 * Pv) N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
     }
     if (p.gamma > 0.0) {  // gamma-threshold: (1 - w)^N >= 1 - gamma -> factor 1 (A19)
@@ -1035,7 +1092,6 @@ struct Resident {
         L = filter_half_length(p, k);
       }
       const Real invL = (Real)1 / (Real)L;
-#if FIF_SPEC == 0
       V v[R], Dn{0, 0};
       int N;
       {
@@ -1052,57 +1108,6 @@ struct Resident {
         }
         irfft(v, Dn, sm, tw, last, j);
       }
-#else
-      // a5, speculative: the cap probe's block reduction is completed at the barrier that
-      // follows the first inverse pass, which already assumes N = cap (the common case); if
-      // SD(cap) <= delta the speculative work is dropped and X restored.
-      double part[2], dd[NB];
-      if constexpr (CAP > 0) probe_part<CAP - 1>(X, Xn, sm, L, invL, p.max_inner, part, dd, j);
-      else probe_part(X, Xn, sm, L, invL, p.max_inner, part, dd, j);
-      double* red = sm.red + slot * 4 * NW;
-      slot ^= 1;
-      warp_publish<2>(part, red, j);
-      V* stash = last;  // not read by anyone until the next write phase: holds X_old
-#pragma unroll
-      for (int q = 0; q < R; ++q) stash[j + T * q] = X[q];
-      const V Xn_old = Xn;
-      // a6 damping: D = d X / n (IMF spectrum), X <- (1 - d) X
-      V v[R], Dn{0, 0};
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        v[q] = cscale(X[q], (Real)dd[q] * invn);
-        X[q] = cscale(X[q], (Real)1 - (Real)dd[q]);
-      }
-      if (j == 0) {
-        Dn = cscale(Xn, (Real)dd[R] * invn);
-        Xn = cscale(Xn, (Real)1 - (Real)dd[R]);
-      }
-      V* zb = (last == sm.bufA) ? sm.bufB : sm.bufA;
-      irfft_p0(v, Dn, sm, zb, j);
-      __syncthreads();
-      block_collect<NW, 2>(part, red, j);
-      int N = p.max_inner;
-      if (part[1] <= p.delta2 * part[0]) {
-        // rare: the minimal passing N is below the cap
-#pragma unroll
-        for (int q = 0; q < R; ++q) X[q] = stash[j + T * q];
-        Xn = Xn_old;
-        N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          v[q] = cscale(X[q], (Real)dd[q] * invn);
-          X[q] = cscale(X[q], (Real)1 - (Real)dd[q]);
-        }
-        if (j == 0) {
-          Dn = cscale(Xn, (Real)dd[R] * invn);
-          Xn = cscale(Xn, (Real)1 - (Real)dd[R]);
-        }
-        last = zb;
-        irfft(v, Dn, sm, tw, last, j);
-      } else {
-        last = irfft_rest(v, sm, tw, zb, j);
-      }
-#endif
       Real* o = out + (size_t)M * slot_stride;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
@@ -1111,7 +1116,7 @@ struct Resident {
       }
       if (j == 0) { lens[M] = 2 * L; iters[M] = N; }
       ++M;
-      k = extrema(rt, sm, last, j);
+      if (M < p.max_imfs) k = extrema(rt, sm, last, j);  // (not needed after the last IMF)
     }
     // trend in slot M, zeros after (A12)
 #pragma unroll
@@ -1128,7 +1133,7 @@ struct Resident {
     sm.bufA = reinterpret_cast<V*>(base + off_bufA);
     sm.bufB = reinterpret_cast<V*>(base + off_bufB);
     sm.sint = reinterpret_cast<Real*>(base + off_sin);
-    sm.isin = reinterpret_cast<Real*>(base + off_isin);
+    sm.isin = TAB ? nullptr : reinterpret_cast<Real*>(base + off_isin);
     sm.red = reinterpret_cast<double*>(base + off_red);
     sm.nbr = reinterpret_cast<V*>(base + off_nbr);
     sm.ired = reinterpret_cast<int*>(base + off_int);
@@ -1138,13 +1143,16 @@ struct Resident {
 
   __device__ static void load_tables(const Smem& sm, const Real* __restrict__ sintab, const Real* __restrict__ isintab,
                                      int j) {
-    for (int i = j; i <= NC; i += T) { sm.sint[i] = sintab[i]; sm.isin[i] = isintab[i]; }
+    for (int i = j; i <= NC; i += T) {
+      sm.sint[i] = sintab[i];
+      if constexpr (!TAB) sm.isin[i] = isintab[i];
+    }
     __syncthreads();
   }
 };
 
 // ------------------------------------------------------------------ kernels
-template <typename Real, int NC, int CAP>
+template <typename Real, int NC, int CAP, bool TAB>
 #ifndef FIF_WARPS_TARGET
 #define FIF_WARPS_TARGET 16  // register budget: this many warps per SM (0: FIF_MINB CTAs per SM)
 #endif
@@ -1154,10 +1162,10 @@ __global__ void __launch_bounds__(NC / kR, FIF_WARPS_TARGET > 0
 fif_resident_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32_t* __restrict__ count,
                     int32_t* __restrict__ lens, int32_t* __restrict__ iters, const Real* __restrict__ sintab,
                     const Real* __restrict__ isintab, const typename Cx<Real>::V* __restrict__ tw, Params p) {
-  using K = Resident<Real, NC, CAP>;
+  using K = Resident<Real, NC, CAP, TAB>;
   extern __shared__ __align__(16) char smem_raw[];
   typename K::Smem sm = K::carve(smem_raw);
-  sm.wtab = reinterpret_cast<const Real*>(p.wtab);
+  sm.wtab = TAB ? p.wtab : nullptr;
   const int j = threadIdx.x;
   K::load_tables(sm, sintab, isintab, j);
   int slot = 0;
@@ -1252,11 +1260,13 @@ __global__ void __launch_bounds__(NC / kR) fif_test_window_kernel(Real* __restri
 
 // Per-L eigenvalue table ("computing in advance the eigenvalues ... for every scaling"):
 // row L - 2 = w_hat_k, k = 0..NC, for L = 2 + blockIdx.x, by the very code the kernel evaluates
-// (bin_w_all), so a table-driven decomposition is bit-identical to the closed-form one.
-template <typename Real, int NC>
-__global__ void __launch_bounds__(NC / kR) fif_wtab_kernel(Real* __restrict__ tab, const Real* __restrict__ sintab,
-                                                         const Real* __restrict__ isintab) {
-  using K = Resident<Real, NC>;
+// (bin_w_all), so a table-driven decomposition is bit-identical to the closed-form one.  fp64 rows
+// also hold e_k = a_k^(cap-1), a = 1 - w_hat, by the power chain the cap probe evaluates (upow_ct for
+// the compile-time cap, upow otherwise): the probe then reads e instead of computing it.
+template <typename Real, int NC, int CAP>
+__global__ void __launch_bounds__(NC / kR) fif_wtab_kernel(void* __restrict__ tab, const Real* __restrict__ sintab,
+                                                         const Real* __restrict__ isintab, int cap) {
+  using K = Resident<Real, NC, CAP>;
   extern __shared__ __align__(16) char smem_raw[];
   const typename K::Smem sm = K::carve(smem_raw);
   const int j = threadIdx.x;
@@ -1265,9 +1275,19 @@ __global__ void __launch_bounds__(NC / kR) fif_wtab_kernel(Real* __restrict__ ta
   const Real invL = (Real)1 / (Real)L;
   double w[K::NB];
   K::bin_w_all(sm, L, invL, j, w);
-  Real* row = tab + (size_t)blockIdx.x * (NC + 1);
-  for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = (Real)w[q];
-  if (j == 0) row[NC] = (Real)w[kR];
+  if constexpr (K::kWE) {
+    double a[K::NB], e[K::NB];
+#pragma unroll
+    for (int q = 0; q < K::NB; ++q) a[q] = 1.0 - w[q];
+    if constexpr (CAP > 0) upow_ct<CAP - 1>(e, a); else upow<K::NB>(e, a, cap - 1);
+    double2* row = reinterpret_cast<double2*>(tab) + (size_t)blockIdx.x * (NC + 1);
+    for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = double2{w[q], e[q]};
+    if (j == 0) row[NC] = double2{w[kR], e[kR]};
+  } else {
+    Real* row = reinterpret_cast<Real*>(tab) + (size_t)blockIdx.x * (NC + 1);
+    for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = (Real)w[q];
+    if (j == 0) row[NC] = (Real)w[kR];
+  }
 }
 
 template <typename Real, int NC, int CAP>

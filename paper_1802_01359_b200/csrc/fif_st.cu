@@ -505,14 +505,19 @@ fif_status st_bind_workspace(fif_plan_s* p, void* base, size_t bytes) {
   const size_t need = st_workspace_bytes(p);
   if (base && bytes < need) return FIF_ERR_INVALID_ARG;
   if (cudaDeviceSynchronize() != cudaSuccess) return FIF_ERR_CUDA;
-  cudaFree(p->d_ws_own);
-  p->d_ws_own = nullptr;
-  p->d_ws_user = base;
-  p->ws_user_bytes = base ? bytes : 0;
+  // the new block first: on failure the plan keeps its current (valid) workspace and buffers
+  void* own = nullptr;
   if (!base) {
-    if (cudaMalloc(&p->d_ws_own, need) != cudaSuccess) return FIF_ERR_OOM;
-    base = p->d_ws_own;
+    if (cudaMalloc(&own, need) != cudaSuccess) {
+      cudaGetLastError();
+      return FIF_ERR_OOM;
+    }
+    base = own;
   }
+  cudaFree(p->d_ws_own);
+  p->d_ws_own = own;
+  p->d_ws_user = own ? nullptr : base;
+  p->ws_user_bytes = own ? 0 : bytes;
   char* w = (char*)base;
   p->d_X = w;
   p->d_Xn = w + p->ws_xn;
