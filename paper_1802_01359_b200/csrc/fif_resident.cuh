@@ -369,7 +369,8 @@ struct Resident {
   static constexpr size_t off_bufA = 0;
   static constexpr size_t off_bufB = off_bufA + sizeof(V) * PADN;
   static constexpr size_t off_sin = off_bufB + sizeof(V) * PADN;
-  static constexpr size_t off_red = off_sin + sizeof(Real) * ((NC + 2) & ~1);   // 2 slots x 4*NW doubles
+  // sin table: sin(pi j/n), j = 0..NC; table mode: only the even j (the real-FFT twiddles)
+  static constexpr size_t off_red = off_sin + sizeof(Real) * (((TAB ? NC / 2 : NC) + 2) & ~1);  // 2 x 4*NW doubles
   static constexpr size_t off_nbr = off_red + sizeof(double) * 8 * NW;         // NW*R V
   static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // 2 NW + 8 ints
   static constexpr size_t off_isin = (off_int + sizeof(int) * (4 * NW + 8) + 15) & ~(size_t)15;  // last: absent if TAB
@@ -959,12 +960,14 @@ struct Resident {
 
   // -------------------------------------------------------------- real-FFT pre/post processing
   // w(k) = e^{+2 pi i k/n} = (sin(pi (n/2 - 2k)/n), sin(pi 2k/n)), 0 <= k <= n/4
-  __device__ static V wk(const Smem& sm, int k) { return V{sm.sint[NC - 2 * k], sm.sint[2 * k]}; }
+  // sin(2 pi i / n) = sin(pi (2i) / n), 0 <= i <= NC/2: table mode keeps only these even entries
+  __device__ static Real sin2(const Smem& sm, int i) { return TAB ? sm.sint[i] : sm.sint[2 * i]; }
+  __device__ static V wk(const Smem& sm, int k) { return V{sin2(sm, NC / 2 - k), sin2(sm, k)}; }
   // e^{-2 pi i k/n} for 0 <= k < NC
   __device__ static V wfwd(const Smem& sm, int k) {
-    if (2 * k <= NC) return V{sm.sint[NC - 2 * k], -sm.sint[2 * k]};
+    if (2 * k <= NC) return V{sin2(sm, NC / 2 - k), -sin2(sm, k)};
     const int kk = NC - k;
-    return V{-sm.sint[NC - 2 * kk], -sm.sint[2 * kk]};
+    return V{-sin2(sm, NC / 2 - kk), -sin2(sm, kk)};
   }
   // inverse: from A = D_k, B = D_{NC-k} (pre-scaled by 1/n), w = e^{2 pi i k/n} -> Z_k, Z_{NC-k}
   __device__ static void pre_inverse(V A, V B, V w, V& Zk, V& Zmk) {
@@ -1144,7 +1147,8 @@ struct Resident {
   __device__ static void load_tables(const Smem& sm, const Real* __restrict__ sintab, const Real* __restrict__ isintab,
                                      int j) {
     for (int i = j; i <= NC; i += T) {
-      sm.sint[i] = sintab[i];
+      if (!TAB) sm.sint[i] = sintab[i];
+      else if (2 * i <= NC) sm.sint[i] = sintab[2 * i];
       if constexpr (!TAB) sm.isin[i] = isintab[i];
     }
     __syncthreads();
