@@ -48,6 +48,15 @@ struct Inst {
                                   (int)K::smem_bytes)) != cudaSuccess) return e;
     return cudaSuccess;
   }
+  static int occ_tab() {  // the table-mode instance's occupancy (its own register budget)
+    static int occ = [] {
+      int o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fif_resident_kernel<Real, NC, kFastCap, true>, K::T,
+                                                    KT::smem_bytes);
+      return o > 0 ? o : 1;
+    }();
+    return occ;
+  }
   static int occupancy() {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fif_resident_kernel<Real, NC, kFastCap, false>, K::T, K::smem_bytes);
@@ -57,11 +66,12 @@ struct Inst {
                         int64_t batch, cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
     prm.wtab = p->d_wtab;
-    const int64_t cap = (int64_t)p->num_sms * p->occ;
-    const int grid = (int)(batch < cap ? batch : cap);
+    prm.ltab = (const int32_t*)p->d_ltab;
     const bool fast = p->max_inner == kFastCap, tab = p->d_wtab != nullptr;
     auto kern = fast ? (tab ? fif_resident_kernel<Real, NC, kFastCap, true> : fif_resident_kernel<Real, NC, kFastCap, false>)
                      : (tab ? fif_resident_kernel<Real, NC, 0, true> : fif_resident_kernel<Real, NC, 0, false>);
+    const int64_t cap = (int64_t)p->num_sms * (tab ? occ_tab() : p->occ);  // persistent grid: one wave
+    const int grid = (int)(batch < cap ? batch : cap);
     kern<<<grid, K::T, tab ? KT::smem_bytes : K::smem_bytes, s>>>((const Real*)sig, (Real*)imfs, cnt, lens, its,
                                                                  (const Real*)p->d_sin, (const Real*)p->d_isin,
                                                                  (const V*)p->d_tw, prm);
@@ -93,6 +103,10 @@ struct Inst {
       fif_wtab_kernel<Real, NC, 0><<<nL, K::T, K::smem_bytes, s>>>(tab, (const Real*)p->d_sin, (const Real*)p->d_isin,
                                                                   p->max_inner);
   }
+  static void fill_ltab(const fif_plan_s* p, int32_t* tab, cudaStream_t s) {
+    Params prm{1, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
+    fif_ltab_kernel<Real, NC><<<(int)((p->n + 256) / 256), 256, 0, s>>>(tab, prm);
+  }
   static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
                          cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
@@ -113,7 +127,7 @@ template <typename Real, int NC>
 const ResOps* res_entry() {
   using I = Inst<Real, NC>;
   static const ResOps ops{&I::prepare,    &I::occupancy,  I::K::T,        I::K::smem_bytes, &I::decompose, &I::test_rfft,
-                          &I::test_irfft, &I::test_extrema, &I::test_window, &I::test_inner, &I::fill_wtab};
+                          &I::test_irfft, &I::test_extrema, &I::test_window, &I::test_inner, &I::fill_wtab, &I::fill_ltab};
   return &ops;
 }
 template <typename Real>

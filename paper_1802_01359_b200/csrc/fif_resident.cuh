@@ -40,6 +40,9 @@
 #ifndef FIF_EXT1
 #define FIF_EXT1 0
 #endif
+#ifndef FIF_TW_ALL
+#define FIF_TW_ALL 0  // every Stockham twiddle from the (L1-resident) table; 0: t^3, t^5..t^7 multiplied out
+#endif
 
 namespace fifgpu {
 
@@ -63,6 +66,9 @@ struct Params {
   // fp64 plans: double2 {w_hat_k, a_k^(max_inner-1)} (the cap probe's power chain precomputed by the
   // kernel's own code, bit-identical); fp32 plans: Real w_hat_k.
   const void* wtab = nullptr;
+  // a3 for every extrema count: ltab[k] = L(k), k = 0..n (fif_ltab_kernel: filter_half_length itself,
+  // bit-identical); nullptr: evaluated per IMF.  One cached load instead of an fp64 division per IMF.
+  const int32_t* ltab = nullptr;
 };
 
 // ------------------------------------------------------------------ a5 alternative: a-priori N0
@@ -198,7 +204,7 @@ __device__ __forceinline__ void stockham_pass(V (&v)[kR], const V* src, V* dst, 
     V w[RP];
 #pragma unroll
     for (int r = 0; r < RP; ++r) w[r] = v[u + r * VP];
-    if constexpr (NS > 1 && NS < 32) {  // few distinct twiddles per warp: table loads are broadcasts
+    if constexpr (NS > 1 && (NS < 32 || FIF_TW_ALL)) {  // table loads (few distinct per warp: broadcasts)
 #pragma unroll
       for (int r = 1; r < RP; ++r) {
         V t = __ldg(tw + (r - 1) * NS + k);
@@ -475,10 +481,13 @@ struct Resident {
     return total;
   }
 
+  // exponent field of a difference: 0 iff the difference is zero or subnormal (the exact rule then decides)
+  __device__ static unsigned expo(double d) { return (unsigned)__double2hiint(d) & 0x7ff00000u; }
+  __device__ static unsigned expo(float d) { return (unsigned)__float_as_int(d) & 0x7f800000u; }
   __device__ static int extrema2(const V (&rt)[R], const Smem& sm, V*& last, int j) {
     const int lane = j & 31, w = j >> 5;
     unsigned S0 = 0, S1 = 0;
-    bool zero = false;
+    unsigned emin = 0xffffffffu;  // min exponent field over the differences: 0 -> a zero (or subnormal) one
     Real xn[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) xn[q] = __shfl_down_sync(0xffffffffu, rt[q].x, 1);
@@ -486,7 +495,7 @@ struct Resident {
     for (int q = 0; q < R; ++q) {
       const Real d0 = rt[q].y - rt[q].x;
       S0 |= sgn_bit(d0) << q;
-      zero |= is_zero(d0);
+      emin = min(emin, expo(d0));
     }
     unsigned S2 = __shfl_down_sync(0xffffffffu, S0, 1);
     int* nmask = sm.ired + NW + 1;
@@ -512,12 +521,12 @@ struct Resident {
     for (int q = 0; q < R; ++q) {
       const Real d1 = xn[q] - rt[q].y;
       S1 |= sgn_bit(d1) << q;
-      zero |= ((valid >> q) & 1u) && is_zero(d1);
+      if ((valid >> q) & 1u) emin = min(emin, expo(d1));
     }
     int cnt = __popc((S0 ^ S1) & valid) + __popc((S1 ^ S2) & valid);
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if (lane == 0) sm.ired[w] = cnt;
-    const int anyzero = __syncthreads_or(zero);
+    const int anyzero = __syncthreads_or(emin == 0u);
     int total = 0;
 #pragma unroll
     for (int ww = 0; ww < NW; ++ww) total += sm.ired[ww];
@@ -1090,9 +1099,9 @@ struct Resident {
       if (p.mask == 1) {  // spectral-peak rule: L from k = 2 f* (A20)
         const int fs = spectral_peak(X, Xn, sm, last, slot, j);
         if (fs == 0) break;
-        L = filter_half_length(p, 2 * fs);
+        L = p.ltab ? __ldg(p.ltab + 2 * fs) : filter_half_length(p, 2 * fs);
       } else {
-        L = filter_half_length(p, k);
+        L = p.ltab ? __ldg(p.ltab + k) : filter_half_length(p, k);
       }
       const Real invL = (Real)1 / (Real)L;
       V v[R], Dn{0, 0};
@@ -1292,6 +1301,15 @@ __global__ void __launch_bounds__(NC / kR) fif_wtab_kernel(void* __restrict__ ta
     for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = (Real)w[q];
     if (j == 0) row[NC] = (Real)w[kR];
   }
+}
+
+// a3 table (reading A8 rule): L for every extrema count k = 2..n by the kernel's own
+// filter_half_length (so a table-driven decomposition is bit-identical); k < 2 never reaches a3.
+template <typename Real, int NC>
+__global__ void fif_ltab_kernel(int32_t* __restrict__ ltab, Params p) {
+  using K = Resident<Real, NC>;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= K::n; k += gridDim.x * blockDim.x)
+    ltab[k] = k >= 2 ? K::filter_half_length(p, k) : 0;
 }
 
 template <typename Real, int NC, int CAP>
