@@ -61,7 +61,9 @@ def lib():
         L.oracle_inner.argtypes = [dp, i64, i64, d, i32, dp, dp, ctypes.c_int]
         L.oracle_inner.restype = i32
         L.oracle_decompose_batch.argtypes = [dp, i64, i64, ctypes.c_int, d, d, i32, i32, dp, ip, ip, ip, ip, dp,
-                                             ctypes.c_int, ctypes.c_int]
+                                             ctypes.c_int, ctypes.c_int, d]
+        L.oracle_extrema_decision_margin.argtypes = [dp, i64, i64, d, d, d, d, ctypes.c_int, ctypes.c_int]
+        L.oracle_extrema_decision_margin.restype = d
         L.oracle_spectral_peak.argtypes = [dp, i64, dp]
         L.oracle_spectral_peak.restype = i64
         L.oracle_inner_n0.argtypes = [dp, i64, i64, d, i32, dp, dp, ctypes.c_int]
@@ -149,16 +151,26 @@ def inner_n0(r, L, delta, max_inner, parallel=False):
     return imf, int(N)
 
 
+def extrema_decision_margin(r, k, em, scale, tau, xi=1.6, window=WINDOW_TRI_SQ, mask=MASK_EXTREMA):
+    """Reading A21: +inf if the a2/a3 decision on r is robust to the f fragile differences (|diff| <= tau*scale,
+    k uncertain by +-2f), else em."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    return float(lib().oracle_extrema_decision_margin(_dp(r), r.shape[0], int(k), float(em), float(scale),
+                                                      float(tau), float(xi), int(window), int(mask)))
+
+
 def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, stop=STOP_SD,
-              mask=MASK_EXTREMA):
+              mask=MASK_EXTREMA, tau=1e-9):
     """Time-domain oracle decomposition of a batch [B, n] (or one signal [n]).
     stop = STOP_SD: the relative SD rule (reading A5); STOP_N0: the a-priori N0 of Thm DIF_conv_stop with
     the absolute delta (readings A16-A18).
 
     Returns dict: imfs [B, max_imfs+1, n], count [B], l [B, max_imfs], N [B, max_imfs],
     k [B, max_imfs+1] (extrema count at each outer step), margins [B, max_imfs+1, 2]
-    (per outer step m: margin of the extrema count at its head relative to max|s|, SD margin
-    |SD - delta|/delta of IMF m; NaN where no decision was taken)."""
+    (reading A21, DESIGN.md -- per outer step m: the margin of the a2/a3 decision at its head (+inf for
+    the first, taken on s itself, and for decisions robust to the differences below tau * max|s|, else
+    min |diff| / max|s|), and the SD margin |SD - delta|/delta * ||iterate|| / ||s|| of IMF m; NaN where
+    no decision was taken)."""
     s = np.ascontiguousarray(np.atleast_2d(np.asarray(signals, dtype=np.float64)))
     B, n = s.shape
     imfs = np.zeros((B, max_imfs + 1, n))
@@ -168,7 +180,8 @@ def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WI
     k = np.zeros((B, max_imfs + 1), dtype=np.int32)
     margins = np.zeros((B, max_imfs + 1, 2))
     lib().oracle_decompose_batch(_dp(s), B, n, int(window), float(xi), float(delta), int(max_inner), int(max_imfs),
-                                 _dp(imfs), _ip(count), _ip(l), _ip(N), _ip(k), _dp(margins), int(stop), int(mask))
+                                 _dp(imfs), _ip(count), _ip(l), _ip(N), _ip(k), _dp(margins), int(stop), int(mask),
+                                 float(tau))
     return {"imfs": imfs, "count": count, "l": l, "N": N, "k": k, "margins": margins}
 
 

@@ -132,7 +132,7 @@ def sd_curve(rhat: np.ndarray, lam: np.ndarray, n: int, max_inner: int) -> np.nd
 
 
 def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0, stop=STOP_SD,
-              mask=MASK_EXTREMA):
+              mask=MASK_EXTREMA, tau=1e-9):
     """Full FIF decomposition of one real signal.  Returns dict with imfs [(max_imfs+1), n]
     (trend in slot M), M, l (2L per IMF), N, k (extrema counts), sd (SD_N, SD_{N-1}).
     stop = STOP_N0: N = min(N0, max_inner) from the a-priori bound with the absolute delta (PAPER.md:599,
@@ -148,9 +148,19 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
     while M < max_imfs:
         k = count_extrema(r)
         ks.append(k)
-        dd = np.abs(np.diff(r))
-        dd = dd[dd > 0]
-        margins[M, 0] = (dd.min() / scale) if (dd.size and scale > 0) else np.inf
+        ad = np.abs(np.diff(r))
+        dd = ad[ad > 0]
+        em = (dd.min() / scale) if (dd.size and scale > 0) else np.inf
+        # reading A21: the first decision is on s itself; later ones are robust unless the f
+        # fragile differences (|diff| <= tau max|s|, k uncertain by +-2f) could change the a3 outcome
+        if M == 0:
+            margins[M, 0] = np.inf
+        else:
+            f = int(np.count_nonzero(ad <= tau * scale))
+            robust = f == 0 or (k >= 2 and k - 2 * f >= 2 and (
+                mask == MASK_SPECTRAL or
+                filter_half_length(xi, n, k - 2 * f, window) == filter_half_length(xi, n, k + 2 * f, window)))
+            margins[M, 0] = np.inf if (robust and f > 0) else em
         if k < 2:
             break
         rhat = np.fft.rfft(r)
@@ -202,7 +212,7 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
 
 
 def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0,
-                    stop=STOP_SD, mask=MASK_EXTREMA):
+                    stop=STOP_SD, mask=MASK_EXTREMA, tau=1e-9):
     """CPU-DF over a batch, returned in the TD oracle's dict layout (imfs, count, l, N, margins)."""
     S = np.atleast_2d(np.asarray(signals, dtype=np.float64))
     B, n = S.shape
@@ -210,7 +220,7 @@ def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, win
            "l": np.zeros((B, max_imfs), np.int32), "N": np.zeros((B, max_imfs), np.int32),
            "margins": np.full((B, max_imfs + 1, 2), np.nan)}
     for b in range(B):
-        d = decompose(S[b], xi, delta, max_inner, max_imfs, window, gamma, stop, mask)
+        d = decompose(S[b], xi, delta, max_inner, max_imfs, window, gamma, stop, mask, tau)
         M = d["M"]
         out["imfs"][b] = d["imfs"]
         out["count"][b] = M

@@ -78,6 +78,29 @@ int64_t oracle_count_extrema(const double* r, int64_t n, double scale, double* m
 }
 
 /* ---------------------------------------------------------------------------
+ * Decision margin of the a2/a3 step (reading A21): f = number of differences
+ * r_{j+1} - r_j with |.| <= tau * scale (zeros included) -- those whose sign (or zero-ness) two
+ * correct implementations may see differently on a remainder computed with other rounding.  Each such
+ * difference changes the count by at most 2, so k' lies in [k - 2f, k + 2f].  The decision (stop when
+ * k < 2, else L(k)) is ROBUST if it is the same for every k' in that range (L is monotone in k: the
+ * end points decide).  Returns +INFINITY when robust, else the plain margin em.
+ * ------------------------------------------------------------------------- */
+int64_t oracle_filter_half_length(double xi, int64_t n, int64_t k, int window);
+double oracle_extrema_decision_margin(const double* r, int64_t n, int64_t k, double em, double scale, double tau,
+                                      double xi, int window, int mask_rule) {
+  int64_t f = 0;
+  for (int64_t j = 0; j + 1 < n; ++j)
+    if (fabs(r[j + 1] - r[j]) <= tau * scale) ++f;
+  if (f == 0) return em;
+  if (k < 2) return em;                              /* k < 2 with fragile differences: not robust */
+  const int64_t klo = k - 2 * f, khi = k + 2 * f;
+  if (klo < 2) return em;                            /* the stop decision could differ */
+  if (mask_rule) return INFINITY;                    /* the spectral rule only uses the stop decision */
+  if (oracle_filter_half_length(xi, n, klo, window) != oracle_filter_half_length(xi, n, khi, window)) return em;
+  return INFINITY;
+}
+
+/* ---------------------------------------------------------------------------
  * Filter half-length L of h (readings A1, A3, A8).  Mask length reported to the
  * user is l = 2L (PAPER.md:81 l := 2 floor(nu N / k)).
  * ------------------------------------------------------------------------- */
@@ -303,7 +326,7 @@ int32_t oracle_inner(const double* r, int64_t n, int64_t L, double delta, int32_
  * ------------------------------------------------------------------------- */
 int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, double delta, int32_t max_inner,
                              int32_t max_imfs, double* imfs, int32_t* l_out, int32_t* N_out, int32_t* k_out,
-                             double* margins, int par, int stop, int mask_rule) {
+                             double* margins, int par, int stop, int mask_rule, double tau) {
   double* r = (double*)malloc(sizeof(double) * (size_t)n);
   memcpy(r, s, sizeof(double) * (size_t)n);
   memset(imfs, 0, sizeof(double) * (size_t)n * (size_t)(max_imfs + 1));
@@ -318,7 +341,11 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
     double em;
     int64_t k = oracle_count_extrema(r, n, scale, &em);
     if (k_out) k_out[M] = (int32_t)k;
-    if (margins) margins[2 * M] = em;
+    /* reading A21: the first count is taken on s itself (the same IEEE differences on any implementation);
+       later ones on remainders, robust unless fragile differences could change the a3 outcome */
+    if (margins) margins[2 * M] = (M == 0) ? INFINITY
+                                           : oracle_extrema_decision_margin(r, n, k, em, scale, tau, xi, window,
+                                                                            mask_rule);
     if (k < 2) break; /* trend: fewer than 2 extrema */
     int64_t L;
     if (mask_rule) {  /* spectral-peak rule (A20): L from k = 2 f* */
@@ -364,7 +391,7 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
  * stencil when batch == 1).  Non-finite input -> count = -1, outputs zeroed. */
 void oracle_decompose_batch(const double* s, int64_t batch, int64_t n, int window, double xi, double delta,
                             int32_t max_inner, int32_t max_imfs, double* imfs, int32_t* counts, int32_t* l_out,
-                            int32_t* N_out, int32_t* k_out, double* margins, int stop, int mask_rule) {
+                            int32_t* N_out, int32_t* k_out, double* margins, int stop, int mask_rule, double tau) {
   int par_inner = (batch == 1);
 #pragma omp parallel for schedule(dynamic, 1) if (batch > 1)
   for (int64_t b = 0; b < batch; ++b) {
@@ -384,7 +411,7 @@ void oracle_decompose_batch(const double* s, int64_t batch, int64_t n, int windo
       continue;
     }
     counts[b] = oracle_decompose_one(sb, n, window, xi, delta, max_inner, max_imfs, ib, lb, nb, kb, mb, par_inner,
-                                     stop, mask_rule);
+                                     stop, mask_rule, tau);
   }
 }
 

@@ -99,3 +99,33 @@ def test_cfg3_time_blocks_and_uid_broadcast(tmp_path):
     np.testing.assert_array_equal(np.concatenate(blocks), full)
     for r in range(world):
         assert (tmp_path / f"u{r}.bin").read_bytes() == bytes(range(128))
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` WITHOUT torchrun re-launches itself with 2 ranks (gloo on the reference arm here):
+    both ranks report in, rank 0 alone prints the JSON line, and it carries n_gpus = 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["OMP_NUM_THREADS"] = "2"
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg0", "--steps", "1",
+           "--warmup", "1", "--gpus", "2"]
+    p = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "launching 2 ranks" in p.stderr
+    for r in range(2):
+        assert f"[bench] rank {r}/2" in p.stderr, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    import json
+
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_gpus_flag_must_match_world_size():
+    """Under torchrun, --gpus must equal WORLD_SIZE (the line's n_gpus is the real rank count)."""
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"), "--impl", "reference",
+           "--config", "cfg0", "--steps", "1", "--warmup", "1", "--gpus", "3"]
+    p = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert p.returncode != 0
+    assert "--gpus 3 but WORLD_SIZE=2" in p.stderr

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 import oracle  # noqa: E402
 from oracle import direct_form as df  # noqa: E402
 from paper_1802_01359_b200 import fif, signals  # noqa: E402
-from test_gpu_parity import assert_parity, run_gpu  # noqa: E402
+from test_gpu_parity import TAU, assert_parity, run_gpu  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -89,7 +89,7 @@ def test_dist_fp32():
     s32 = signals.cfg4_signal(n, 3)
     gpu = run_dist(s32, P, "f32")
     s64 = s32.astype(np.float64)
-    ref = df.decompose_batch(s64[None])
+    ref = df.decompose_batch(s64[None], tau=TAU["f32"])
     assert_parity(s64, gpu, ref, 0, 0, "f32")
 
 

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import direct_form as df  # noqa: E402
 from paper_1802_01359_b200 import fif, signals  # noqa: E402
-from test_gpu_parity import assert_parity  # noqa: E402
+from test_gpu_parity import TAU, assert_parity  # noqa: E402
 
 LENGTHS = [512, 1024, 2048, 4096, 8192, 3 * 1024, 5 * 1024, 3 * 5 * 512, 9 * 1024, 16384, 25 * 512, 3 * 8192]
 
@@ -78,7 +78,8 @@ def test_fuzz_vs_direct_form(seed, monkeypatch):
     plan.close()
     s64 = s.astype(np.float64)
     ref = df.decompose_batch(s64, delta=p["delta"], max_inner=p["max_inner"], max_imfs=p["max_imfs"],
-                             window=p["window"], gamma=p["gamma"], stop=p["stop"], mask=p["mask"])
+                             window=p["window"], gamma=p["gamma"], stop=p["stop"], mask=p["mask"],
+                             tau=TAU[p["dtype"]])
     for b in range(B):
         assert_parity(s64[b], gpu, ref, b, b, p["dtype"])
 
@@ -109,5 +110,5 @@ def test_fuzz_distributed_vs_direct_form(seed):
     plan_kw = dict(kw)
     gpu = run_dist(s, P, dtype=dtype, stop=stop, gamma=gamma, **plan_kw)
     s64 = s.astype(np.float64)[None]
-    ref = df.decompose_batch(s64, gamma=gamma, stop=stop, **kw)
+    ref = df.decompose_batch(s64, gamma=gamma, stop=stop, tau=TAU[dtype], **kw)
     assert_parity(s64[0], gpu, ref, 0, 0, dtype)

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 import oracle  # noqa: E402
 from oracle import direct_form as df  # noqa: E402
 from paper_1802_01359_b200 import fif, signals  # noqa: E402
-from test_gpu_parity import assert_parity  # noqa: E402
+from test_gpu_parity import TAU, assert_parity  # noqa: E402
 from test_gpu_dist import run_dist  # noqa: E402
 
 
@@ -69,7 +69,7 @@ def test_gamma_and_n0_combined_fp32():
     s32 = np.stack([signals.cfg4_signal(n, i) for i in range(3)])
     gpu = run_opt(s32, stop=fif.STOP_N0, gamma=0.2, dtype="f32", delta=20.0)
     s64 = s32.astype(np.float64)
-    ref = df.decompose_batch(s64, delta=20.0, gamma=0.2, stop=df.STOP_N0)
+    ref = df.decompose_batch(s64, delta=20.0, gamma=0.2, stop=df.STOP_N0, tau=TAU["f32"])
     for b in range(3):
         assert_parity(s64[b], gpu, ref, b, b, "f32")
 
@@ -126,7 +126,7 @@ def test_spectral_peak_rule_fp32_and_dist_unsupported():
     gpu = [t.cpu().numpy() for t in out]
     plan.close()
     s64 = s32.astype(np.float64)
-    ref = df.decompose_batch(s64, mask=df.MASK_SPECTRAL)
+    ref = df.decompose_batch(s64, mask=df.MASK_SPECTRAL, tau=TAU["f32"])
     for b in range(2):
         assert_parity(s64[b], gpu, ref, b, b, "f32")
     dp = fif.Plan.dist(4096, 0, 2, emulated=True)

@@ -8,6 +8,7 @@ Bar (BASELINE.json north_star):
 Seeds whose oracle decision margins fall below 1e-9 (fp64) are screened (sub-seed t+1), as DESIGN.md says.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -15,11 +16,49 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+import conftest  # noqa: E402
 import oracle  # noqa: E402
 from oracle import direct_form as df  # noqa: E402
 from paper_1802_01359_b200 import fif, signals  # noqa: E402
 
 TOL = {"f64": (1e-9, 1e-5), "f32": (2e-4, 1e-3)}
+TAU = {"f64": 1e-9, "f32": 1e-5}  # the oracle's fragility threshold per dtype (reading A21; MARGIN_THR below)
+
+
+def _df_one(args):
+    row, kw = args
+    return df.decompose(row, **kw)
+
+
+def df_batch(signals_, **kw):
+    """oracle/direct_form.py over a batch, one host process per signal (the oracle code as it stands; only the
+    loop over independent signals is spread over the box's cores), in decompose_batch's layout."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    S = np.atleast_2d(np.asarray(signals_, dtype=np.float64))
+    B, n = S.shape
+    max_imfs = kw.get("max_imfs", 10)
+    with cf.ProcessPoolExecutor(max_workers=max(1, min(B, os.cpu_count() or 1, 32)),
+                                mp_context=mp.get_context("fork")) as ex:
+        res = list(ex.map(_df_one, [(S[b], kw) for b in range(B)]))
+    out = {"imfs": np.zeros((B, max_imfs + 1, n)), "count": np.zeros(B, np.int32),
+           "l": np.zeros((B, max_imfs), np.int32), "N": np.zeros((B, max_imfs), np.int32),
+           "margins": np.full((B, max_imfs + 1, 2), np.nan)}
+    for b, d in enumerate(res):
+        M = d["M"]
+        out["imfs"][b] = d["imfs"]
+        out["count"][b] = M
+        out["l"][b, :M] = d["l"]
+        out["N"][b, :M] = d["N"]
+        out["margins"][b] = d["margins"]
+    return out
+
+
+def sample_idx(B):
+    """Every (B/64)-th signal of a full batch, the last one included."""
+    step = max(1, B // 64)
+    return np.unique(np.concatenate([np.arange(0, B, step), [B - 1]]))
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -82,9 +121,12 @@ def safe_prefix(ref, b, dtype):
 
 
 def assert_parity(s, gpu, ref, b_gpu, b_ref, dtype="f64"):
+    """Integers bit-exact over every decision the oracle marks safe (all of them when `full`), IMFs within the
+    tolerance; (P, full, M) is logged for the test's parity floor (tests/conftest.py)."""
     imfs, count, lens, iters = gpu
     M = int(ref["count"][b_ref])
     P, full = safe_prefix(ref, b_ref, dtype)
+    conftest.PARITY_LOG.append((P, full, M))
     if full:
         assert int(count[b_gpu]) == M, (b_gpu, count[b_gpu], M)
         np.testing.assert_array_equal(lens[b_gpu], ref["l"][b_ref])
@@ -179,6 +221,7 @@ def test_inner_hook(n, L):
 
 
 # ------------------------------------------------------------------------------------------ full decomposition
+@pytest.mark.parity(min_full=0.5, min_prefix=8)  # the noise-free signal: IMFs 9, 10 at rounding level (above)
 def test_cfg0_full():
     for s in (signals.make_batch("cfg0"), signals.cfg0_signal(0, noise=0.0)[None, :]):
         gpu = run_gpu(s)
@@ -186,30 +229,45 @@ def test_cfg0_full():
         assert_parity(s[0], gpu, ref, 0, 0)
 
 
+@pytest.mark.parity(min_full=0.0, min_prefix=8)
 def test_cfg0_noise_free_integers():
-    """Noise-free config 0 through the whole pipeline: the (l, N) sequence must equal the oracle's."""
+    """Noise-free config 0 through the whole pipeline against the golden fixture (tests/golden/cfg0_noise_free.json:
+    the oracle's Alg. 2 run, which equals the survey's independent computation).
+    M, every l_m and every N_m are compared; the ONLY entries allowed to differ are those whose SD decision the
+    oracle marks as taken at rounding level (reading A21 margin < 1e-9): IMFs 9 and 10, where the remainder is
+    <= 2.5e-10 ||s|| (IMF 10 is rounding noise) -- asserted to be exactly that set, with their margins."""
+    import json
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg0_noise_free.json")))
     s = signals.cfg0_signal(0, noise=0.0)[None, :]
     gpu = run_gpu(s)
+    assert int(gpu[1][0]) == g["M"]
+    assert gpu[2][0].tolist() == g["l"]
+    unsafe = [m for m, v in enumerate(g["margins_sd"]) if v is not None and v < 1e-9]
+    assert unsafe == [8, 9], unsafe
+    assert g["margins_sd"][8] < 1e-10 and g["margins_sd"][9] < 1e-13
+    Ng = gpu[3][0].tolist()
+    assert [Ng[m] for m in range(g["M"]) if m not in unsafe] == [g["N"][m] for m in range(g["M"]) if m not in unsafe]
+    print("noise-free cfg0: GPU N", Ng, "golden N", g["N"], "(entries 8, 9 at rounding level)")
+    # the safe prefix in full (IMFs within 1e-9), via the usual protocol
     ref = oracle.decompose(s)
-    assert list(gpu[1]) == list(ref["count"])
-    assert gpu[2][0].tolist() == ref["l"][0].tolist()
+    _, P, full = assert_parity(s[0], gpu, ref, 0, 0)
+    assert P == 8 and not full
 
 
+@pytest.mark.parity(min_full=1.0)
 def test_cfg1_sampled_full_batch():
-    """Config 1 at its full size (4096 x 4096 fp64, the bench launch: per-L eigenvalue table on), 24 sampled
-    signals vs the TD oracle."""
+    """Config 1 at its full size (4096 x 4096 fp64, the bench launch: per-L eigenvalue table on): every
+    (B/64)-th signal (65) vs the TD oracle, all compared in full; properties on every signal."""
     B = 4096
     s = signals.make_batch("cfg1", batch=B)
     gpu = run_gpu(s, eig=True)
-    idx = np.linspace(0, B - 1, 24).astype(int)
+    idx = sample_idx(B)
     ref = oracle.decompose(s[idx])
     worst = 0.0
-    nfull = 0
     for i, b in enumerate(idx):
         errs, P, full = assert_parity(s[b], gpu, ref, b, i)
         worst = max(worst, errs.max())
-        nfull += full
-    assert nfull >= len(idx) - 1  # generated noisy signals: decisions far from ties
     # properties at every signal of the batch: counts in range, telescoping
     imfs, count, lens, iters = gpu
     assert ((count >= 1) & (count <= 10)).all()
@@ -246,7 +304,11 @@ def test_wide_window_R3():
         assert_parity(s[b], gpu, ref, b, b)
 
 
-@pytest.mark.parametrize("delta,max_inner,max_imfs", [(1e-4, 200, 10), (1e-2, 50, 3), (0.3, 7, 12), (1e-3, 1, 4)])
+@pytest.mark.parametrize("delta,max_inner,max_imfs", [
+    (1e-4, 200, 10), (1e-2, 50, 3),
+    # delta = 0.3 with a cap of 7: SD sits near delta on late IMFs (oracle margins < 1e-9 on 5 of 6 signals)
+    pytest.param(0.3, 7, 12, marks=pytest.mark.parity(min_full=1 / 6, min_prefix=5)),
+    (1e-3, 1, 4)])
 def test_parameters(delta, max_inner, max_imfs):
     s = signals.make_batch("cfg1", batch=6, start=77)
     gpu = run_gpu(s, delta=delta, max_inner=max_inner, max_imfs=max_imfs)
@@ -256,6 +318,7 @@ def test_parameters(delta, max_inner, max_imfs):
 
 
 # ------------------------------------------------------------------------------------------ edge cases
+@pytest.mark.parity(min_full=6 / 7, min_prefix=4)  # the 1e-300 tone: later decisions on subnormal-scale remainders
 def test_degenerate_inputs():
     n = 1024
     rows = [np.zeros(n), np.full(n, 2.5), np.linspace(-1, 1, n), np.linspace(0, 1, n) ** 3,
@@ -304,13 +367,17 @@ def test_ragged_batch_beyond_grid():
 
 
 # ------------------------------------------------------------------------------------------ fp32
+# fp32 remainders differ from the fp64 oracle's by ~1e-7 ||s||: many decisions of noisy signals are within that
+# (oracle margins below the fp32 thresholds), so a part of each sample is compared on a prefix only
+@pytest.mark.parity(min_full=0.15)
 @pytest.mark.parametrize("n", [1024, 4096])
 def test_fp32_path(n):
-    s32 = np.stack([signals.cfg4_signal(n, i) for i in range(8)])
+    B = 32
+    s32 = np.stack([signals.cfg4_signal(n, i) for i in range(B)])
     gpu = run_gpu(s32, "f32")
     s64 = s32.astype(np.float64)
-    ref = oracle.decompose(s64)
-    for b in range(8):
+    ref = oracle.decompose(s64, tau=TAU["f32"])
+    for b in range(B):
         assert_parity(s64[b], gpu, ref, b, b, "f32")
 
 
@@ -352,6 +419,6 @@ def test_resident_fp32_16384_hooks_and_decomposition():
     s32 = np.stack([signals.cfg4_signal(n, i) for i in range(4)])
     gpu = run_gpu(s32, "f32")
     s64 = s32.astype(np.float64)
-    refd = df.decompose_batch(s64)
+    refd = df.decompose_batch(s64, tau=TAU["f32"])
     for b in range(4):
         assert_parity(s64[b], gpu, refd, b, b, "f32")

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 import oracle  # noqa: E402
 from oracle import direct_form as df  # noqa: E402
 from paper_1802_01359_b200 import fif, signals  # noqa: E402
-from test_gpu_parity import assert_parity, run_gpu  # noqa: E402
+from test_gpu_parity import TAU, assert_parity, df_batch, run_gpu, sample_idx  # noqa: E402
 
 ST = fif.REGIME_STREAMED
 
@@ -58,12 +58,13 @@ def test_streamed_mixed_radix_vs_td_oracle(n):
 
 
 def test_cfg2_full_batch_sampled():
-    """Config 2 at full size (512 x 65536 fp64, delta = 1e-4): 4 sampled signals vs the direct form."""
+    """Config 2 at full size (512 x 65536 fp64, delta = 1e-4, the bench launch): every (B/64)-th signal (65)
+    vs the direct form (spread over the host's cores), all compared in full; telescoping on every signal."""
     B = 512
     s = signals.make_batch("cfg2", batch=B)
     gpu = run_gpu(s, delta=1e-4)
-    idx = [0, 171, 342, 511]
-    ref = df.decompose_batch(s[idx], delta=1e-4)
+    idx = sample_idx(B)
+    ref = df_batch(s[idx], delta=1e-4)
     for i, b in enumerate(idx):
         assert_parity(s[b], gpu, ref, b, i)
     imfs, count = gpu[0], gpu[1]
@@ -77,7 +78,7 @@ def test_cfg4_fp32_lengths(n):
     s32 = np.stack([signals.cfg4_signal(n, i) for i in range(B)])
     gpu = run_gpu(s32, "f32")
     s64 = s32.astype(np.float64)
-    ref = df.decompose_batch(s64)
+    ref = df.decompose_batch(s64, tau=TAU["f32"])
     for b in range(B):
         assert_parity(s64[b], gpu, ref, b, b, "f32")
 
@@ -87,7 +88,7 @@ def test_cfg4_fp32_2p20():
     s32 = np.stack([signals.cfg4_signal(n, i) for i in range(2)])
     gpu = run_gpu(s32, "f32")
     s64 = s32.astype(np.float64)
-    ref = df.decompose_batch(s64)
+    ref = df.decompose_batch(s64, tau=TAU["f32"])
     for b in range(2):
         assert_parity(s64[b], gpu, ref, b, b, "f32")
 

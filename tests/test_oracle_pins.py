@@ -527,3 +527,132 @@ def test_spectral_rule_td_equals_direct_form():
     for b in range(3):
         f, _ = oracle.spectral_peak(s[b])
         assert a["l"][b][0] == 2 * oracle.filter_half_length(1.6, 1024, 2 * f)
+
+
+# ----------------------------------------------------------------------------- decision margins (reading A21)
+# The margins decide which IMFs the GPU parity tests compare (tests/test_gpu_parity.py::safe_prefix), so
+# they are pinned here against hand-built cases and closed forms, and across the two oracle engines.
+
+def test_extrema_margin_hand_built_plateaus():
+    """min |nonzero diff| / max|r| on a hand-built row with plateaus (SPEC.md:94 zeros dropped):
+    diffs 1, 0, -0.5, 0, 1.5, -6, -0.25 -> signs + - + - -  -> k = 3; margin 0.25 / 4.25."""
+    r = np.array([0.0, 1.0, 1.0, 0.5, 0.5, 2.0, -4.0, -4.25])
+    k, m = oracle.count_extrema(r)
+    assert k == 3
+    assert m == 0.25 / 4.25
+
+
+def _zigzag_then_ramp(n, K, fragile_at=None, eps=1e-13):
+    """K interior extrema (0,1,0,1,... over the first K+2 points), then a strictly increasing ramp; optionally
+    one ramp step of size eps (a 'fragile' difference) or 0 (a plateau)."""
+    x = np.empty(n)
+    x[: K + 2] = [(j % 2) * 1.0 for j in range(K + 2)]
+    base = x[K + 1]
+    steps = np.full(n - K - 2, 1.0)
+    if fragile_at is not None:
+        steps[fragile_at] = eps
+    x[K + 2:] = base + 2.0 + np.cumsum(steps)
+    return x
+
+
+@pytest.mark.parametrize("K,robust", [(300, True), (320, False), (100, False)])
+@pytest.mark.parametrize("eps", [1e-13, 0.0])
+def test_extrema_decision_margin_robustness(K, robust, eps):
+    """Reading A21: f fragile differences leave k uncertain by +-2f; the decision is robust iff
+    floor(fl(xi n)/k') is the same at k' = k - 2f and k + 2f (exact rational floors):
+    n = 1000, xi = 1.6: 1600/298 = 5.37, 1600/302 = 5.30 (robust); 1600/318 = 5.03, 1600/322 = 4.97 (not);
+    1600/98 = 16.3, 1600/102 = 15.7 (not).  Here f = 1 (one ramp step of size eps: tiny or a plateau)."""
+    n = 1000
+    x = _zigzag_then_ramp(n, K, fragile_at=200, eps=eps)
+    k, em = oracle.count_extrema(x)
+    assert k == K
+    lo, hi = Fraction(1600, K - 2), Fraction(1600, K + 2)
+    assert (math.floor(lo) == math.floor(hi)) == robust  # the case is what its name says
+    m = oracle.extrema_decision_margin(x, k, em, np.abs(x).max(), 1e-9)
+    assert (m == math.inf) == robust
+    if not robust:
+        assert m == em
+    # no fragile difference: the plain margin whatever k
+    y = _zigzag_then_ramp(n, K)
+    ky, emy = oracle.count_extrema(y)
+    assert oracle.extrema_decision_margin(y, ky, emy, np.abs(y).max(), 1e-9) == emy
+
+
+def test_extrema_decision_margin_stop_decision():
+    """k < 2 with a fragile difference, or k - 2f < 2: the stop decision is not robust."""
+    x = np.arange(50.0)
+    x[20] = x[19]  # one plateau step: k = 0, f = 1
+    k, em = oracle.count_extrema(x)
+    assert k == 0
+    assert oracle.extrema_decision_margin(x, k, em, 49.0, 1e-9) == em
+    y = _zigzag_then_ramp(60, 2, fragile_at=10)  # k = 2, f = 1 -> k - 2 = 0 < 2
+    ky, emy = oracle.count_extrema(y)
+    assert ky == 2 and oracle.extrema_decision_margin(y, ky, emy, np.abs(y).max(), 1e-9) == emy
+
+
+def _fejer4(n, L, f):
+    """w_hat_f in closed form (independent of the oracle): [sin(pi L f/n) / (L sin(pi f/n))]^4."""
+    return (math.sin(math.pi * L * f / n) / (L * math.sin(math.pi * f / n))) ** 4
+
+
+@pytest.mark.parametrize("f,delta,expect_N", [(64, 1e-3, 200), (300, 0.9, 1)])
+def test_sd_margin_pure_tone_closed_form(f, delta, expect_N):
+    """A pure tone is an eigenvector: SD_N = w_hat_f for every N, the iterate norms are
+    (1 - w_hat)^(N-1) ||s||, so the SD margin (reading A21: |SD - delta|/delta * ||iterate|| / ||s||, the
+    smaller of the decisions at N and N - 1) is |w - delta|/delta (1 - w)^(N-1) with N = cap = 200 when
+    w > delta, and |w - delta|/delta at N = 1 when w <= delta.  The first extrema decision is on s: +inf."""
+    n = 1024
+    s = np.cos(2 * np.pi * f * np.arange(n) / n + 0.3)
+    r = oracle.decompose(s, delta=delta, max_imfs=1)
+    k = int(r["k"][0, 0])
+    L = oracle.filter_half_length(1.6, n, k)
+    w = _fejer4(n, L, f)
+    assert int(r["N"][0, 0]) == expect_N
+    want = abs(w - delta) / delta * ((1 - w) ** (expect_N - 1) if expect_N > 1 else 1.0)
+    assert r["margins"][0, 0, 0] == math.inf
+    assert r["margins"][0, 0, 1] == pytest.approx(want, rel=1e-9)
+
+
+def test_margins_td_equal_direct_form():
+    """The two oracle engines report the same margins (definitions of reading A21 evaluated once by the literal
+    iteration, once through Parseval): cfg0 (noisy and noise-free) and 3 cfg1 signals; margins above the
+    rounding level agree to 1e-6 relative, +inf where one is +inf."""
+    rows = [signals.make_batch("cfg0")[0], signals.cfg0_signal(0, noise=0.0)] + list(signals.make_batch("cfg1", batch=3))
+    for s in rows:
+        td = oracle.decompose(s)
+        dfr = df.decompose(s)
+        M = int(td["count"][0])
+        assert M == dfr["M"]
+        a, b = td["margins"][0][: M + 1], dfr["margins"][: M + 1]
+        for m in range(M + 1):
+            for c in range(2):
+                x, y = a[m, c], b[m, c]
+                if np.isnan(x) or np.isnan(y):
+                    assert np.isnan(x) and np.isnan(y)
+                elif math.isinf(x) or math.isinf(y):
+                    assert x == y
+                elif max(x, y) > 1e-9:
+                    assert x == pytest.approx(y, rel=1e-6), (m, c, x, y)
+
+
+# ----------------------------------------------------------------------------- noise-free cfg0 fixture
+SURVEY_E9 = {  # SURVEY.md §8c "Noise-free cfg0 fixture (R1 readings, TD literal; E9)": an independent
+    "k": [128, 128, 128, 112, 32, 32, 20, 4, 4, 4],  # throwaway numpy model written during the survey
+    "l": [24, 24, 24, 28, 102, 102, 162, 510, 510, 510],
+    "N": [200, 200, 200, 8, 200, 200, 200, 50, 150, 200],
+    "M": 10,
+}
+
+
+def test_noise_free_cfg0_golden_matches_survey_and_oracle():
+    """tests/golden/cfg0_noise_free.json (written by make_cfg0_golden.py from oracle/ only) equals the survey's
+    independent computation, and the oracle as it stands still reproduces it (Alg. 2,
+    PAPER.md:401-417)."""
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg0_noise_free.json")))
+    assert g["M"] == SURVEY_E9["M"]
+    assert g["k"][: g["M"]] == SURVEY_E9["k"]
+    assert g["l"] == SURVEY_E9["l"] and g["N"] == SURVEY_E9["N"]
+    s = signals.cfg0_signal(0, noise=0.0)
+    r = oracle.decompose(s)
+    assert int(r["count"][0]) == g["M"]
+    assert r["l"][0].tolist() == g["l"] and r["N"][0].tolist() == g["N"]
