@@ -160,7 +160,7 @@ def extrema_decision_margin(r, k, em, scale, tau, xi=1.6, window=WINDOW_TRI_SQ, 
 
 
 def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, stop=STOP_SD,
-              mask=MASK_EXTREMA, tau=1e-9):
+              mask=MASK_EXTREMA, tau=1e-11):
     """Time-domain oracle decomposition of a batch [B, n] (or one signal [n]).
     stop = STOP_SD: the relative SD rule (reading A5); STOP_N0: the a-priori N0 of Thm DIF_conv_stop with
     the absolute delta (readings A16-A18).
@@ -169,8 +169,8 @@ def decompose(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WI
     k [B, max_imfs+1] (extrema count at each outer step), margins [B, max_imfs+1, 2]
     (reading A21, DESIGN.md -- per outer step m: the margin of the a2/a3 decision at its head (+inf for
     the first, taken on s itself, and for decisions robust to the differences below tau * max|s|, else
-    min |diff| / max|s|), and the SD margin |SD - delta|/delta * ||iterate|| / ||s|| of IMF m; NaN where
-    no decision was taken)."""
+    min |diff| / max|s|), and the SD margin |SD - delta| * ||iterate|| / (2 ||s||) of IMF m (the remainder
+    perturbation, in units of ||s||, that can flip it); NaN where no decision was taken)."""
     s = np.ascontiguousarray(np.atleast_2d(np.asarray(signals, dtype=np.float64)))
     B, n = s.shape
     imfs = np.zeros((B, max_imfs + 1, n))

@@ -132,7 +132,7 @@ def sd_curve(rhat: np.ndarray, lam: np.ndarray, n: int, max_inner: int) -> np.nd
 
 
 def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0, stop=STOP_SD,
-              mask=MASK_EXTREMA, tau=1e-9):
+              mask=MASK_EXTREMA, tau=1e-11):
     """Full FIF decomposition of one real signal.  Returns dict with imfs [(max_imfs+1), n]
     (trend in slot M), M, l (2L per IMF), N, k (extrema counts), sd (SD_N, SD_{N-1}).
     stop = STOP_N0: N = min(N0, max_inner) from the a-priori bound with the absolute delta (PAPER.md:599,
@@ -200,9 +200,10 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
             if N > 1:
                 sm = min(sm, abs(n0_f(N - 1) / rhs - 1.0))
         else:
-            sm = abs(curve[N - 1] - delta) / delta * (itn(N - 1) / snorm if snorm > 0 else 1.0)
+            # reading A21: the remainder perturbation (units of ||s||) that can flip SD <= delta, first order
+            sm = 0.5 * abs(curve[N - 1] - delta) * (itn(N - 1) / snorm if snorm > 0 else 1.0)
             if N > 1:
-                sm = min(sm, abs(curve[N - 2] - delta) / delta * (itn(N - 2) / snorm if snorm > 0 else 1.0))
+                sm = min(sm, 0.5 * abs(curve[N - 2] - delta) * (itn(N - 2) / snorm if snorm > 0 else 1.0))
         margins[M, 1] = sm
         M += 1
     if M == max_imfs:
@@ -212,7 +213,7 @@ def decompose(s, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_T
 
 
 def decompose_batch(signals, xi=1.6, delta=1e-3, max_inner=200, max_imfs=10, window=WINDOW_TRI_SQ, gamma=0.0,
-                    stop=STOP_SD, mask=MASK_EXTREMA, tau=1e-9):
+                    stop=STOP_SD, mask=MASK_EXTREMA, tau=1e-11):
     """CPU-DF over a batch, returned in the TD oracle's dict layout (imfs, count, l, N, margins)."""
     S = np.atleast_2d(np.asarray(signals, dtype=np.float64))
     B, n = S.shape

@@ -370,11 +370,13 @@ int32_t oracle_decompose_one(const double* s, int64_t n, int window, double xi, 
       if (!isnan(sd[1]) && fabs(sd[1]) < sm) sm = fabs(sd[1]);
       margins[2 * M + 1] = sm;
     } else if (margins) {
-      /* |SD - delta| / delta, scaled by ||iterate|| / ||s||: absolute rounding differences are
-         ~1e-16 ||s||, so a decision on a remainder at rounding level has no margin. */
-      double sm = fabs(sd[0] - delta) / delta * (snorm > 0.0 ? sd[2] / snorm : 1.0);
+      /* reading A21: the remainder perturbation, in units of ||s||, that can flip the decision SD <= delta
+         (to first order |dSD| <= 2 ||dr|| / ||iterate||): |SD - delta| ||iterate|| / (2 ||s||), the smaller
+         of the tests at N and N - 1.  Two implementations' remainders differ by ~1e-16 ||s||, so a decision
+         on a remainder at rounding level has no margin. */
+      double sm = 0.5 * fabs(sd[0] - delta) * (snorm > 0.0 ? sd[2] / snorm : 1.0);
       if (!isnan(sd[1])) {
-        double s1 = fabs(sd[1] - delta) / delta * (snorm > 0.0 ? sd[3] / snorm : 1.0);
+        double s1 = 0.5 * fabs(sd[1] - delta) * (snorm > 0.0 ? sd[3] / snorm : 1.0);
         if (s1 < sm) sm = s1;
       }
       margins[2 * M + 1] = sm;

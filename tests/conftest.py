@@ -35,6 +35,8 @@ def _parity_floor(request):
     nfull = sum(1 for _, full, _ in PARITY_LOG if full)
     assert nfull >= math.ceil(min_full * n - 1e-9), \
         f"parity floor: {nfull}/{n} signals compared in full, the test requires >= {min_full:.2f}"
-    worst = min(p if not full else m for p, full, m in PARITY_LOG)
-    assert worst >= min_prefix, f"parity floor: a signal compared on {worst} leading IMFs only (< {min_prefix})"
-    print(f"[parity] {nfull}/{n} signals in full, min prefix {worst}")
+    partial = [p for p, full, _ in PARITY_LOG if not full]
+    worst = min(partial) if partial else None
+    assert worst is None or worst >= min_prefix, \
+        f"parity floor: a signal compared on {worst} leading IMFs only (< {min_prefix})"
+    print(f"[parity] {nfull}/{n} signals in full, shortest partial prefix {worst}")

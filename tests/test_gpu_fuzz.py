@@ -53,9 +53,17 @@ def _case(seed):
     return p
 
 
+# random shapes and parameters (fp32, max_inner = 1, small delta ...) produce decisions at the oracle's margin
+# thresholds by construction: fp64 cases compare every signal on at least its first IMF (in full when safe);
+# fp32 cases whatever the margins allow (a first SD decision within the fp32 threshold is common)
+def _fuzz_floor(request, dtype):
+    request.node.add_marker(pytest.mark.parity(min_full=0.0, min_prefix=1 if dtype == "f64" else 0))
+
+
 @pytest.mark.parametrize("seed", range(int(os.environ.get("FIF_FUZZ_CASES", "40"))))
-def test_fuzz_vs_direct_form(seed, monkeypatch):
+def test_fuzz_vs_direct_form(seed, monkeypatch, request):
     p = _case(seed)
+    _fuzz_floor(request, p["dtype"])
     n, B = p["n"], p["B"]
     s = np.stack([signals.tones_signal(n, 77, p["sig_seed"] + i) for i in range(B)])
     if p["dtype"] == "f32":
@@ -85,7 +93,7 @@ def test_fuzz_vs_direct_form(seed, monkeypatch):
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("FIF_FUZZ_DIST_CASES", "12"))))
-def test_fuzz_distributed_vs_direct_form(seed):
+def test_fuzz_distributed_vs_direct_form(seed, request):
     """One signal over P emulated ranks (the distributed regime): random P, length, dtype, window,
     parameters and stopping options."""
     from test_gpu_dist import run_dist
@@ -107,6 +115,7 @@ def test_fuzz_distributed_vs_direct_form(seed):
     s = signals.tones_signal(n, 78, int(rng.integers(0, 1 << 30)))
     if dtype == "f32":
         s = s.astype(np.float32)
+    _fuzz_floor(request, dtype)
     plan_kw = dict(kw)
     gpu = run_dist(s, P, dtype=dtype, stop=stop, gamma=gamma, **plan_kw)
     s64 = s.astype(np.float64)[None]

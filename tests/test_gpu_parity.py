@@ -22,37 +22,10 @@ from oracle import direct_form as df  # noqa: E402
 from paper_1802_01359_b200 import fif, signals  # noqa: E402
 
 TOL = {"f64": (1e-9, 1e-5), "f32": (2e-4, 1e-3)}
-TAU = {"f64": 1e-9, "f32": 1e-5}  # the oracle's fragility threshold per dtype (reading A21; MARGIN_THR below)
+TAU = {"f64": 1e-11, "f32": 1e-5}  # the oracle's fragility threshold per dtype (reading A21; MARGIN_THR below)
 
 
-def _df_one(args):
-    row, kw = args
-    return df.decompose(row, **kw)
-
-
-def df_batch(signals_, **kw):
-    """oracle/direct_form.py over a batch, one host process per signal (the oracle code as it stands; only the
-    loop over independent signals is spread over the box's cores), in decompose_batch's layout."""
-    import concurrent.futures as cf
-    import multiprocessing as mp
-
-    S = np.atleast_2d(np.asarray(signals_, dtype=np.float64))
-    B, n = S.shape
-    max_imfs = kw.get("max_imfs", 10)
-    with cf.ProcessPoolExecutor(max_workers=max(1, min(B, os.cpu_count() or 1, 32)),
-                                mp_context=mp.get_context("fork")) as ex:
-        res = list(ex.map(_df_one, [(S[b], kw) for b in range(B)]))
-    out = {"imfs": np.zeros((B, max_imfs + 1, n)), "count": np.zeros(B, np.int32),
-           "l": np.zeros((B, max_imfs), np.int32), "N": np.zeros((B, max_imfs), np.int32),
-           "margins": np.full((B, max_imfs + 1, 2), np.nan)}
-    for b, d in enumerate(res):
-        M = d["M"]
-        out["imfs"][b] = d["imfs"]
-        out["count"][b] = M
-        out["l"][b, :M] = d["l"]
-        out["N"][b, :M] = d["N"]
-        out["margins"][b] = d["margins"]
-    return out
+from df_pool import df_batch  # noqa: E402,F401  (re-exported for the other test files)
 
 
 def sample_idx(B):
@@ -102,7 +75,11 @@ def imf_errors(gpu_imfs, ref_imfs, s, M, dtype):
     return np.array(errs), tol
 
 
-MARGIN_THR = {"f64": (1e-9, 1e-9), "f32": (1e-5, 1e-4)}  # (extremum, SD) decision margins
+# (extremum, SD) decision-margin thresholds (reading A21), from the remainder differences measured between the
+# GPU and the oracle (asserted below in test_cfg1_sampled_full_batch and test_fp32_path):
+#   fp64: samples within 6.4e-15 max|s|, norms within ~1e-15 ||s||  -> extremum 1e-11 max|s|, SD 1e-13 ||s||;
+#   fp32: samples within 3.5e-7 max|s|, norms within 2e-7 ||s||     -> extremum 1e-5 max|s|,  SD 1e-6 ||s||.
+MARGIN_THR = {"f64": (1e-11, 1e-13), "f32": (1e-5, 1e-6)}
 
 
 def safe_prefix(ref, b, dtype):
@@ -243,9 +220,9 @@ def test_cfg0_noise_free_integers():
     gpu = run_gpu(s)
     assert int(gpu[1][0]) == g["M"]
     assert gpu[2][0].tolist() == g["l"]
-    unsafe = [m for m, v in enumerate(g["margins_sd"]) if v is not None and v < 1e-9]
+    unsafe = [m for m, v in enumerate(g["margins_sd"]) if v is not None and v < MARGIN_THR["f64"][1]]
     assert unsafe == [8, 9], unsafe
-    assert g["margins_sd"][8] < 1e-10 and g["margins_sd"][9] < 1e-13
+    assert g["margins_sd"][8] < 1e-13 and g["margins_sd"][9] < 1e-16
     Ng = gpu[3][0].tolist()
     assert [Ng[m] for m in range(g["M"]) if m not in unsafe] == [g["N"][m] for m in range(g["M"]) if m not in unsafe]
     print("noise-free cfg0: GPU N", Ng, "golden N", g["N"], "(entries 8, 9 at rounding level)")
@@ -265,9 +242,19 @@ def test_cfg1_sampled_full_batch():
     idx = sample_idx(B)
     ref = oracle.decompose(s[idx])
     worst = 0.0
+    dev = dn = 0.0
     for i, b in enumerate(idx):
         errs, P, full = assert_parity(s[b], gpu, ref, b, i)
         worst = max(worst, errs.max())
+        # sample-wise difference of the remainders the two sides take their decisions on (reading A21's bound)
+        rg, ro = s[b].copy(), s[b].copy()
+        for m in range(int(ref["count"][i])):
+            rg -= gpu[0][b, m]
+            ro -= ref["imfs"][i, m]
+            dev = max(dev, np.abs(rg - ro).max() / np.abs(s[b]).max())
+            dn = max(dn, np.linalg.norm(rg - ro) / np.linalg.norm(s[b]))
+    assert dev <= MARGIN_THR["f64"][0] / 100 and dn <= MARGIN_THR["f64"][1] / 10, (dev, dn)
+    print(f"cfg1 max remainder deviation {dev:.2e} max|s|, {dn:.2e} ||s||")
     # properties at every signal of the batch: counts in range, telescoping
     imfs, count, lens, iters = gpu
     assert ((count >= 1) & (count <= 10)).all()
@@ -294,6 +281,7 @@ def test_other_lengths(n):
         assert_parity(s[b], gpu, ref, b, b)
 
 
+@pytest.mark.parity(min_full=0.5, min_prefix=4)  # the two-tone row: IMF 5 decided within 1e-11 max|s|
 def test_wide_window_R3():
     n = 512
     t = np.arange(n) / n
@@ -306,8 +294,8 @@ def test_wide_window_R3():
 
 @pytest.mark.parametrize("delta,max_inner,max_imfs", [
     (1e-4, 200, 10), (1e-2, 50, 3),
-    # delta = 0.3 with a cap of 7: SD sits near delta on late IMFs (oracle margins < 1e-9 on 5 of 6 signals)
-    pytest.param(0.3, 7, 12, marks=pytest.mark.parity(min_full=1 / 6, min_prefix=5)),
+    # delta = 0.3 with a cap of 7: SD sits near delta on late IMFs (two signals carry an unsafe late decision)
+    pytest.param(0.3, 7, 12, marks=pytest.mark.parity(min_full=4 / 6, min_prefix=10)),
     (1e-3, 1, 4)])
 def test_parameters(delta, max_inner, max_imfs):
     s = signals.make_batch("cfg1", batch=6, start=77)
@@ -318,7 +306,7 @@ def test_parameters(delta, max_inner, max_imfs):
 
 
 # ------------------------------------------------------------------------------------------ edge cases
-@pytest.mark.parity(min_full=6 / 7, min_prefix=4)  # the 1e-300 tone: later decisions on subnormal-scale remainders
+@pytest.mark.parity(min_full=6 / 7, min_prefix=5)  # the 1e-300 tone: later decisions on subnormal-scale remainders
 def test_degenerate_inputs():
     n = 1024
     rows = [np.zeros(n), np.full(n, 2.5), np.linspace(-1, 1, n), np.linspace(0, 1, n) ** 3,
@@ -377,8 +365,18 @@ def test_fp32_path(n):
     gpu = run_gpu(s32, "f32")
     s64 = s32.astype(np.float64)
     ref = oracle.decompose(s64, tau=TAU["f32"])
+    dev = dn = 0.0
     for b in range(B):
-        assert_parity(s64[b], gpu, ref, b, b, "f32")
+        _, P, _ = assert_parity(s64[b], gpu, ref, b, b, "f32")
+        # remainder differences behind the fp32 thresholds (reading A21): sample-wise vs max|s| and in norm
+        rg, ro = s64[b].copy(), s64[b].copy()
+        for m in range(P):
+            rg -= gpu[0][b, m].astype(np.float64)
+            ro -= ref["imfs"][b, m]
+            dev = max(dev, np.abs(rg - ro).max() / np.abs(s64[b]).max())
+            dn = max(dn, np.linalg.norm(rg - ro) / np.linalg.norm(s64[b]))
+    assert dev <= MARGIN_THR["f32"][0] / 10 and dn <= MARGIN_THR["f32"][1], (dev, dn)
+    print(f"fp32 n={n}: max remainder deviation {dev:.2e} max|s|, {dn:.2e} ||s||")
 
 
 # ------------------------------------------------------------------------------------------ e2e host path
@@ -395,6 +393,7 @@ def test_host_path_matches_device_path():
 
 
 # ------------------------------------------------------------------------------------------ n = 16384 fp32 resident
+@pytest.mark.parity(min_full=0.15)  # fp32: see tests/test_gpu_parity.py::test_fp32_path
 def test_resident_fp32_16384_hooks_and_decomposition():
     """The largest resident kernel (fp32, n/2 = 8192: 1024 threads, 192 KB shared memory; config 4's
     n = 2^14 point): FFT hooks vs numpy and the extrema hook vs the oracle, then whole decompositions vs

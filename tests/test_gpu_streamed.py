@@ -72,6 +72,7 @@ def test_cfg2_full_batch_sampled():
     assert np.abs(imfs.sum(axis=1) - s).max() <= 1e-11 * np.abs(s).max()
 
 
+@pytest.mark.parity(min_full=0.15)  # fp32: see tests/test_gpu_parity.py::test_fp32_path
 @pytest.mark.parametrize("n", [1 << 14, 1 << 17, 3 << 14, 5 << 14])
 def test_cfg4_fp32_lengths(n):
     B = 6
@@ -83,6 +84,7 @@ def test_cfg4_fp32_lengths(n):
         assert_parity(s64[b], gpu, ref, b, b, "f32")
 
 
+@pytest.mark.parity(min_full=0.15)  # fp32: see tests/test_gpu_parity.py::test_fp32_path
 def test_cfg4_fp32_2p20():
     n = 1 << 20
     s32 = np.stack([signals.cfg4_signal(n, i) for i in range(2)])

@@ -598,9 +598,9 @@ def _fejer4(n, L, f):
 @pytest.mark.parametrize("f,delta,expect_N", [(64, 1e-3, 200), (300, 0.9, 1)])
 def test_sd_margin_pure_tone_closed_form(f, delta, expect_N):
     """A pure tone is an eigenvector: SD_N = w_hat_f for every N, the iterate norms are
-    (1 - w_hat)^(N-1) ||s||, so the SD margin (reading A21: |SD - delta|/delta * ||iterate|| / ||s||, the
-    smaller of the decisions at N and N - 1) is |w - delta|/delta (1 - w)^(N-1) with N = cap = 200 when
-    w > delta, and |w - delta|/delta at N = 1 when w <= delta.  The first extrema decision is on s: +inf."""
+    (1 - w_hat)^(N-1) ||s||, so the SD margin (reading A21: |SD - delta| ||iterate|| / (2 ||s||), the
+    smaller of the decisions at N and N - 1) is |w - delta| (1 - w)^(N-1) / 2 with N = cap = 200 when
+    w > delta, and |w - delta| / 2 at N = 1 when w <= delta.  The first extrema decision is on s: +inf."""
     n = 1024
     s = np.cos(2 * np.pi * f * np.arange(n) / n + 0.3)
     r = oracle.decompose(s, delta=delta, max_imfs=1)
@@ -608,7 +608,7 @@ def test_sd_margin_pure_tone_closed_form(f, delta, expect_N):
     L = oracle.filter_half_length(1.6, n, k)
     w = _fejer4(n, L, f)
     assert int(r["N"][0, 0]) == expect_N
-    want = abs(w - delta) / delta * ((1 - w) ** (expect_N - 1) if expect_N > 1 else 1.0)
+    want = 0.5 * abs(w - delta) * ((1 - w) ** (expect_N - 1) if expect_N > 1 else 1.0)
     assert r["margins"][0, 0, 0] == math.inf
     assert r["margins"][0, 0, 1] == pytest.approx(want, rel=1e-9)
 
