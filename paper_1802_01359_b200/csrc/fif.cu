@@ -78,7 +78,6 @@ void free_plan(fif_plan_s* p) {
   cudaFree(p->d_isin);
   cudaFree(p->d_tw);
   cudaFree(p->d_wtab);
-  cudaFree(p->d_ltab);
   st_free(p);
   dist_free(p);
   for (int i = 0; i < p->nstages; ++i) {
@@ -170,16 +169,6 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
   p->smem = ops->smem;
   if (ce != cudaSuccess || p->occ < 1) {
     fprintf(stderr, "fif: kernel setup failed: %s (occ %d)\n", cudaGetErrorString(ce), p->occ);
-    free_plan(p);
-    return FIF_ERR_CUDA;
-  }
-  // the a3 rule tabulated for every extrema count (xi, n and the window are fixed per plan)
-  if (cudaMalloc(&p->d_ltab, sizeof(int32_t) * (size_t)(n + 1)) != cudaSuccess) {
-    free_plan(p);
-    return FIF_ERR_OOM;
-  }
-  ops->fill_ltab(p, (int32_t*)p->d_ltab, 0);
-  if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
     free_plan(p);
     return FIF_ERR_CUDA;
   }

@@ -41,7 +41,6 @@ struct fif_plan_s {
   void* d_sin = nullptr;   // Real[NC+1]  sin(pi j/n)
   void* d_isin = nullptr;  // Real[NC+1]  1/sin(pi j/n) (j >= 1)
   void* d_tw = nullptr;    // V[twtotal]  Stockham twiddles e^{-2 pi i k r/(NS RP)}
-  void* d_ltab = nullptr;  // int32[n+1]: filter half-length L for every extrema count (resident regime)
   void* d_wtab = nullptr;  // Real[(n-1)/4 - 1][NC+1] per-L eigenvalue table (fif_plan_set_eigen_table)
   int block = 0, occ = 0;
   size_t smem = 0;
@@ -73,7 +72,7 @@ struct fif_plan_s {
   fifhost::DistPlan* dist = nullptr;  // distributed regime (fif_dist.cu)
   cudaStream_t st_streams[2] = {nullptr, nullptr};  // waves alternate between these
   cudaEvent_t st_ev[3] = {nullptr, nullptr, nullptr};
-  size_t st_smem_col[fifgpu::st::kMaxLev] = {}, st_smem_rows = 0;
+  size_t st_smem_col[fifgpu::st::kMaxLev] = {}, st_smem_rows = 0, st_smem_rows_inv = 0;
   int st_col_cs[fifgpu::st::kMaxLev] = {};  // column transform path per level (st::col_fft CS)
   int st_row_rs = 0;                         // row transform path (st::row_fft RS)
   // host (e2e) path staging
@@ -97,7 +96,6 @@ struct ResOps {
   void (*test_window)(const fif_plan_s*, int, void*, cudaStream_t);
   void (*test_inner)(const fif_plan_s*, int, const void*, void*, int32_t*, int64_t, cudaStream_t);
   void (*fill_wtab)(const fif_plan_s*, void*, int, cudaStream_t);
-  void (*fill_ltab)(const fif_plan_s*, int32_t*, cudaStream_t);
 };
 const ResOps* res_ops_f64(int NC);
 const ResOps* res_ops_f32(int NC);

@@ -66,7 +66,6 @@ struct Inst {
                         int64_t batch, cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
     prm.wtab = p->d_wtab;
-    prm.ltab = (const int32_t*)p->d_ltab;
     const bool fast = p->max_inner == kFastCap, tab = p->d_wtab != nullptr;
     auto kern = fast ? (tab ? fif_resident_kernel<Real, NC, kFastCap, true> : fif_resident_kernel<Real, NC, kFastCap, false>)
                      : (tab ? fif_resident_kernel<Real, NC, 0, true> : fif_resident_kernel<Real, NC, 0, false>);
@@ -103,10 +102,6 @@ struct Inst {
       fif_wtab_kernel<Real, NC, 0><<<nL, K::T, K::smem_bytes, s>>>(tab, (const Real*)p->d_sin, (const Real*)p->d_isin,
                                                                   p->max_inner);
   }
-  static void fill_ltab(const fif_plan_s* p, int32_t* tab, cudaStream_t s) {
-    Params prm{1, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
-    fif_ltab_kernel<Real, NC><<<(int)((p->n + 256) / 256), 256, 0, s>>>(tab, prm);
-  }
   static void test_inner(const fif_plan_s* p, int L, const void* in, void* out, int32_t* N, int64_t batch,
                          cudaStream_t s) {
     Params prm{batch, p->xi, p->delta * p->delta, p->max_inner, p->max_imfs, (int32_t)p->window, p->stop, p->delta, p->gamma, p->mask};
@@ -127,7 +122,7 @@ template <typename Real, int NC>
 const ResOps* res_entry() {
   using I = Inst<Real, NC>;
   static const ResOps ops{&I::prepare,    &I::occupancy,  I::K::T,        I::K::smem_bytes, &I::decompose, &I::test_rfft,
-                          &I::test_irfft, &I::test_extrema, &I::test_window, &I::test_inner, &I::fill_wtab, &I::fill_ltab};
+                          &I::test_irfft, &I::test_extrema, &I::test_window, &I::test_inner, &I::fill_wtab};
   return &ops;
 }
 template <typename Real>

@@ -66,9 +66,6 @@ struct Params {
   // fp64 plans: double2 {w_hat_k, a_k^(max_inner-1)} (the cap probe's power chain precomputed by the
   // kernel's own code, bit-identical); fp32 plans: Real w_hat_k.
   const void* wtab = nullptr;
-  // a3 for every extrema count: ltab[k] = L(k), k = 0..n (fif_ltab_kernel: filter_half_length itself,
-  // bit-identical); nullptr: evaluated per IMF.  One cached load instead of an fp64 division per IMF.
-  const int32_t* ltab = nullptr;
 };
 
 // ------------------------------------------------------------------ a5 alternative: a-priori N0
@@ -1099,9 +1096,9 @@ struct Resident {
       if (p.mask == 1) {  // spectral-peak rule: L from k = 2 f* (A20)
         const int fs = spectral_peak(X, Xn, sm, last, slot, j);
         if (fs == 0) break;
-        L = p.ltab ? __ldg(p.ltab + 2 * fs) : filter_half_length(p, 2 * fs);
+        L = filter_half_length(p, 2 * fs);
       } else {
-        L = p.ltab ? __ldg(p.ltab + k) : filter_half_length(p, k);
+        L = filter_half_length(p, k);
       }
       const Real invL = (Real)1 / (Real)L;
       V v[R], Dn{0, 0};
@@ -1301,15 +1298,6 @@ __global__ void __launch_bounds__(NC / kR) fif_wtab_kernel(void* __restrict__ ta
     for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = (Real)w[q];
     if (j == 0) row[NC] = (Real)w[kR];
   }
-}
-
-// a3 table (reading A8 rule): L for every extrema count k = 2..n by the kernel's own
-// filter_half_length (so a table-driven decomposition is bit-identical); k < 2 never reaches a3.
-template <typename Real, int NC>
-__global__ void fif_ltab_kernel(int32_t* __restrict__ ltab, Params p) {
-  using K = Resident<Real, NC>;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= K::n; k += gridDim.x * blockDim.x)
-    ltab[k] = k >= 2 ? K::filter_half_length(p, k) : 0;
 }
 
 template <typename Real, int NC, int CAP>

@@ -324,7 +324,8 @@ fif_status st_setup_t(fif_plan_s* p) {
   for (int i = 0; i < g.L - 1; ++i)  // three tile buffers + the level's twiddles
     p->st_smem_col[i] = 3 * sizeof(V) * (size_t)g.lv[i].C * g.lv[i].pitch + sizeof(V) * (size_t)g.lv[i].F;
   p->st_smem_rows = 2 * sizeof(V) * 2 * (size_t)g.lv[g.L - 1].pitch;
-  size_t smax = p->st_smem_rows;
+  p->st_smem_rows_inv = 3 * sizeof(V) * 2 * (size_t)g.lv[g.L - 1].pitch;  // two staging buffers + the FFT's
+  size_t smax = p->st_smem_rows_inv;
   for (int i = 0; i < g.L - 1; ++i) smax = smax > p->st_smem_col[i] ? smax : p->st_smem_col[i];
   cudaError_t e = cudaSuccess;
   auto attr = [&](auto kern) {
@@ -355,8 +356,8 @@ fif_status st_setup_t(fif_plan_s* p) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, st::k_col<Real, 1, st::PASS_INV_LAST>, st::kColThreads, smax);
     p->st_grid_col = p->num_sms * (occ > 0 ? occ : 1);
   }
-  p->st_grid_rows = p->st_row_rs ? occ_grid(p, st::k_rows_inv<Real, kFastCap, 1, 1>, p->st_smem_rows)
-                                 : occ_grid(p, st::k_rows_inv<Real, kFastCap, 1, 0>, p->st_smem_rows);
+  p->st_grid_rows = p->st_row_rs ? occ_grid(p, st::k_rows_inv<Real, kFastCap, 1, 1>, p->st_smem_rows_inv)
+                                 : occ_grid(p, st::k_rows_inv<Real, kFastCap, 1, 0>, p->st_smem_rows_inv);
   p->st_grid_probe = occ_grid(p, st::k_probe<Real, kFastCap, 1>, 0);
   p->st_grid = p->st_grid_rows;
   for (int i = 0; i < 2; ++i)
@@ -452,10 +453,10 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
       auto rows = [&](auto spec, auto cap, int redo_only) {
         if (p->st_row_rs)
           st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value, 1>
-              <<<grow, TB, p->st_smem_rows, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
+              <<<grow, TB, p->st_smem_rows_inv, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
         else
           st::k_rows_inv<Real, decltype(cap)::value, decltype(spec)::value, 0>
-              <<<grow, TB, p->st_smem_rows, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
+              <<<grow, TB, p->st_smem_rows_inv, s>>>(g, top, g.lv[Lv - 2], out, Xi, Xo, Xni, Xno, tb, c, redo_only);
       };
       auto probe = [&](auto cap, auto mode) {
         st::k_probe<Real, decltype(cap)::value, decltype(mode)::value><<<gprobe, TB, 0, s>>>(g, Xi, Xni, tb, c);

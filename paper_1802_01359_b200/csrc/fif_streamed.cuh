@@ -52,6 +52,9 @@ constexpr int kColThreads = FIF_COL_THREADS;  // block size of the column passes
 #ifndef FIF_ST_MINB
 #define FIF_ST_MINB 3  // resident CTAs per SM the heavy streamed kernels are register-budgeted for
 #endif
+#ifndef FIF_ROWS_MINB
+#define FIF_ROWS_MINB 2  // the inverse row kernel: 3 x 32 KiB of shared memory (two staging buffers + one FFT buffer)
+#endif
 
 struct Level {
   int F;          // sub-FFT length of this digit
@@ -299,8 +302,20 @@ __device__ V* cta_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict
 
 // The same passes with the transform length, a radix schedule and the swizzled pitch known at compile
 // time: constant index math.
-template <int P, int DIR, typename V, int F, int NS, int PITCH = F, int SWZ = 1>
-__device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const V* __restrict__ tw) {
+// the twiddles of the thread's first butterfly of a pass (they depend on neither the data nor the previous
+// pass): loaded BEFORE the pass's barrier, so the table latency overlaps the barrier wait
+template <int P, int DIR, typename V, int F, int NS>
+__device__ __forceinline__ void pass_tw_pre(V (&t)[P], const V* __restrict__ tw) {
+  if constexpr (NS > 1) {
+    constexpr int per = F / P, tstride = F / (NS * P);
+    const int kt = ((int)(threadIdx.x % per) % NS) * tstride;
+#pragma unroll
+    for (int r = 1; r < P; ++r) t[r] = tw[r * kt];
+  }
+}
+template <int P, int DIR, typename V, int F, int NS, int PITCH = F, int SWZ = 1, bool PRE = false>
+__device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const V* __restrict__ tw,
+                                           const V (&tpre)[P]) {
   constexpr int per = F / P, tstride = F / (NS * P);
   for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
     const int f = idx / per, vt = idx % per, k = vt % NS;
@@ -309,9 +324,10 @@ __device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const
     for (int r = 0; r < P; ++r) x[r] = src[sidx<V>(f, vt + r * per, PITCH, SWZ)];
     if constexpr (NS > 1) {
       const int kt = k * tstride;
+      const bool first = PRE && idx == (int)threadIdx.x;
 #pragma unroll
       for (int r = 1; r < P; ++r) {
-        V t = tw[r * kt];
+        V t = first ? tpre[r] : tw[r * kt];
         if (DIR > 0) t.y = -t.y;
         x[r] = cmul(x[r], t);
       }
@@ -322,10 +338,26 @@ __device__ __forceinline__ void cta_pass_c(const V* src, V* dst, int cols, const
     for (int r = 0; r < P; ++r) dst[sidx<V>(f, j0 + r * NS, PITCH, SWZ)] = x[r];
   }
 }
+// PRE: twiddles from global memory, prefetched ahead of each pass's barrier (the row passes); the column
+// passes read theirs from shared memory and keep the registers
+template <int DIR, typename V, int F, int NS, int P, int... Rest>
+__device__ __forceinline__ V* cta_fft_c_pre(V* a, V* b, int cols, const V* __restrict__ tw) {
+  V tpre[P];
+  pass_tw_pre<P, DIR, V, F, NS>(tpre, tw);
+  __syncthreads();
+  cta_pass_c<P, DIR, V, F, NS, F, 1, true>(a, b, cols, tw, tpre);
+  if constexpr (sizeof...(Rest) == 0) {
+    __syncthreads();
+    return b;
+  } else {
+    return cta_fft_c_pre<DIR, V, F, NS * P, Rest...>(b, a, cols, tw);
+  }
+}
 template <int DIR, typename V, int F, int NS, int P, int... Rest>
 __device__ __forceinline__ V* cta_fft_c(V* a, V* b, int cols, const V* __restrict__ tw) {
+  V tpre[P];
   __syncthreads();
-  cta_pass_c<P, DIR, V, F, NS>(a, b, cols, tw);
+  cta_pass_c<P, DIR, V, F, NS>(a, b, cols, tw, tpre);
   if constexpr (sizeof...(Rest) == 0) {
     __syncthreads();
     return b;
@@ -336,8 +368,9 @@ __device__ __forceinline__ V* cta_fft_c(V* a, V* b, int cols, const V* __restric
 // the same for an unswizzled (odd-pitch) level: the mixed-radix column lengths
 template <int DIR, typename V, int F, int NS, int P, int... Rest>
 __device__ __forceinline__ V* cta_fft_c_odd(V* a, V* b, int cols, const V* __restrict__ tw) {
+  V tpre[P];
   __syncthreads();
-  cta_pass_c<P, DIR, V, F, NS, F + 1, 0>(a, b, cols, tw);
+  cta_pass_c<P, DIR, V, F, NS, F + 1, 0>(a, b, cols, tw, tpre);
   if constexpr (sizeof...(Rest) == 0) {
     __syncthreads();
     return b;
@@ -361,8 +394,8 @@ __device__ __forceinline__ bool sched_is(const Level& lv) {
 // 2048 = 8 16 16), 0 = the generic passes.
 template <int DIR, typename V, int RS>
 __device__ __forceinline__ V* row_fft(V* a, V* b, const Level& lv, int cols, const V* __restrict__ tw) {
-  if constexpr (RS == 1 && sizeof(V) == 16) return cta_fft_c<DIR, V, 1024, 1, 2, 8, 8, 8>(a, b, cols, tw + lv.twoff);
-  else if constexpr (RS == 1) return cta_fft_c<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw + lv.twoff);
+  if constexpr (RS == 1 && sizeof(V) == 16) return cta_fft_c_pre<DIR, V, 1024, 1, 2, 8, 8, 8>(a, b, cols, tw + lv.twoff);
+  else if constexpr (RS == 1) return cta_fft_c_pre<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw + lv.twoff);
   else return cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(a, b, lv, cols, tw);
 }
 // Column transforms.  CS selects, per kernel instance, ONE transform path (the host picks it from the
@@ -740,6 +773,33 @@ static __global__ void k_init(const __grid_constant__ Geo g, const __grid_consta
   }
 }
 
+// ------------------------------------------------------------------ bulk copies (TMA engine)
+// cp.async.bulk global -> shared with mbarrier completion (transaction bytes): one instruction moves a whole
+// contiguous row; the copy engine runs it while the CTA transforms the previous unit.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// generic-proxy accesses to a buffer (ordered by a barrier) before the async proxy refills it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // ------------------------------------------------------------------ column passes
 enum { PASS_MID = 0, PASS_FWD_FIRST = 1, PASS_INV_LAST = 2 };
 
@@ -1089,7 +1149,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
 // the K-ary search reads the untouched X_in, and a SPEC = 0 launch with redo_only recomputes X_out
 // and the IMF slot for those signals.  X_in / X_out (and the Nyquist bins) ping-pong per IMF.
 template <typename Real, int CAP, int SPEC, int RS = 0>
-__global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
+__global__ void __launch_bounds__(kThreads, FIF_ROWS_MINB) k_rows_inv(
     const __grid_constant__ Geo g, const __grid_constant__ Level lv, const __grid_constant__ Level lvn,
     Real* __restrict__ imfs,
     const typename Cx<Real>::V* __restrict__ Xin, typename Cx<Real>::V* __restrict__ Xout,
@@ -1099,63 +1159,107 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
   extern __shared__ __align__(16) char smem_raw[];
   __shared__ double sred[kNW][2];
   __shared__ int last;
-  V* A = reinterpret_cast<V*>(smem_raw);
-  V* Bf = A + 2 * lv.pitch;
+  __shared__ __align__(8) uint64_t mbar[2];
   const int F = lv.F;
+  // two staging buffers for the unit's rows (filled by the bulk-copy engine, linear row layout) and the
+  // FFT's first buffer; the current staging buffer doubles as the FFT's second one once it is read
+  const size_t rowbuf = 2 * (size_t)lv.pitch;
+  V* St0 = reinterpret_cast<V*>(smem_raw);
+  V* Bf = St0 + 2 * rowbuf;
   const double invn = 1.0 / (double)g.n;
   const uint32_t units = (uint32_t)g.units;
   // redo launch: only the listed signals (SD(cap) <= delta)
   const uint32_t ntile = (!SPEC && redo_only) ? (uint32_t)(*c.scnt) * units : (uint32_t)(g.batch * g.units);
-  for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x) {
-    uint32_t b = t / units;
-    const uint32_t u = t - b * units;
-    if (!SPEC && redo_only) b = (uint32_t)c.slist[b];
-    if (!c.active[b] || (!SPEC && redo_only && !c.redo[b])) continue;
+  auto sig_of = [&](uint32_t t) -> uint32_t {
+    const uint32_t b = t / units;
+    return (!SPEC && redo_only) ? (uint32_t)c.slist[b] : b;
+  };
+  auto wanted = [&](uint32_t t) {
+    const uint32_t b = sig_of(t);
+    return c.active[b] && !(!SPEC && redo_only && !c.redo[b]);
+  };
+  auto next = [&](uint32_t t) {
+    for (; t < ntile; t += gridDim.x)
+      if (wanted(t)) return t;
+    return ntile;
+  };
+  // one thread issues the unit's row copies: one bulk copy per (contiguous) row, completion on mbar[stg]
+  auto issue = [&](uint32_t t, int stg) {
+    const uint32_t b = sig_of(t), u = t % units;
+    int64_t ra, rb, bA;
+    int two;
+    pair_of<Real>(g, u, ra, rb, bA, two);
+    const V* Xb = Xin + (int64_t)b * g.NC;
+    const uint32_t rowb = (uint32_t)(F * sizeof(V));
+    V* dst = St0 + stg * rowbuf;
+    mbar_expect_tx(&mbar[stg], two ? 2 * rowb : rowb);
+    bulk_g2s(dst, Xb + ra * F, rowb, &mbar[stg]);
+    if (two) bulk_g2s(dst + F, Xb + rb * F, rowb, &mbar[stg]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // per-thread constants of the window / twiddle recurrences (bin k = base + P i, i = tid + j blockDim)
+  const double2 Ekstep = E64(tb.Eh, tb.El, g.eb, (int64_t)g.P * blockDim.x);  // e^{i pi P blockDim/n}
+  uint32_t t = next(blockIdx.x);
+  if (threadIdx.x == 0 && t < ntile) issue(t, 0);
+  uint32_t phase = 0;  // bit s: parity of the next wait on mbar[s]
+  for (int it = 0; t < ntile; ++it) {
+    const int cs = it & 1;
+    const uint32_t tn = next(t + gridDim.x);
+    if (threadIdx.x == 0 && tn < ntile) {
+      fence_proxy_async();  // the other buffer's generic-proxy use (last iteration's FFT) precedes the copy
+      issue(tn, cs ^ 1);
+    }
+    const uint32_t b = sig_of(t), u = t % units;
     int64_t ra, rb, bA;
     int two;
     pair_of<Real>(g, u, ra, rb, bA, two);
     const int L = c.L[b], N = SPEC ? g.max_inner : c.N[b];
-    const V* Xb = Xin + b * g.NC;
-    V* Xo = Xout + b * g.NC;
-    {
-      constexpr int UR = TileCap<Real>::value / 2 / kThreads;
-      // the mirror row is loaded unconditionally (the row itself when there is none): a conditionally
-      // assigned register array is kept in local memory, which serialises the loads behind its spills
-      const int64_t rbb = two ? rb : ra;
-      V xa[UR], xb[UR];
-#pragma unroll
-      for (int j = 0; j < UR; ++j) {
-        const int i = threadIdx.x + j * kThreads;
-        const int ic = i < F ? i : 0;
-        xa[j] = Xb[ra * F + ic];
-        xb[j] = Xb[rbb * F + ic];
-      }
-#pragma unroll
-      for (int j = 0; j < UR; ++j) {
-        const int i = threadIdx.x + j * kThreads;
-        if (i < F) {
-          A[sidx<V>(0, i, lv.pitch, lv.swz)] = xa[j];
-          if (two) A[sidx<V>(1, i, lv.pitch, lv.swz)] = xb[j];
-        }
-      }
-    }
-    __syncthreads();
+    V* Xo = Xout + (int64_t)b * g.NC;
+    V* A = St0 + cs * rowbuf;
     const int cb = two ? 1 : 0;
     double sP = 0.0, sQ = 0.0;
-    // L k mod n, advanced by L P blockDim per iteration
-    // 32-bit bin arithmetic (n <= 2^27: k, L k mod n and mk + mstep < 2^31)
-    const int n32 = (int)g.n, P32 = (int)g.P, bA32 = (int)bA;
-    int mk = (int)mod_n((int64_t)L * (bA + g.P * threadIdx.x), g.n, invn);
-    const int mstep = (int)mod_n((int64_t)L * ((g.P * blockDim.x) % g.n), g.n, invn);
-    for (int i = threadIdx.x; i < F; i += blockDim.x, mk = (mk + mstep >= n32) ? mk + mstep - n32 : mk + mstep) {
+    // e^{i pi k/n} and e^{i pi L k/n} advance geometrically over the thread's bins (a few complex products
+    // instead of two scattered table gathers per bin pair): sin(pi k/n) = Im, sin(pi r_k/n) = |Im e^{i pi Lk/n}|
+    // (the table reads are issued before the wait for the rows, so their latency overlaps the copy)
+    const int64_t k0 = bA + g.P * (int64_t)threadIdx.x;
+    const int64_t n2 = 2 * g.n;
+    double2 Ek = E64(tb.Eh, tb.El, g.eb, k0);
+    double2 Sk = E64(tb.Eh, tb.El, g.eb, mod_n((int64_t)L * k0 % n2, n2, 0.5 * invn));
+    const double2 Ss = E64(tb.Eh, tb.El, g.eb, ((int64_t)L * ((g.P * blockDim.x) % n2)) % n2);
+    const V xn0 = Xnin[b];
+    mbar_wait(&mbar[cs], (phase >> cs) & 1u);
+    phase ^= 1u << cs;
+    const int P32 = (int)g.P, bA32 = (int)bA;
+    for (int i = threadIdx.x; i < F; i += blockDim.x, Ek = cmul(Ek, Ekstep), Sk = cmul(Sk, Ss)) {
       int tm;
       if (!mirror_t(g, bA, two, F, i, tm)) continue;
       const int k = bA32 + P32 * i;
-      const V xk = A[sidx<V>(0, i, lv.pitch, lv.swz)];
-      const V xm = k == 0 ? Xnin[b] : A[sidx<V>(cb, tm, lv.pitch, lv.swz)];
+      const V xk = A[i];
+      const V xm = k == 0 ? xn0 : A[cb * F + tm];
       double wk, wm;
-      double2 Ek;
-      what_pair_m(g, tb, L, k, mk, wk, wm, Ek);
+      {
+        const double nk = fabs(Sk.y), nm = (L & 1) ? fabs(Sk.x) : fabs(Sk.y);
+        const double dk = Ek.y, dm = Ek.x;
+        const double Ld = (double)L;
+        double sk, sm;
+        if (k == 0) {
+          sk = 1.0;
+          sm = nm / (Ld * dm);
+        } else {
+          const double inv = 1.0 / (Ld * Ld * dk * dm);
+          sk = nk * Ld * dm * inv;
+          sm = nm * Ld * dk * inv;
+        }
+        sk *= sk;
+        sm *= sm;
+        wk = sk * sk;
+        wm = sm * sm;
+      }
       const double ak = 1.0 - wk, am = 1.0 - wm;
       double dk, dm;
       if (SPEC) {
@@ -1212,8 +1316,9 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
         sred[threadIdx.x >> 5][1] = sQ;
       }
     }
-    V* out = row_fft<1, V, RS>(Bf, A, lv, two ? 2 : 1, tb.tw);  // (its first barrier also publishes sred)
-    V* W = reinterpret_cast<V*>(imfs + b * g.sig_stride + (int64_t)c.M[b] * g.n);
+    // (its first barrier publishes Bf and sred and ends every read of A, which becomes its second buffer)
+    V* out = row_fft<1, V, RS>(Bf, A, lv, two ? 2 : 1, tb.tw);
+    V* W = reinterpret_cast<V*>(imfs + (int64_t)b * g.sig_stride + (int64_t)c.M[b] * g.n);
     // the next (coarser) level's conjugate twiddle e^{+2 pi i s k'/(F' S')}: s = element, k' = row mod F'
     // (geometric in i: two table products per row and thread, one multiply per element)
     const int64_t ka = ra % lvn.F, kb = rb % lvn.F;
@@ -1234,8 +1339,8 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
         double v = 0.0;
         for (int w = 0; w < kNW; ++w) v += sred[w][threadIdx.x];
         c.red[((int64_t)b * g.nbch + u) * (2 * kProbes) + threadIdx.x] = v;
+        __threadfence();  // (only the writers fence: their partials are visible before the counter moves)
       }
-      __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) last = atomicAdd(c.cnt + b, 1u) == (uint32_t)(g.units - 1);
       __syncthreads();
@@ -1276,6 +1381,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_inv(
       }
     }
     __syncthreads();
+    t = tn;
   }
 }
 
