@@ -143,6 +143,9 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
   fif_plan_s* p = new fif_plan_s();
   p->n = n; p->batch = batch; p->dtype = dtype; p->window = window; p->xi = xi; p->delta = delta;
   p->max_inner = max_inner; p->max_imfs = max_imfs; p->NC = (int)(NC < (1 << 30) ? NC : 0); p->regime = reg;
+  // test-only knob: cap every persistent grid (other CTA schedules of the same decomposition must give the
+  // same bits -- the determinism / race check that stands in for compute-sanitizer, closed on this pool)
+  if (const char* gc = getenv("FIF_GRID_CAP")) p->grid_cap = atoi(gc) > 0 ? atoi(gc) : 0;
   if (cudaGetDevice(&p->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
     free_plan(p);
@@ -268,6 +271,7 @@ static fif_status create_dist(fif_plan_t* out, int64_t n, fif_dtype dtype, fif_w
   fif_plan_s* p = new fif_plan_s();
   p->n = n; p->batch = 1; p->dtype = dtype; p->window = window; p->xi = xi; p->delta = delta;
   p->max_inner = max_inner; p->max_imfs = max_imfs; p->regime = 2;
+  if (const char* gc = getenv("FIF_GRID_CAP")) p->grid_cap = atoi(gc) > 0 ? atoi(gc) : 0;
   if (cudaGetDevice(&p->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
     free_plan(p);
@@ -296,6 +300,9 @@ fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int3
   if (!d_signals || !d_imfs || !d_imf_count || !d_filter_len || !d_iters) return FIF_ERR_INVALID_ARG;
   if (((uintptr_t)d_signals | (uintptr_t)d_imfs) & 15) return FIF_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  Nvtx range(p->regime == 2 ? "fif_decompose/distributed"
+                            : p->regime == 1 ? "fif_decompose/streamed"
+                                             : p->regime == 3 ? "fif_decompose/iterative" : "fif_decompose/resident");
   if (p->regime == 2) {
     fif_status st = dist_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, s);
     if (st != FIF_OK) return st;
@@ -321,6 +328,7 @@ fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs,
   if (!h_signals || !h_imfs || !h_imf_count || !h_filter_len || !h_iters) return FIF_ERR_INVALID_ARG;
   if (p->regime == 2) return FIF_ERR_INVALID_ARG;  // distributed plans take device buffers
   if (p->regime == 1 && (!p->d_X || !p->d_ctl)) return FIF_ERR_INVALID_ARG;  // no workspace bound
+  Nvtx range("fif_decompose_host");
   const size_t es = elem_size(p->dtype);
   const size_t in_sig = (size_t)p->n * es, out_sig = in_sig * (size_t)(p->max_imfs + 1);
   const size_t meta_sig = (size_t)(1 + 2 * p->max_imfs);

@@ -866,6 +866,11 @@ fif_status dist_setup_t(fif_plan_s* p, DistPlan& D) {
   D.grid_pass = p->num_sms * (occ > 0 ? occ : 1);
   D.grid_elem = p->num_sms * 8;
   D.grid_probe = p->num_sms * 3;
+  if (p->grid_cap > 0) {  // test knob (FIF_GRID_CAP): other CTA schedules, same bits
+    D.grid_pass = D.grid_pass < p->grid_cap ? D.grid_pass : p->grid_cap;
+    D.grid_elem = D.grid_elem < p->grid_cap ? D.grid_elem : p->grid_cap;
+    D.grid_probe = D.grid_probe < p->grid_cap ? D.grid_probe : p->grid_cap;
+  }
   D.rounds = 0;
   for (int64_t len = p->max_inner; len > 1; len = (len + kProbes) / (kProbes + 1)) ++D.rounds;
   // per-rank buffers
@@ -1011,6 +1016,7 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
   ext_gather();
   all([&](int li, DRank& R) { k_d_decide_ext<<<1, 1, 0, s>>>(R.d, R.c, 0, lens + li * p->max_imfs, its + li * p->max_imfs); });
   // ---- a1 forward transform
+  Nvtx fwd_range("distributed/forward");
   // peer tables of local rank li: U pointers, T pointers (device), and the partner's T (host value)
   auto ptabU = [&](int li) { return (V* const*)((void**)D.dpeer + (size_t)li * 2 * D.P); };
   auto ptabT = [&](int li) { return (V* const*)((void**)D.dpeer + (size_t)li * 2 * D.P + D.P); };
@@ -1050,6 +1056,7 @@ fif_status dist_decompose_t(fif_plan_s* p, DistPlan& D, const void* sig, void* i
   }
   // ---- IMFs
   for (int m = 0; m < p->max_imfs; ++m) {
+    Nvtx imf_range("distributed/imf");
     // a4/a5: cap probe, then K-ary rounds (device-side early exit when not searching)
     all([&](int, DRank& R) {
       if (fast) k_d_probe<Real, kFastCap, 0><<<gp, TB, 0, s>>>(R.d, (const V*)R.X, (const V*)R.Xm, tb, R.c);

@@ -6,11 +6,22 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fif.h"
 #include "fif_streamed.cuh"
 
 namespace fifhost {
 struct DistPlan;
+
+// NVTX range for the duration of a scope (header-only NVTX3: a no-op unless a profiler such as nsys or
+// ncu --nvtx is attached).  Names the host phases that enqueue the kernels of each regime.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 enum { FIF_MAX_STAGES = 3 };
 // max_inner value with a compile-time-specialised kernel (the paper's/BASELINE's cap of 200,
@@ -43,6 +54,7 @@ struct fif_plan_s {
   void* d_tw = nullptr;    // V[twtotal]  Stockham twiddles e^{-2 pi i k r/(NS RP)}
   void* d_wtab = nullptr;  // Real[(n-1)/4 - 1][NC+1] per-L eigenvalue table (fif_plan_set_eigen_table)
   int block = 0, occ = 0;
+  int grid_cap = 0;        // > 0: persistent grids capped at this many CTAs (FIF_GRID_CAP at creation; tests)
   size_t smem = 0;
   int regime = 0;  // 0 resident, 1 streamed
   // streamed regime

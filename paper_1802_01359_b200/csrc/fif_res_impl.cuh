@@ -69,7 +69,8 @@ struct Inst {
     const bool fast = p->max_inner == kFastCap, tab = p->d_wtab != nullptr;
     auto kern = fast ? (tab ? fif_resident_kernel<Real, NC, kFastCap, true> : fif_resident_kernel<Real, NC, kFastCap, false>)
                      : (tab ? fif_resident_kernel<Real, NC, 0, true> : fif_resident_kernel<Real, NC, 0, false>);
-    const int64_t cap = (int64_t)p->num_sms * (tab ? occ_tab() : p->occ);  // persistent grid: one wave
+    int64_t cap = (int64_t)p->num_sms * (tab ? occ_tab() : p->occ);  // persistent grid: one wave
+    if (p->grid_cap > 0 && p->grid_cap < cap) cap = p->grid_cap;
     const int grid = (int)(batch < cap ? batch : cap);
     kern<<<grid, K::T, tab ? KT::smem_bytes : K::smem_bytes, s>>>((const Real*)sig, (Real*)imfs, cnt, lens, its,
                                                                  (const Real*)p->d_sin, (const Real*)p->d_isin,

@@ -383,6 +383,7 @@ st::Ctl ctl_at(const st::Ctl& c, const st::Geo& g, int64_t b0, size_t rsz) {
   return r;
 }
 int grid_for(int64_t work, int cap) { return (int)(work < cap ? (work > 0 ? work : 1) : cap); }
+int capped(const fif_plan_s* p, int g) { return p->grid_cap > 0 && p->grid_cap < g ? p->grid_cap : g; }
 
 // the whole decomposition as stream-ordered kernels (no host synchronisation), one L2 wave at a time
 template <typename Real>
@@ -423,11 +424,12 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     const int Lv = g.L;
     const bool fast = g.max_inner == kFastCap;
     const st::Level& top = g.lv[Lv - 1];
-    const int gcol = p->st_grid_col, grow = grid_for(g.batch * g.units, p->st_grid_rows);
-    const int gprobe = grid_for(g.batch * g.nbch, p->st_grid_probe);
-    const int gfold = grid_for(g.batch * g.ngrp, p->num_sms * 4);
+    const int gcol = capped(p, p->st_grid_col), grow = grid_for(g.batch * g.units, capped(p, p->st_grid_rows));
+    const int gprobe = grid_for(g.batch * g.nbch, capped(p, p->st_grid_probe));
+    const int gfold = grid_for(g.batch * g.ngrp, capped(p, p->num_sms * 4));
     const int gsig = (int)((g.batch + TB - 1) / TB);
     auto col = [&](int i) { return grid_for(g.batch * g.lv[i].tiles, gcol); };
+    Nvtx wave("streamed/wave");
     st::k_init<<<gsig, TB, 0, s>>>(g, c);
     launch_col<Real, -1, st::PASS_FWD_FIRST>(p->st_col_cs[0], col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
     st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
@@ -442,6 +444,7 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     };
     peaks(X, Xn);
     for (int m = 0; m < g.max_imfs; ++m) {
+      Nvtx imf("streamed/imf");
       V* Xi = (m & 1) ? Xalt : X;
       V* Xo = (m & 1) ? X : Xalt;
       V* Xni = (m & 1) ? Xnalt : Xn;
