@@ -55,9 +55,12 @@ typedef enum {
   FIF_REGIME_RESIDENT = 1,  /* one CTA per signal, r and r_hat on chip for all IMFs (power-of-two 512 <= n <= 8192;
                                fp32 also n = 16384) */
   FIF_REGIME_STREAMED = 2,  /* spectrum / work buffers in HBM, multi-level FFT, a short kernel sequence per IMF */
-  FIF_REGIME_ITERATIVE = 3  /* the baseline the paper compares FIF against: Algorithm 2 run
+  FIF_REGIME_ITERATIVE = 3, /* the baseline the paper compares FIF against: Algorithm 2 run
                                literally, N circular convolutions s <- s - w (*) s per IMF (fp64, n <= 4096);
                                same decisions and readings; never chosen by AUTO */
+  FIF_REGIME_CLUSTER = 4    /* one signal per thread-block cluster of P = 2, 4, 8 CTAs, r and r_hat on chip
+                               for all IMFs, four-step FFT over the cluster (fp64, n/2 = 4096 P: n = 16384,
+                               32768, 65536); chosen by AUTO for those n when a cluster fits */
 } fif_regime;
 
 /* Create a plan for `batch` independent signals of length n.

@@ -16,35 +16,6 @@ using namespace fifhost;
 
 namespace {
 
-// ---------------------------------------------------------------- tables (host, long double)
-template <typename Real>
-void build_tables(int64_t n, int NC, std::vector<Real>& sint, std::vector<Real>& isin,
-                  std::vector<typename Cx<Real>::V>& tw) {
-  const long double PI = 3.141592653589793238462643383279502884L;
-  sint.assign(NC + 1, (Real)0);
-  isin.assign(NC + 1, (Real)0);
-  for (int j = 0; j <= NC; ++j) {
-    // sin(pi j / n), j <= n/2; reflect to keep the argument <= pi/4 for accuracy
-    long double v;
-    if (2 * (int64_t)j <= n / 2) v = sinl(PI * (long double)j / (long double)n);
-    else v = cosl(PI * (long double)(n / 2 - j) / (long double)n);
-    sint[j] = (Real)v;
-    isin[j] = j ? (Real)(1.0L / v) : (Real)0;
-  }
-  const int P = sched_passes(NC);
-  tw.assign(sched_twtotal(NC) > 0 ? sched_twtotal(NC) : 1, typename Cx<Real>::V{0, 0});
-  for (int p = 1; p < P; ++p) {
-    const int RP = sched_radix(NC, p), NS = sched_ns(NC, p), off = sched_twoff(NC, p);
-    const int64_t den = (int64_t)NS * RP;
-    for (int r = 1; r < RP; ++r)
-      for (int k = 0; k < NS; ++k) {
-        const int64_t m = ((int64_t)k * r) % den;
-        const long double th = 2.0L * PI * (long double)m / (long double)den;
-        tw[off + (r - 1) * NS + k] = typename Cx<Real>::V{(Real)cosl(th), (Real)(-sinl(th))};
-      }
-  }
-}
-
 template <typename Real>
 fif_status upload_tables(fif_plan_s* p) {
   std::vector<Real> sint, isin;
@@ -80,6 +51,7 @@ void free_plan(fif_plan_s* p) {
   cudaFree(p->d_wtab);
   st_free(p);
   dist_free(p);
+  cl_free(p);
   for (int i = 0; i < p->nstages; ++i) {
     cudaFree(p->st[i].d_in);
     cudaFree(p->st[i].d_out);
@@ -119,7 +91,7 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
       max_imfs < 1 || (dtype != FIF_F64 && dtype != FIF_F32) ||
       (window != FIF_WINDOW_TRI_SQ && window != FIF_WINDOW_TRI_SQ_WIDE) ||
       (regime != FIF_REGIME_AUTO && regime != FIF_REGIME_RESIDENT && regime != FIF_REGIME_STREAMED &&
-       regime != FIF_REGIME_ITERATIVE))
+       regime != FIF_REGIME_ITERATIVE && regime != FIF_REGIME_CLUSTER))
     return FIF_ERR_INVALID_ARG;
   if (n % 2 != 0) return FIF_ERR_UNSUPPORTED_N;
   const int64_t NC = n / 2;
@@ -133,8 +105,11 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
   } else if (regime == FIF_REGIME_ITERATIVE) {
     if (dtype != FIF_F64 || n > 4096) return FIF_ERR_UNSUPPORTED_N;
     reg = 3;
+  } else if (regime == FIF_REGIME_CLUSTER) {
+    if (!cl_cluster_size(n, dtype)) return FIF_ERR_UNSUPPORTED_N;
+    reg = 4;
   } else {
-    reg = resident_ok ? 0 : 1;
+    reg = resident_ok ? 0 : (cl_cluster_size(n, dtype) ? 4 : 1);
   }
   if (reg == 1) {  // host-side check of the streamed factorisation before any CUDA call
     st::Geo g;
@@ -159,6 +134,19 @@ fif_status fif_plan_create_ex(fif_plan_t* out, int64_t n, int64_t batch, fif_dty
   }
   if (reg == 1) {
     fif_status st = st_setup(p);
+    if (st != FIF_OK) { free_plan(p); return st; }
+    *out = p;
+    return FIF_OK;
+  }
+  if (reg == 4) {
+    fif_status st = cl_setup(p);
+    if (st == FIF_ERR_UNSUPPORTED_N && regime == FIF_REGIME_AUTO) {  // no cluster fits: the streamed regime
+      cl_free(p);
+      p->d_cl_scr = nullptr;
+      p->regime = reg = 1;
+      st::Geo g;
+      st = st_geometry(n, dtype == FIF_F64, g) ? st_setup(p) : FIF_ERR_UNSUPPORTED_N;
+    }
     if (st != FIF_OK) { free_plan(p); return st; }
     *out = p;
     return FIF_OK;
@@ -190,7 +178,7 @@ fif_status fif_plan_set_options(fif_plan_t p, fif_stop_rule stop, double gamma) 
 
 fif_status fif_plan_set_mask_rule(fif_plan_t p, fif_mask_rule rule) {
   if (!p || (rule != FIF_MASK_EXTREMA && rule != FIF_MASK_SPECTRAL)) return FIF_ERR_INVALID_ARG;
-  if (rule == FIF_MASK_SPECTRAL && (p->regime == 2 || p->regime == 3)) return FIF_ERR_UNSUPPORTED_N;
+  if (rule == FIF_MASK_SPECTRAL && (p->regime == 2 || p->regime == 3 || p->regime == 4)) return FIF_ERR_UNSUPPORTED_N;
   const int32_t old = p->mask;
   p->mask = (int32_t)rule;
   if (p->regime == 1 && old != p->mask) {  // the power array lives in the workspace: re-carve it
@@ -301,8 +289,9 @@ fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int3
   if (((uintptr_t)d_signals | (uintptr_t)d_imfs) & 15) return FIF_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   Nvtx range(p->regime == 2 ? "fif_decompose/distributed"
-                            : p->regime == 1 ? "fif_decompose/streamed"
-                                             : p->regime == 3 ? "fif_decompose/iterative" : "fif_decompose/resident");
+             : p->regime == 1 ? "fif_decompose/streamed"
+             : p->regime == 3 ? "fif_decompose/iterative"
+             : p->regime == 4 ? "fif_decompose/cluster" : "fif_decompose/resident");
   if (p->regime == 2) {
     fif_status st = dist_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, s);
     if (st != FIF_OK) return st;
@@ -315,6 +304,10 @@ fif_status fif_decompose(fif_plan_t p, const void* d_signals, void* d_imfs, int3
   }
   if (p->regime == 3) {
     it_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
+    return launch_status();
+  }
+  if (p->regime == 4) {
+    cl_decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
     return launch_status();
   }
   res_ops(p->dtype, p->NC)->decompose(p, d_signals, d_imfs, d_imf_count, d_filter_len, d_iters, p->batch, s);
@@ -386,6 +379,8 @@ fif_status fif_decompose_host(fif_plan_t p, const void* h_signals, void* h_imfs,
       st_decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, b0, S.stream);
     } else if (p->regime == 3) {
       it_decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
+    } else if (p->regime == 4) {
+      cl_decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
     } else {
       res_ops(p->dtype, p->NC)->decompose(p, S.d_in, S.d_out, d_cnt, d_len, d_it, nb, S.stream);
     }
@@ -431,13 +426,17 @@ int32_t fif_plan_kernels_per_call(fif_plan_t p) {
 const char* fif_plan_regime(fif_plan_t p) {
   if (!p) return "none";
   if (p->regime == 3) return "iterative";
+  if (p->regime == 4) return "cluster";
   return p->regime == 2 ? "distributed" : (p->regime == 1 ? "streamed" : "resident");
 }
 
 fif_status fif_plan_launch_config(fif_plan_t p, int32_t* grid, int32_t* block, int32_t* smem_bytes) {
   if (!p) return FIF_ERR_INVALID_ARG;
-  const int64_t cap = p->regime == 1 ? (int64_t)p->st_grid : (int64_t)p->num_sms * p->occ;
-  if (grid) *grid = (int32_t)(p->batch < cap || p->regime == 1 ? (p->regime == 1 ? cap : p->batch) : cap);
+  const int64_t cap = p->regime == 1 ? (int64_t)p->st_grid
+                      : p->regime == 4 ? (int64_t)p->cl_clusters * p->cl_P : (int64_t)p->num_sms * p->occ;
+  if (grid) *grid = (int32_t)(p->regime == 1 ? cap
+                             : p->regime == 4 ? (p->batch < p->cl_clusters ? p->batch * p->cl_P : cap)
+                                              : (p->batch < cap ? p->batch : cap));
   if (block) *block = p->block;
   if (smem_bytes) *smem_bytes = (int32_t)p->smem;
   return FIF_OK;

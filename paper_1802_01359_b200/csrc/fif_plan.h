@@ -6,7 +6,10 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <math.h>
 #include <nvtx3/nvToolsExt.h>
+
+#include <vector>
 
 #include "../../include/fif.h"
 #include "fif_streamed.cuh"
@@ -56,7 +59,10 @@ struct fif_plan_s {
   int block = 0, occ = 0;
   int grid_cap = 0;        // > 0: persistent grids capped at this many CTAs (FIF_GRID_CAP at creation; tests)
   size_t smem = 0;
-  int regime = 0;  // 0 resident, 1 streamed
+  int regime = 0;  // 0 resident, 1 streamed, 2 distributed, 3 iterative, 4 cluster
+  // cluster regime (fif_cluster.cu)
+  int cl_P = 0, cl_clusters = 0;
+  void* d_cl_scr = nullptr;  // per-cluster L2 scratch (mirror publish + transpose landing regions)
   // streamed regime
   fifgpu::st::Geo geo{};
   void* d_Eh = nullptr;   // double2 e^{i pi (h 2^eb)/n}
@@ -95,6 +101,36 @@ struct fif_plan_s {
 
 namespace fifhost {
 using fifgpu::Cx;
+// ---------------------------------------------------------------- tables (host, long double)
+// sin(pi j/n), 1/sin(pi j/n) (j <= NC) and the Stockham twiddles of the resident FFT of NC points
+template <typename Real>
+inline void build_tables(int64_t n, int NC, std::vector<Real>& sint, std::vector<Real>& isin,
+                  std::vector<typename Cx<Real>::V>& tw) {
+  const long double PI = 3.141592653589793238462643383279502884L;
+  sint.assign(NC + 1, (Real)0);
+  isin.assign(NC + 1, (Real)0);
+  for (int j = 0; j <= NC; ++j) {
+    // sin(pi j / n), j <= n/2; reflect to keep the argument <= pi/4 for accuracy
+    long double v;
+    if (2 * (int64_t)j <= n / 2) v = sinl(PI * (long double)j / (long double)n);
+    else v = cosl(PI * (long double)(n / 2 - j) / (long double)n);
+    sint[j] = (Real)v;
+    isin[j] = j ? (Real)(1.0L / v) : (Real)0;
+  }
+  const int P = fifgpu::sched_passes(NC);
+  tw.assign(fifgpu::sched_twtotal(NC) > 0 ? fifgpu::sched_twtotal(NC) : 1, typename Cx<Real>::V{0, 0});
+  for (int p = 1; p < P; ++p) {
+    const int RP = fifgpu::sched_radix(NC, p), NS = fifgpu::sched_ns(NC, p), off = fifgpu::sched_twoff(NC, p);
+    const int64_t den = (int64_t)NS * RP;
+    for (int r = 1; r < RP; ++r)
+      for (int k = 0; k < NS; ++k) {
+        const int64_t m = ((int64_t)k * r) % den;
+        const long double th = 2.0L * PI * (long double)m / (long double)den;
+        tw[off + (r - 1) * NS + k] = typename Cx<Real>::V{(Real)cosl(th), (Real)(-sinl(th))};
+      }
+  }
+}
+
 // resident regime: per-(dtype, NC) launchers (fif_res_f64.cu, fif_res_f32.cu)
 struct ResOps {
   cudaError_t (*prepare)();
@@ -127,6 +163,13 @@ size_t st_workspace_bytes(const fif_plan_s* p);
 fif_status st_bind_workspace(fif_plan_s* p, void* base, size_t bytes);
 // compile-time transform path of a C x F tile level (st::col_fft CS; 0 = generic)
 int pass_schedule(const fifgpu::st::Level& lv, bool f64);
+
+// cluster-resident regime (fif_cluster.cu): one signal per thread-block cluster, r and r_hat on chip
+int cl_cluster_size(int64_t n, fif_dtype dt);  // 0: not covered
+fif_status cl_setup(fif_plan_s* p);
+void cl_decompose(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, int32_t* lens, int32_t* its, int64_t batch,
+                  cudaStream_t s);
+void cl_free(fif_plan_s* p);
 
 // iterative regime (fif_iterative.cu): Algorithm 2 literally (the IF baseline of PAPER.md:693)
 fif_status it_setup(fif_plan_s* p);

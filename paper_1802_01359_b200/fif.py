@@ -19,7 +19,7 @@ STATUS = {0: "FIF_OK", 1: "FIF_ERR_INVALID_ARG", 2: "FIF_ERR_UNSUPPORTED_N", 3: 
           5: "FIF_ERR_NCCL"}
 
 # every symbol include/fif.h declares (checked by tests/test_abi.py)
-REGIME_AUTO, REGIME_RESIDENT, REGIME_STREAMED, REGIME_ITERATIVE = 0, 1, 2, 3
+REGIME_AUTO, REGIME_RESIDENT, REGIME_STREAMED, REGIME_ITERATIVE, REGIME_CLUSTER = 0, 1, 2, 3, 4
 SYMBOLS = ["fif_plan_create", "fif_plan_create_ex", "fif_decompose", "fif_decompose_host", "fif_destroy", "fif_status_string",
            "fif_plan_kernels_per_call", "fif_plan_regime", "fif_plan_launch_config", "fif_test_rfft",
            "fif_test_irfft", "fif_test_extrema", "fif_test_window_spectrum", "fif_test_inner", "fif_nccl_unique_id",
