@@ -100,7 +100,7 @@ fif_status cl_setup(fif_plan_s* p) {
     return FIF_ERR_UNSUPPORTED_N;
   }
   p->cl_clusters = nclu;
-  // per-cluster scratch: the mirror-publish and transpose regions (2 NC complex each cluster, L2-resident)
+  // per-cluster scratch: the mirror-publish and transpose regions (2 NC complex per cluster, L2-resident)
   const size_t per = (size_t)NC * sizeof(double2);
   if (cudaMalloc(&p->d_cl_scr, 2 * per * (size_t)nclu) != cudaSuccess) return FIF_ERR_OOM;
   p->block = kQ64 / kR;

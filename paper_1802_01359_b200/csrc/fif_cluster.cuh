@@ -72,7 +72,7 @@ struct Clu {
   static constexpr size_t oNbr = oBnd + sizeof(double) * P * P * 4;   // warp lane-0 values [NW][R]
   static constexpr size_t oInt = oNbr + sizeof(Real) * NW * R;        // ints: [NW] counts, [NW] masks, misc
   static constexpr size_t oBar = (oInt + sizeof(int) * (2 * NW + 2 * P + 8) + 15) & ~(size_t)15;
-  static constexpr size_t smem_bytes = oBar + 16;
+  static constexpr size_t smem_bytes = oBar + 32;  // bar (bulk landings), cbar[2] (cluster reductions)
 
   struct Sm {
     V *A, *B, *Rl;
@@ -83,6 +83,7 @@ struct Clu {
     Real* nbr;
     int* ints;
     uint64_t* bar;
+    uint64_t* cbar;  // [2] reduction slots: each CTA's partials land by st.async, counted in transaction bytes
   };
   __device__ static Sm carve(char* base) {
     Sm s;
@@ -97,6 +98,7 @@ struct Clu {
     s.nbr = reinterpret_cast<Real*>(base + oNbr);
     s.ints = reinterpret_cast<int*>(base + oInt);
     s.bar = reinterpret_cast<uint64_t*>(base + oBar);
+    s.cbar = s.bar + 1;
     return s;
   }
 
@@ -106,48 +108,53 @@ struct Clu {
     return cmul(s.Eh[j >> EB], s.El[j & (NEL - 1)]);
   }
 
-  // ---- cluster-wide sum of M doubles (deterministic: block totals, then the P partials in rank order)
-  template <int M>
-  __device__ static void csum(double (&v)[M], const Sm& s, cg::cluster_group& cl, int& slot, int rank, int t) {
+  // ---- cluster-wide sum of M doubles (deterministic: block totals, then the P partials in rank order).
+  // No cluster barrier: every CTA stores its partials into every CTA's slot with st.async, whose bytes
+  // complete a transaction count on the destination's mbarrier (the local arrival announces how many);
+  // each CTA waits on its own barrier only.  `slot` carries the alternating slot (bit 0) and the phase
+  // parity of each slot's barrier (bits 1, 2); a slot is reused two reductions later, when every CTA has
+  // necessarily consumed it.  `extra`: bytes other st.async writes (chunk ends) add to this reduction.
+  __device__ static uint32_t mapa(uint32_t a, int r) {
+    uint32_t x;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(x) : "r"(a), "r"(r));
+    return x;
+  }
+  __device__ static void st_async(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n"
+                 ::"r"(raddr), "l"(__double_as_longlong(v)), "r"(rbar) : "memory");
+  }
+  template <int M, typename S>
+  __device__ static void csum_t(S (&v)[M], const Sm& s, int& slot, int rank, int t, uint32_t extra) {
     static_assert(M <= 8, "");
-    double* red = s.red + slot * 4 * NW;
-    double* cr = s.cred + slot * P * 8;
-    slot ^= 1;
+    const int sl = slot & 1;
+    const uint32_t ph = ((uint32_t)slot >> (1 + sl)) & 1u;
+    slot ^= 1 | (2 << sl);
+    S* red = reinterpret_cast<S*>(s.red + sl * 4 * NW);
+    double* cr = s.cred + sl * P * 8;
     block_sum<NW, M>(v, red, t);
+    if (t == 0) st::mbar_expect_tx(&s.cbar[sl], (uint32_t)(P * M * 8) + extra);
     if (t < P) {
-      double* dst = cl.map_shared_rank(cr, t) + rank * 8;
+      const uint32_t ra = mapa(st::smem_u32(cr + rank * 8), t), rb = mapa(st::smem_u32(&s.cbar[sl]), t);
 #pragma unroll
-      for (int i = 0; i < M; ++i) dst[i] = v[i];
+      for (int i = 0; i < M; ++i) st_async(ra + 8 * i, (double)v[i], rb);
     }
-    cl.sync();
+    st::mbar_wait(&s.cbar[sl], ph);
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       double a = 0.0;
 #pragma unroll
       for (int r = 0; r < P; ++r) a += cr[r * 8 + i];
-      v[i] = a;
+      v[i] = (S)a;
     }
   }
-  // float version for the hint (partials carried as doubles)
   template <int M>
-  __device__ static void csumf(float (&v)[M], const Sm& s, cg::cluster_group& cl, int& slot, int rank, int t) {
-    float* red = reinterpret_cast<float*>(s.red + slot * 4 * NW);
-    double* cr = s.cred + slot * P * 8;
-    slot ^= 1;
-    block_sum<NW, M>(v, red, t);
-    if (t < P) {
-      double* dst = cl.map_shared_rank(cr, t) + rank * 8;
-#pragma unroll
-      for (int i = 0; i < M; ++i) dst[i] = (double)v[i];
-    }
-    cl.sync();
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-      double a = 0.0;
-#pragma unroll
-      for (int r = 0; r < P; ++r) a += cr[r * 8 + i];
-      v[i] = (float)a;
-    }
+  __device__ static void csum(double (&v)[M], const Sm& s, cg::cluster_group&, int& slot, int rank, int t,
+                              uint32_t extra = 0) {
+    csum_t<M, double>(v, s, slot, rank, t, extra);
+  }
+  template <int M>
+  __device__ static void csumf(float (&v)[M], const Sm& s, cg::cluster_group&, int& slot, int rank, int t) {
+    csum_t<M, float>(v, s, slot, rank, t, 0);
   }
 
   // ---- bulk copy of Q contiguous complex values (L2 scratch) into the landing buffer; all threads wait
@@ -326,9 +333,9 @@ struct Clu {
       if (c == 0 && t == 0) mx = fmax(mx, (double)Xn.x * (double)Xn.x);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      double* red = s.red + slot * 4 * NW;
-      double* cr = s.cred + slot * P * 8;
-      slot ^= 1;
+      double* red = s.red + (slot & 1) * 4 * NW;
+      double* cr = s.cred + (slot & 1) * P * 8;
+      slot ^= 1;  // (a barrier-synchronised use: the slot's mbarrier phase is untouched)
       if ((t & 31) == 0) red[t >> 5] = mx;
       __syncthreads();
       mx = 0.0;
@@ -448,26 +455,28 @@ struct Clu {
       z |= cnts[ww] >> 30;
     }
     if (t == 0 || t == T - 1) {
-      // publish to every CTA: [src rank][p][first x, first S0 bit | last y, last S0 bit]
+      // publish to every CTA: [src rank][p][first x, first S0 bit | last y, last S0 bit], by st.async on the
+      // mbarrier of the reduction slot the partial counts use next (its byte count includes these)
+      const uint32_t cb = st::smem_u32(&s.cbar[slot & 1]);
 #pragma unroll
-      for (int pp = 0; pp < P; ++pp) {
-        const int q0 = pp, q1 = (U - 1) * P + pp;
+      for (int r = 0; r < P; ++r) {
+        const uint32_t ra = mapa(st::smem_u32(bmine), r), rb = mapa(cb, r);
 #pragma unroll
-        for (int r = 0; r < P; ++r) {
-          double* dst = cl.map_shared_rank(bmine, r) + pp * 4;
+        for (int pp = 0; pp < P; ++pp) {
+          const int q0 = pp, q1 = (U - 1) * P + pp;
           if (t == 0) {
-            dst[0] = (double)rt[q0].x;
-            dst[1] = (double)((S0 >> q0) & 1u);
+            st_async(ra + (pp * 4 + 0) * 8, (double)rt[q0].x, rb);
+            st_async(ra + (pp * 4 + 1) * 8, (double)((S0 >> q0) & 1u), rb);
           } else {
-            dst[2] = (double)rt[q1].y;
-            dst[3] = (double)((S0 >> q1) & 1u);
+            st_async(ra + (pp * 4 + 2) * 8, (double)rt[q1].y, rb);
+            st_async(ra + (pp * 4 + 3) * 8, (double)((S0 >> q1) & 1u), rb);
           }
         }
       }
     }
     // partial count and zero flag (rank order), then the chunk-end terms, evaluated by every CTA alike
     double pv[2] = {t == 0 ? (double)ctot : 0.0, t == 0 ? (double)z : 0.0};  // (one contribution per CTA)
-    csum<2>(pv, s, cl, slot, rank, t);  // (its cluster barrier also publishes the chunk ends)
+    csum<2>(pv, s, cl, slot, rank, t, (uint32_t)(P * P * 4 * 8));  // (its barrier also lands the chunk ends)
     // the P x P chunk-end terms, spread over the lanes of every warp (each warp gets the same total)
     int bt = 0;
     bool bz = false;
@@ -764,6 +773,8 @@ fif_cluster_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32_
   for (int i = t; i < K::NEL; i += K::T) s.El[i] = El[i];
   if (t == 0) {
     st::mbar_init(s.bar, 1);
+    st::mbar_init(&s.cbar[0], 1);
+    st::mbar_init(&s.cbar[1], 1);
     st::mbar_fence_init();
   }
   __syncthreads();
