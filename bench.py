@@ -399,7 +399,8 @@ def run_ours(args, world, rank, local):
         cnt = cnt[:1]  # one signal; the count is replicated on every (emulated) rank
     Mtot = int(np.clip(cnt, 0, None).sum())
     eb = 8 if dt == "f64" else 4
-    passes = 2 if cfgl["regime"] == "resident" else 4  # four-step: two read+write passes per transform
+    # on-chip regimes (resident, cluster): one read+write pass per transform; four-step (streamed, distributed): two
+    passes = 2 if cfgl["regime"] in ("resident", "cluster") else 4
     fft_bytes = passes * n * eb * (Mtot + B)      # passes*n*b per transform, (M+1) transforms per signal
     comp_bytes = n * eb * (Mtot + 2 * B)          # read s once + write M IMFs + trend
     written_bytes = n * eb * B * (plan.max_imfs + 1) + n * eb * B  # output slots + input
@@ -481,7 +482,8 @@ def run_ours(args, world, rank, local):
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "traffic": traffic, "peak_kind": peak_kind,
                          "model": f"FFT-pass bytes {passes}*n*{eb}*(M+1) per signal (SURVEY.md 8d)",
-                         "scope": "whole step" if cfgl["regime"] != "resident" else "the single resident kernel",
+                         "scope": "the single resident kernel" if cfgl["regime"] == "resident" else
+                                  ("the single cluster kernel" if cfgl["regime"] == "cluster" else "whole step"),
                          "compulsory_frac": comp_bytes / (ms * 1e-3) / 1e9 / peak,
                          "written_bytes_per_launch": written_bytes},
             "cpu_baseline": cpu,

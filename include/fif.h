@@ -65,8 +65,9 @@ typedef enum {
 
 /* Create a plan for `batch` independent signals of length n.
  *   n          : samples per signal, even.  Resident regime: powers of two 512 <= n <= 8192 (fp32: <= 16384).
+ *                Cluster regime (fp64): n = 16384, 32768, 65536 (one signal per cluster of 2, 4, 8 CTAs).
  *                Streamed regime: n/2 of the form 2^a 3^b 5^c, n <= 2^27 (a multi-level FFT of 2-4
- *                levels in HBM).  Other n -> FIF_ERR_UNSUPPORTED_N.
+ *                levels in HBM).  AUTO picks the first that applies.  Other n -> FIF_ERR_UNSUPPORTED_N.
  *   batch      : number of signals, >= 0 (0 is a valid no-op plan).
  *   dtype      : element type of signals and IMFs.  f32 computes the FFTs in fp32 and
  *                accumulates the stopping sums and takes the floor in fp64 (reading A14).
@@ -106,6 +107,8 @@ fif_status fif_plan_set_options(fif_plan_t plan, fif_stop_rule stop, double gamm
  *   |DFT(r)_f|^2 >= 1e-4 max (1% in magnitude), and L from the extrema rule at k = 2 f*
  *   (reading A20); no such bin ends the decomposition (the extrema guard k >= 2 still applies).
  * Batch plans only (FIF_ERR_UNSUPPORTED_N on a distributed plan: neighbouring bins live on other ranks).
+ * A cluster plan (FIF_REGIME_CLUSTER) switches to the streamed regime when the spectral rule is set (same
+ * decomposition; its bins' neighbours live in other CTAs of the cluster).
  * A streamed plan needs (n/2+1) doubles per signal more workspace under FIF_MASK_SPECTRAL: a plan-owned
  * workspace is re-allocated (FIF_ERR_OOM), a caller workspace must already be large enough
  * (FIF_ERR_INVALID_ARG otherwise, the rule unchanged).  No decompose on the plan may be pending. */

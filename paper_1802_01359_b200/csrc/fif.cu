@@ -178,7 +178,24 @@ fif_status fif_plan_set_options(fif_plan_t p, fif_stop_rule stop, double gamma) 
 
 fif_status fif_plan_set_mask_rule(fif_plan_t p, fif_mask_rule rule) {
   if (!p || (rule != FIF_MASK_EXTREMA && rule != FIF_MASK_SPECTRAL)) return FIF_ERR_INVALID_ARG;
-  if (rule == FIF_MASK_SPECTRAL && (p->regime == 2 || p->regime == 3 || p->regime == 4)) return FIF_ERR_UNSUPPORTED_N;
+  if (rule == FIF_MASK_SPECTRAL && (p->regime == 2 || p->regime == 3)) return FIF_ERR_UNSUPPORTED_N;
+  if (rule == FIF_MASK_SPECTRAL && p->regime == 4) {
+    // the cluster kernel has no spectral-peak search (its neighbouring bins live in other CTAs): the plan
+    // becomes a streamed one, which computes the same decomposition (tests/test_gpu_cluster.py)
+    if (cudaDeviceSynchronize() != cudaSuccess) return FIF_ERR_CUDA;
+    st::Geo g;
+    if (!st_geometry(p->n, p->dtype == FIF_F64, g)) return FIF_ERR_UNSUPPORTED_N;
+    cl_free(p);
+    p->d_cl_scr = nullptr;
+    p->cl_P = p->cl_clusters = 0;
+    cudaFree(p->d_Eh);
+    cudaFree(p->d_El);
+    cudaFree(p->d_tw);
+    p->d_Eh = p->d_El = p->d_tw = nullptr;
+    p->regime = 1;
+    fif_status st = st_setup(p);
+    if (st != FIF_OK) return st;
+  }
   const int32_t old = p->mask;
   p->mask = (int32_t)rule;
   if (p->regime == 1 && old != p->mask) {  // the power array lives in the workspace: re-carve it

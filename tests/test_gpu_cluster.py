@@ -81,3 +81,23 @@ def test_cluster_batch_beyond_grid_and_options():
     ref = df_batch(s[idx], delta=3e-3, max_inner=57, max_imfs=6)
     for i, b in enumerate(idx):
         assert_parity(s[b], gpu, ref, b, i)
+
+
+def test_cluster_plan_switches_to_streamed_for_the_spectral_rule():
+    """The spectral-peak rule (A20) on an AUTO plan of a cluster length: the plan becomes a streamed
+    one and decomposes as the oracle does."""
+    n, B = 16384, 3
+    s = np.stack([signals.tones_signal(n, 44, i) for i in range(B)])
+    plan = fif.Plan(n, B, "f64")
+    assert plan.launch_config()["regime"] == "cluster"
+    plan.set_mask_rule(fif.MASK_SPECTRAL)
+    assert plan.launch_config()["regime"] == "streamed"
+    x = torch.from_numpy(s).cuda()
+    out = plan.alloc_outputs()
+    plan.decompose(x, *out)
+    torch.cuda.synchronize()
+    gpu = [t.cpu().numpy() for t in out]
+    plan.close()
+    ref = df.decompose_batch(s, mask=df.MASK_SPECTRAL)
+    for b in range(B):
+        assert_parity(s[b], gpu, ref, b, b)
