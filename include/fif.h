@@ -117,10 +117,12 @@ fif_status fif_plan_set_mask_rule(fif_plan_t plan, fif_mask_rule rule);
 
 /* Per-L eigenvalue table (SURVEY.md §8f "next" 4; "computing in advance the eigenvalues
  * ... for every scaling reduces even further the computational time"): enable != 0 precomputes, on the
- * plan's device, w_hat_k (k = 0..n/2) for every filter half-length L = 2..floor((n-1)/4) the rule can
- * produce ((floor((n-1)/4) - 1) (n/2 + 1) elements of dtype: 16.8 MB at n = 4096 fp64), with the same
- * device code that otherwise evaluates the closed form per IMF, and the decomposition then reads the
- * row of its L instead -- bit-identical results.  enable = 0 frees it.  Resident regime only
+ * plan's device, for every filter half-length L = 2..floor((n-1)/4) the rule can produce and every bin
+ * k = 0..n/2, the window spectrum w = w_hat_k and the cap probe's power e = (1 - w)^(max_inner-1)
+ * (2 (floor((n-1)/4) - 1) (n/2 + 1) elements of dtype: 33.5 MB at n = 4096 fp64), with the same device
+ * code that otherwise evaluates the closed form per IMF, and the decomposition then reads the row of its
+ * L instead -- bit-identical results.
+ * enable = 0 frees it.  Resident regime only
  * (FIF_ERR_UNSUPPORTED_N otherwise; enable = 0 is always accepted).  Synchronises the device.
  * Errors: FIF_ERR_OOM, FIF_ERR_CUDA. */
 fif_status fif_plan_set_eigen_table(fif_plan_t plan, int32_t enable);

@@ -221,8 +221,8 @@ fif_status fif_plan_set_eigen_table(fif_plan_t p, int32_t enable) {
   }
   if (p->d_wtab) return FIF_OK;
   const int nL = (int)((p->n - 1) / 4) - 1;  // L = 2 .. floor((n-1)/4) (reading A3)
-  // fp64: {w_hat, a^(max_inner-1)} pairs; fp32: w_hat (fif_wtab_kernel)
-  const size_t es = p->dtype == FIF_F64 ? 2 * sizeof(double) : sizeof(float);
+  // per bin a Real pair {w_hat, a^(max_inner-1)} (fif_wtab_kernel)
+  const size_t es = 2 * (p->dtype == FIF_F64 ? sizeof(double) : sizeof(float));
   if (cudaMalloc(&p->d_wtab, (size_t)nL * (size_t)(p->NC + 1) * es) != cudaSuccess) {
     p->d_wtab = nullptr;
     return FIF_ERR_OOM;

@@ -55,7 +55,7 @@ struct fif_plan_s {
   void* d_sin = nullptr;   // Real[NC+1]  sin(pi j/n)
   void* d_isin = nullptr;  // Real[NC+1]  1/sin(pi j/n) (j >= 1)
   void* d_tw = nullptr;    // V[twtotal]  Stockham twiddles e^{-2 pi i k r/(NS RP)}
-  void* d_wtab = nullptr;  // Real[(n-1)/4 - 1][NC+1] per-L eigenvalue table (fif_plan_set_eigen_table)
+  void* d_wtab = nullptr;  // Real[(n-1)/4 - 1][NC+1][2] per-L eigenvalue table (fif_plan_set_eigen_table)
   int block = 0, occ = 0;
   int grid_cap = 0;        // > 0: persistent grids capped at this many CTAs (FIF_GRID_CAP at creation; tests)
   size_t smem = 0;

@@ -62,9 +62,9 @@ struct Params {
   double delta;     // delta (absolute, for stop = 1)
   double gamma;     // > 0: gamma-threshold variant (A19)
   int32_t mask;     // 0: extrema filter-length rule (A1-A3); 1: spectral-peak rule (A20)
-  // per-L eigenvalue table, row L - 2, bins 0..NC; nullptr: closed form per IMF.
-  // fp64 plans: double2 {w_hat_k, a_k^(max_inner-1)} (the cap probe's power chain precomputed by the
-  // kernel's own code, bit-identical); fp32 plans: Real w_hat_k.
+  // per-L eigenvalue table; nullptr: closed form per IMF.  Row L - 2, bins 0..NC: Real
+  // pairs {w_hat_k, a_k^(max_inner-1)} (the cap probe's power chain precomputed in fp64 by the kernel's own
+  // code and rounded to Real, so table and closed form give the same bits).
   const void* wtab = nullptr;
 };
 
@@ -383,8 +383,7 @@ struct Resident {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
     const void* wtab;  // per-L eigenvalue table (Params::wtab) or nullptr
   };
-  // fp64: the table rows hold {w_hat, a^(cap-1)} pairs (TabE); fp32: w_hat only
-  static constexpr bool kWE = sizeof(Real) == 8;
+  static constexpr bool kF64 = sizeof(Real) == 8;
 
   // group layout: bin index of spectrum register q for thread j
   __device__ static int g2_of(int j) { return j == 0 ? NC / 8 : G - j; }
@@ -683,17 +682,10 @@ struct Resident {
   // sin((q+1)B - A) (group 2, g2 = n/8 - j), so only (sA, cA) are per-thread table gathers.
   __device__ static void bin_w_all(const Smem& sm, int L, Real invL, int j, double (&w)[NB]) {
     if constexpr (TAB) {  // precomputed eigenvalues of this scaling, filled by fif_wtab_kernel
-      if constexpr (kWE) {
-        const double* row = reinterpret_cast<const double*>(wtab_row(sm, L));  // .x of the {w, e} pairs
+      const Real* row = reinterpret_cast<const Real*>(tab_row(sm, L));  // .x of the {w, e} pairs
 #pragma unroll
-        for (int q = 0; q < R; ++q) w[q] = __ldg(row + 2 * bin_of(j, q));
-        w[R] = __ldg(row + 2 * NC);
-      } else {
-        const Real* row = reinterpret_cast<const Real*>(sm.wtab) + (size_t)(L - 2) * (NC + 1);
-#pragma unroll
-        for (int q = 0; q < R; ++q) w[q] = (double)__ldg(row + bin_of(j, q));
-        w[R] = (double)__ldg(row + NC);
-      }
+      for (int q = 0; q < R; ++q) w[q] = (double)__ldg(row + 2 * bin_of(j, q));
+      w[R] = (double)__ldg(row + 2 * NC);
       return;
     } else {
       Real cq[5], sq[5];
@@ -725,8 +717,9 @@ struct Resident {
       w[R] = (double)what(sm, L, invL, NC);
     }
   }
-  __device__ static const double2* wtab_row(const Smem& sm, int L) {
-    return reinterpret_cast<const double2*>(sm.wtab) + (size_t)(L - 2) * (NC + 1);
+  // table row of scaling L: {w, a^(cap-1)} pairs (Params::wtab)
+  __device__ static const V* tab_row(const Smem& sm, int L) {
+    return reinterpret_cast<const V*>(sm.wtab) + (size_t)(L - 2) * (NC + 1);
   }
   // |X_k|^2 c_k / 2 (the factor 2 is applied to the thread's sums); explicit roundings so that every
   // code path (closed form, table, test hooks) accumulates bit-identical values
@@ -742,7 +735,13 @@ struct Resident {
     Q = __fma_rn(px, __dmul_rn(w, w), Q);
     d = __dmul_rn(e, __dsub_rn(1.0, w));
   }
-
+  // fp32 plans' cap-probe bin (reading A14: terms and the thread's partial sums in fp32)
+  __device__ static void accum_bin32(float p1, float w, float e, float& P, float& Q, double& d) {
+    const float px = __fmul_rn(p1, __fmul_rn(e, e));
+    P = __fadd_rn(P, px);
+    Q = __fmaf_rn(px, __fmul_rn(w, w), Q);
+    d = (double)__fmul_rn(e, __fsub_rn(1.0f, w));
+  }
   // One fp64 probe at N: (P, Q) block totals and d_k = a_k^N.  ECT >= 0: N - 1 == ECT at compile time.
   template <int ECT = -1>
   __device__ static void probe(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int N, double& P,
@@ -782,8 +781,8 @@ struct Resident {
   // the same accumulation as probe_part<cap-1>, so the result is bit-identical.
   __device__ static void probe_cap_tab(const V (&X)[R], const V& Xn, const Smem& sm, int L, double (&v)[2],
                                        double (&d)[NB], int j) {
-    const double2* row = wtab_row(sm, L);
-    double2 we[R];
+    const V* row = tab_row(sm, L);
+    V we[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) we[q] = __ldg(row + bin_of(j, q));
     v[0] = 0.0; v[1] = 0.0;
@@ -791,10 +790,61 @@ struct Resident {
     for (int q = 0; q < R; ++q) accum_bin(bin_p1(X, Xn, j, q), we[q].x, we[q].y, v[0], v[1], d[q]);
     d[R] = 0.0;
     if (j == 0) {
-      const double2 wn = __ldg(row + NC);
+      const V wn = __ldg(row + NC);
       accum_bin(bin_p1(X, Xn, 0, R), wn.x, wn.y, v[0], v[1], d[R]);
     }
     v[0] *= 2.0; v[1] *= 2.0;
+  }
+  // The cap probe (N = max_inner; 70-97% of IMFs stop there): per bin P += p e^2, Q += p e^2 w^2 and
+  // d = e a, e = a^(cap-1), with {w, e} from the per-L table or, without it, from the closed
+  // form and the fp64 power chain (rounded to Real: the table's values).  fp64 plans accumulate in fp64;
+  // fp32 plans form the terms and the thread's partial sums in fp32 (reading A14: the block sums and the
+  // decision are fp64).  v = the thread's (P, Q) shares, dd = a^cap.
+  __device__ static void probe_cap(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL, int cap,
+                                   double (&v)[2], double (&dd)[NB], int j) {
+    V we[NB];
+    if constexpr (TAB) {
+      const V* row = tab_row(sm, L);
+#pragma unroll
+      for (int q = 0; q < R; ++q) we[q] = __ldg(row + bin_of(j, q));
+      we[R] = __ldg(row + NC);
+    } else {
+      double wall[NB];
+      bin_w_all(sm, L, invL, j, wall);
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        constexpr int M = 4;
+        double a[M], e[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) a[i] = 1.0 - wall[4 * g + i];
+        if constexpr (CAP > 0) upow_ct<CAP - 1>(e, a); else upow<M>(e, a, cap - 1);
+#pragma unroll
+        for (int i = 0; i < M; ++i) we[4 * g + i] = V{(Real)wall[4 * g + i], (Real)e[i]};
+      }
+      if (j == 0) {
+        double a[1] = {1.0 - wall[R]}, e[1];
+        if constexpr (CAP > 0) upow_ct<CAP - 1>(e, a); else upow<1>(e, a, cap - 1);
+        we[R] = V{(Real)wall[R], (Real)e[0]};
+      }
+    }
+    dd[R] = 0.0;
+    if constexpr (kF64) {
+      v[0] = 0.0; v[1] = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) accum_bin(bin_p1(X, Xn, j, q), we[q].x, we[q].y, v[0], v[1], dd[q]);
+      if (j == 0) accum_bin(bin_p1(X, Xn, 0, R), we[R].x, we[R].y, v[0], v[1], dd[R]);
+      v[0] *= 2.0; v[1] *= 2.0;
+    } else {
+      float P = 0.f, Q = 0.f;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        float p1 = __fmaf_rn(X[q].x, X[q].x, __fmul_rn(X[q].y, X[q].y));
+        if (q == 0 && j == 0) p1 *= 0.5f;
+        accum_bin32(p1, we[q].x, we[q].y, P, Q, dd[q]);
+      }
+      if (j == 0) accum_bin32(0.5f * __fmul_rn(Xn.x, Xn.x), we[R].x, we[R].y, P, Q, dd[R]);
+      v[0] = 2.0 * (double)P; v[1] = 2.0 * (double)Q;
+    }
   }
 
   // fp32 hint for the minimal passing N in [1, hi] (pass(hi) known): a 4-ary search on fp32 sums, three
@@ -941,9 +991,14 @@ struct Resident {
       slot ^= 1;
       verify(X, Xn, sm, L, invL, N, p.delta2, lo, hi, dd, red2, j);
     } else {
-      if constexpr (kWE && TAB) {
+      if constexpr (kF64 && TAB) {  // (the fp64 table probe keeps its own code shape: register allocation)
         double v[2];
         probe_cap_tab(X, Xn, sm, L, v, dd, j);
+        block_sum<NW, 2>(v, red, j);
+        Pv = v[0]; Qv = v[1];
+      } else if constexpr (!kF64) {
+        double v[2];
+        probe_cap(X, Xn, sm, L, invL, cap, v, dd, j);
         block_sum<NW, 2>(v, red, j);
         Pv = v[0]; Qv = v[1];
       } else if constexpr (CAP > 0) {
@@ -1283,21 +1338,15 @@ __global__ void __launch_bounds__(NC / kR) fif_wtab_kernel(void* __restrict__ ta
   K::load_tables(sm, sintab, isintab, j);
   const int L = 2 + (int)blockIdx.x;
   const Real invL = (Real)1 / (Real)L;
-  double w[K::NB];
+  double w[K::NB], a[K::NB], e[K::NB];
   K::bin_w_all(sm, L, invL, j, w);
-  if constexpr (K::kWE) {
-    double a[K::NB], e[K::NB];
 #pragma unroll
-    for (int q = 0; q < K::NB; ++q) a[q] = 1.0 - w[q];
-    if constexpr (CAP > 0) upow_ct<CAP - 1>(e, a); else upow<K::NB>(e, a, cap - 1);
-    double2* row = reinterpret_cast<double2*>(tab) + (size_t)blockIdx.x * (NC + 1);
-    for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = double2{w[q], e[q]};
-    if (j == 0) row[NC] = double2{w[kR], e[kR]};
-  } else {
-    Real* row = reinterpret_cast<Real*>(tab) + (size_t)blockIdx.x * (NC + 1);
-    for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = (Real)w[q];
-    if (j == 0) row[NC] = (Real)w[kR];
-  }
+  for (int q = 0; q < K::NB; ++q) a[q] = 1.0 - w[q];
+  if constexpr (CAP > 0) upow_ct<CAP - 1>(e, a); else upow<K::NB>(e, a, cap - 1);
+  using V = typename Cx<Real>::V;
+  V* row = reinterpret_cast<V*>(tab) + (size_t)blockIdx.x * (NC + 1);
+  for (int q = 0; q < kR; ++q) row[K::bin_of(j, q)] = V{(Real)w[q], (Real)e[q]};
+  if (j == 0) row[NC] = V{(Real)w[kR], (Real)e[kR]};
 }
 
 template <typename Real, int NC, int CAP>

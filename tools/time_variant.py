@@ -4,14 +4,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1802_01359_b200 import fif, signals
 eig = "--eig" in sys.argv
-sys.argv = [a for a in sys.argv if a != "--eig"]
+f32 = "--f32" in sys.argv
+sys.argv = [a for a in sys.argv if a not in ("--eig", "--f32")]
 if len(sys.argv) > 1:
     fif.LIB_PATH = os.path.abspath(sys.argv[1])
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
-s = signals.make_batch("cfg1", batch=B, n=n)
-x = torch.from_numpy(s).cuda()
-plan = fif.Plan(n, B, "f64")
+s = signals.make_batch("cfg4", batch=min(B, 4096), n=n) if f32 else signals.make_batch("cfg1", batch=B, n=n)
+if B > s.shape[0]:
+    s = np.concatenate([s] * ((B + s.shape[0] - 1) // s.shape[0]))[:B]
+x = torch.from_numpy(np.ascontiguousarray(s)).cuda()
+plan = fif.Plan(n, B, "f32" if f32 else "f64")
 if eig:
     plan.set_eigen_table(True)
 out = plan.alloc_outputs()
