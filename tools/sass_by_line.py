@@ -40,11 +40,11 @@ for ln in lst:
         infunc = (".text." + kern) in st
     if not infunc:
         continue
-    m = re.search(r"line (\d+)", ln)
+    m = re.search(r'File "([^"]+)", line (\d+)', ln)
     if st.startswith("//##") and m:
         if not prevc:
             chain = []
-        chain.append((int(m.group(1)), srcf.split("/")[-1] in ln))
+        chain.append((int(m.group(2)), m.group(1).split("/")[-1] == srcf.split("/")[-1]))
         prevc = True
         continue
     if prevc:
