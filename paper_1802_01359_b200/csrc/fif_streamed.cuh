@@ -508,6 +508,29 @@ __device__ __forceinline__ double upow_rt(double a, int e) {
   return r;
 }
 
+// fp32 plans (reading A14): the damping powers and the probe terms in fp32.  a^m = 2^(m log2(1 - w)) through
+// the SFU; log2(1 - w) from the series -(w + w^2/2 + ... + w^7/7) log2(e) for w < 1/16 (relative error
+// ~1e-7 of w, truncation < w^7/8), lg2.approx(1 - w) above (absolute error ~2^-22: relative error of a^m
+// m 2^-22 ln 2, on values a^m <= (15/16)^m that are then tiny).  w >= 1 (rounding) gives log2 0 = -inf, a^m = 0.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float log2_1m(float w) {
+  float p = fmaf(w, 1.f / 7.f, 1.f / 6.f);
+  p = fmaf(w, p, 0.2f);
+  p = fmaf(w, p, 0.25f);
+  p = fmaf(w, p, 1.f / 3.f);
+  p = fmaf(w, p, 0.5f);
+  p = fmaf(w, p, 1.f);
+  const float ser = -1.44269504088896341f * w * p;
+  float lg;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(fmaxf(1.f - w, 0.f)));
+  return w < 0.0625f ? ser : lg;
+}
+__device__ __forceinline__ float pow_l2(float l2, int m) { return m > 0 ? ex2_approx((float)m * l2) : 1.f; }
+
 // row index (position / F_{L-1}) of the row whose bins are base + P t, and back
 __device__ __forceinline__ int64_t row_of_base(const Geo& g, int64_t base) {
   int64_t r = 0;
@@ -1223,6 +1246,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ROWS_MINB) k_rows_inv(
     V* A = St0 + cs * rowbuf;
     const int cb = two ? 1 : 0;
     double sP = 0.0, sQ = 0.0;
+    float sPf = 0.f, sQf = 0.f;  // fp32 plans: the thread's partial sums (reading A14)
     // e^{i pi k/n} and e^{i pi L k/n} advance geometrically over the thread's bins (a few complex products
     // instead of two scattered table gathers per bin pair): sin(pi k/n) = Im, sin(pi r_k/n) = |Im e^{i pi Lk/n}|
     // (the table reads are issued before the wait for the rows, so their latency overlaps the copy)
@@ -1260,6 +1284,36 @@ __global__ void __launch_bounds__(kThreads, FIF_ROWS_MINB) k_rows_inv(
         wk = sk * sk;
         wm = sm * sm;
       }
+      Real dkr, dmr;  // a^N of the pair, rounded to Real
+      V E2v;          // e^{2 pi i k/n}
+      const bool self = !two && i == tm && k != 0;  // a self-paired bin (k = NC - k) is counted once
+      if constexpr (sizeof(Real) == 4) {
+        const float wkf = (float)wk, wmf = (float)wm;
+        const float lk = log2_1m(wkf), lm = log2_1m(wmf);
+        float dkf, dmf;
+        if (SPEC) {
+          const int m1 = (CAP > 0 ? CAP : N) - 1;
+          const float ek = pow_l2(lk, m1), em = pow_l2(lm, m1);  // a^{cap-1}
+          const float ck = k == 0 ? 1.f : 2.f, cm = self ? 0.f : (k == 0 ? 1.f : 2.f);
+          const float pk = ck * fmaf(xk.x, xk.x, xk.y * xk.y) * (ek * ek);
+          const float pm = cm * fmaf(xm.x, xm.x, xm.y * xm.y) * (em * em);
+          sPf += pk + pm;
+          sQf += fmaf(pk, wkf * wkf, pm * (wmf * wmf));
+          dkf = ek * fmaxf(1.f - wkf, 0.f);
+          dmf = em * fmaxf(1.f - wmf, 0.f);
+        } else {
+          dkf = pow_l2(lk, N);
+          dmf = pow_l2(lm, N);
+        }
+        if (g.gamma > 0.0) {  // gamma-threshold (A19)
+          if (dkf >= (float)(1.0 - g.gamma)) dkf = 1.f;
+          if (dmf >= (float)(1.0 - g.gamma)) dmf = 1.f;
+        }
+        dkr = dkf;
+        dmr = dmf;
+        const V Ekf = V{(Real)Ek.x, (Real)Ek.y};
+        E2v = cmul(Ekf, Ekf);
+      } else {
       const double ak = 1.0 - wk, am = 1.0 - wm;
       double dk, dm;
       if (SPEC) {
@@ -1271,8 +1325,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ROWS_MINB) k_rows_inv(
           ek = upow_rt(ak, N - 1);
           em = upow_rt(am, N - 1);
         }
-        // Parseval weights c_k: 1 for k = 0 and the Nyquist bin, 2 otherwise; a self-paired bin once
-        const bool self = !two && i == tm && k != 0;
+        // Parseval weights c_k: 1 for k = 0 and the Nyquist bin, 2 otherwise
         const double ck = k == 0 ? 1.0 : 2.0, cm = self ? 0.0 : (k == 0 ? 1.0 : 2.0);
         const double pk = ck * ((double)xk.x * (double)xk.x + (double)xk.y * (double)xk.y) * (ek * ek);
         const double pm = cm * ((double)xm.x * (double)xm.x + (double)xm.y * (double)xm.y) * (em * em);
@@ -1291,21 +1344,29 @@ __global__ void __launch_bounds__(kThreads, FIF_ROWS_MINB) k_rows_inv(
         if (dk >= 1.0 - g.gamma) dk = 1.0;
         if (dm >= 1.0 - g.gamma) dm = 1.0;
       }
-      const V Av = cscale(xk, (Real)(dk * invn)), Bv = cscale(xm, (Real)(dm * invn));
+      dkr = (Real)dk;
+      dmr = (Real)dm;
+      const double2 E2k = cmul(Ek, Ek);  // e^{2 pi i k/n}
+      E2v = V{(Real)E2k.x, (Real)E2k.y};
+      }
+      const V Av = cscale(xk, dkr * (Real)invn), Bv = cscale(xm, dmr * (Real)invn);
       const V S = V{Av.x + Bv.x, Av.y - Bv.y};
       const V D = V{Av.x - Bv.x, Av.y + Bv.y};
-      const double2 E2k = cmul(Ek, Ek);  // e^{2 pi i k/n}
-      const V T = mul_i<1>(cmul(V{(Real)E2k.x, (Real)E2k.y}, D));
+      const V T = mul_i<1>(cmul(E2v, D));
       Bf[sidx<V>(0, i, lv.pitch, lv.swz)] = cadd(S, T);
-      Xo[ra * F + i] = cscale(xk, (Real)(1.0 - dk));
+      Xo[ra * F + i] = cscale(xk, (Real)1 - dkr);
       if (k == 0) {
-        Xnout[b] = cscale(xm, (Real)(1.0 - dm));
+        Xnout[b] = cscale(xm, (Real)1 - dmr);
       } else {
         Bf[sidx<V>(cb, tm, lv.pitch, lv.swz)] = cconj(csub(S, T));
-        Xo[(two ? rb : ra) * F + tm] = cscale(xm, (Real)(1.0 - dm));
+        Xo[(two ? rb : ra) * F + tm] = cscale(xm, (Real)1 - dmr);
       }
     }
     if (SPEC) {  // unit partial sums -> c.red, last CTA of the signal decides (fixed order)
+      if constexpr (sizeof(Real) == 4) {
+        sP = (double)sPf;
+        sQ = (double)sQf;
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         sP += __shfl_xor_sync(0xffffffffu, sP, o);
@@ -1421,8 +1482,11 @@ __global__ void __launch_bounds__(kThreads, MODE == 1 ? FIF_PROBE1_MINB : 3) k_p
       N0 = lo + step;
     }
     double acc[NV];
+    float accf[MODE == 1 && sizeof(Real) == 4 ? NV : 1];  // fp32 plans' K-ary partial sums
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(accf) / sizeof(float)); ++i) accf[i] = 0.f;
     int64_t ra, rb, bA;
     int two;
     pair_of<Real>(g, ch, ra, rb, bA, two);
@@ -1475,6 +1539,21 @@ __global__ void __launch_bounds__(kThreads, MODE == 1 ? FIF_PROBE1_MINB : 3) k_p
         em *= em;
         acc[0] += pk * ek + pm * em;
         acc[1] += pk * wk * wk * ek + pm * wm * wm * em;
+      } else if constexpr (sizeof(Real) == 4) {  // fp32 plans: terms and the thread's sums in fp32 (A14)
+        const float wkf = (float)wk, wmf = (float)wm;
+        const float lk = log2_1m(wkf), lm = log2_1m(wmf);
+        float yk = pow_l2(lk, 2 * (N0 - 1)), ym = pow_l2(lm, 2 * (N0 - 1));
+        const float zk = pow_l2(lk, 2 * step), zm = pow_l2(lm, 2 * step);
+        const float ck = k == 0 ? 1.f : 2.f, cm = self ? 0.f : (k == 0 ? 1.f : 2.f);
+        const float pkf = ck * fmaf(xk.x, xk.x, xk.y * xk.y), pmf = cm * fmaf(xm.x, xm.x, xm.y * xm.y);
+        const float qk = pkf * (wkf * wkf), qm = pmf * (wmf * wmf);
+#pragma unroll
+        for (int q = 0; q < kProbes; ++q) {
+          accf[2 * q] += fmaf(pkf, yk, pmf * ym);
+          accf[2 * q + 1] += fmaf(qk, yk, qm * ym);
+          yk *= zk;
+          ym *= zm;
+        }
       } else {
         const double a2k = ak * ak, a2m = am * am;
         double yk = upow_rt(a2k, N0 - 1), ym = upow_rt(a2m, N0 - 1);
@@ -1488,6 +1567,10 @@ __global__ void __launch_bounds__(kThreads, MODE == 1 ? FIF_PROBE1_MINB : 3) k_p
           ym *= zm;
         }
       }
+    }
+    if constexpr (MODE == 1 && sizeof(Real) == 4) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[i] = (double)accf[i];
     }
     constexpr int nv = NV;
     const bool useMax = MODE == 0 && g.stop == 1;
