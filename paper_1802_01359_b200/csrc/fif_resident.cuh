@@ -377,7 +377,9 @@ struct Resident {
   static constexpr size_t off_nbr = off_red + sizeof(double) * 8 * NW;         // NW*R V
   static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // 2 NW + 8 ints
   static constexpr size_t off_isin = (off_int + sizeof(int) * (4 * NW + 8) + 15) & ~(size_t)15;  // last: absent if TAB
-  static constexpr size_t smem_bytes = TAB ? off_isin : off_isin + sizeof(Real) * ((NC + 2) & ~1);
+  static constexpr size_t off_red2 = ((TAB ? off_isin : off_isin + sizeof(Real) * ((NC + 2) & ~1)) + 15) & ~(size_t)15;
+  // fp32 plans: two slots of 8 NW doubles for the fp32 search's fp64 block sums (search_below_cap32)
+  static constexpr size_t smem_bytes = off_red2 + (sizeof(Real) == 8 ? 0 : sizeof(double) * 16 * NW);
 
   struct Smem {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
@@ -961,6 +963,76 @@ struct Resident {
     return hi;
   }
 
+  // fp32 plans (reading A14): the search below the cap on fp32 terms -- a^(2(m-1)) = 2^(2(m-1) log2(1 - w))
+  // through the SFU (log2(1 - w) by the series for small w, streamed regime's log2_1m) and per-thread fp32
+  // partial sums -- with every decision on fp64 block sums, so the 4-ary search is itself the decision (no
+  // fp64 verification); d = a^N the same way.  pass(cap) is known.
+  __device__ static float log2_1m(float w) {
+    float q = __fmaf_rn(w, 1.f / 7.f, 1.f / 6.f);
+    q = __fmaf_rn(w, q, 0.2f);
+    q = __fmaf_rn(w, q, 0.25f);
+    q = __fmaf_rn(w, q, 1.f / 3.f);
+    q = __fmaf_rn(w, q, 0.5f);
+    q = __fmaf_rn(w, q, 1.f);
+    const float ser = -1.44269504088896341f * w * q;
+    return w < 0.0625f ? ser : lg2f(fmaxf(1.f - w, 0.f));  // (lg2 0 = -inf: a^m = 0)
+  }
+  __device__ static float pow2m(float l2, int m) { return m > 0 ? ex2f((float)m * l2) : 1.f; }
+  __device__ static int search_below_cap32(const V (&X)[R], const V& Xn, const Smem& sm, int L, Real invL,
+                                           const Params& p, double (&dd)[NB], int j) {
+    float l2[NB], pk[NB], pw[NB];
+    {
+      double wall[NB];
+      bin_w_all(sm, L, invL, j, wall);
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const float w = (float)wall[q];
+        float p1;
+        if (q == R) p1 = j == 0 ? 0.5f * __fmul_rn((float)Xn.x, (float)Xn.x) : 0.f;
+        else {
+          p1 = __fmaf_rn((float)X[q].x, (float)X[q].x, __fmul_rn((float)X[q].y, (float)X[q].y));
+          if (q == 0 && j == 0) p1 *= 0.5f;
+        }
+        l2[q] = log2_1m(w);
+        pk[q] = p1;
+        pw[q] = p1 * (w * w);
+      }
+    }
+    double* red2 = reinterpret_cast<double*>(reinterpret_cast<char*>(sm.bufA) + off_red2);
+    int s2 = 0;
+    int lo = 0, hi = p.max_inner;
+    while (hi - lo > 1) {
+      const int D = (hi - lo + 3) >> 2;
+      float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const float x1 = pow2m(l2[i], 2 * (lo + D - 1)), st = pow2m(l2[i], 2 * D);
+        const float x2 = x1 * st, x3 = x2 * st;
+        v[0] = __fmaf_rn(pk[i], x1, v[0]); v[1] = __fmaf_rn(pw[i], x1, v[1]);
+        v[2] = __fmaf_rn(pk[i], x2, v[2]); v[3] = __fmaf_rn(pw[i], x2, v[3]);
+        v[4] = __fmaf_rn(pk[i], x3, v[4]); v[5] = __fmaf_rn(pw[i], x3, v[5]);
+      }
+      double vd[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) vd[i] = 2.0 * (double)v[i];
+      block_sum<NW, 6>(vd, red2 + s2 * 8 * NW, j);
+      s2 ^= 1;
+      int nlo = lo, nhi = hi;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int m = lo + (i + 1) * D;
+        if (m >= hi) break;
+        if (vd[2 * i + 1] <= p.delta2 * vd[2 * i]) { nhi = m; break; }
+        nlo = m;
+      }
+      lo = nlo; hi = nhi;
+    }
+#pragma unroll
+    for (int q = 0; q < NB; ++q) dd[q] = (double)pow2m(l2[q], hi);
+    if (j != 0) dd[R] = 0.0;
+    return hi;
+  }
+
   // Full search (cap probe first); used by the test hook.  The decomposition loop inlines the cap
   // probe speculatively (decompose_one).
   __device__ static int search(const V (&X)[R], const V& Xn, const Smem& sm, int L, const Params& p, Real (&d)[R],
@@ -1006,7 +1078,10 @@ struct Resident {
       } else {
         probe(X, Xn, sm, L, invL, cap, Pv, Qv, dd, red, j);
       }
-      if (Qv <= p.delta2 * Pv) N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
+      if (Qv <= p.delta2 * Pv) {
+        if constexpr (kF64) N = search_below_cap(X, Xn, sm, L, invL, p, dd, slot, j);
+        else N = search_below_cap32(X, Xn, sm, L, invL, p, dd, j);
+      }
     }
     if (p.gamma > 0.0) {  // gamma-threshold: (1 - w)^N >= 1 - gamma -> factor 1 (A19)
 #pragma unroll
