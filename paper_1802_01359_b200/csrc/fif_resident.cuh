@@ -378,8 +378,11 @@ struct Resident {
   static constexpr size_t off_int = off_nbr + sizeof(V) * NW * R;              // 2 NW + 8 ints
   static constexpr size_t off_isin = (off_int + sizeof(int) * (4 * NW + 8) + 15) & ~(size_t)15;  // last: absent if TAB
   static constexpr size_t off_red2 = ((TAB ? off_isin : off_isin + sizeof(Real) * ((NC + 2) & ~1)) + 15) & ~(size_t)15;
-  // fp32 plans: two slots of 8 NW doubles for the fp32 search's fp64 block sums (search_below_cap32)
-  static constexpr size_t smem_bytes = off_red2 + (sizeof(Real) == 8 ? 0 : sizeof(double) * 16 * NW);
+  // fp32 plans: two slots of 8 NW doubles for the fp32 search's fp64 block sums (search_below_cap32), and
+  // for n <= 4096 the a3 rule L(k), k = 0..n, tabulated per CTA (filter_half_length itself, at kernel start)
+  static constexpr bool kLtab = sizeof(Real) == 4 && n <= 4096;
+  static constexpr size_t off_ltab = off_red2 + (sizeof(Real) == 8 ? 0 : sizeof(double) * 16 * NW);
+  static constexpr size_t smem_bytes = off_ltab + (kLtab ? ((sizeof(int16_t) * (n + 1) + 15) & ~(size_t)15) : 0);
 
   struct Smem {
     V* bufA; V* bufB; Real* sint; Real* isin; double* red; V* nbr; int* ired;
@@ -631,6 +634,17 @@ struct Resident {
     return (int)B;
   }
 
+  __device__ static int16_t* ltab(const Smem& sm) {
+    return reinterpret_cast<int16_t*>(reinterpret_cast<char*>(sm.bufA) + off_ltab);
+  }
+  __device__ static void fill_ltab(const Params& p, const Smem& sm, int j) {
+    if constexpr (kLtab)
+      for (int k = 2 + j; k <= n; k += T) ltab(sm)[k] = (int16_t)filter_half_length(p, k);
+  }
+  __device__ static int half_length(const Params& p, const Smem& sm, int k) {
+    if constexpr (kLtab) return ltab(sm)[k];
+    else return filter_half_length(p, k);
+  }
   __device__ static int filter_half_length(const Params& p, int k) {
     const double t = __dmul_rn(p.xi, (double)n);   // fl(xi * n), never contracted (A8)
     const double u = __ddiv_rn(t, (double)k);      // fl(fl(xi n)/k)
@@ -1226,9 +1240,9 @@ struct Resident {
       if (p.mask == 1) {  // spectral-peak rule: L from k = 2 f* (A20)
         const int fs = spectral_peak(X, Xn, sm, last, slot, j);
         if (fs == 0) break;
-        L = filter_half_length(p, 2 * fs);
+        L = half_length(p, sm, 2 * fs);
       } else {
-        L = filter_half_length(p, k);
+        L = half_length(p, sm, k);
       }
       const Real invL = (Real)1 / (Real)L;
       V v[R], Dn{0, 0};
@@ -1307,6 +1321,7 @@ fif_resident_kernel(const Real* __restrict__ sig, Real* __restrict__ imfs, int32
   typename K::Smem sm = K::carve(smem_raw);
   sm.wtab = TAB ? p.wtab : nullptr;
   const int j = threadIdx.x;
+  K::fill_ltab(p, sm, j);
   K::load_tables(sm, sintab, isintab, j);
   int slot = 0;
   typename Cx<Real>::V* last = sm.bufA;
