@@ -438,6 +438,12 @@ __device__ __forceinline__ typename Cx<Real>::V Er(const Tabs<Real>& tb, int eb,
   return cmul(__ldg(tb.Th + (j >> eb)), __ldg(tb.Tl + (j & ((1LL << eb) - 1))));
 }
 
+// (E2 x) mod 2n for an inter-level twiddle index: E2 (x mod F S) = (E2 x) mod 2n since E2 F S = 2n, and E(j)
+// has period 2n -- a mask for power-of-two n instead of a 64-bit division per tile or element
+__device__ __forceinline__ int64_t mod2n(const Geo& g, int64_t x) {
+  const int64_t m = 2 * g.n;
+  return (g.n & (g.n - 1)) == 0 ? (x & (m - 1)) : x % m;
+}
 // a4: w_hat_k for 0 <= k <= n/2: r = min(L k mod n, n - L k mod n)
 template <typename Real>
 __device__ __forceinline__ double what_tab(const Geo& g, const Tabs<Real>& tb, int L, int64_t k) {
@@ -892,7 +898,22 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
     r.src = KIND == PASS_FWD_FIRST ? reinterpret_cast<const V*>(sig + r.b * g.n) : r.buf;
     return r;
   };
+  // (C a power of two dividing the block: a thread's column is fixed and its digit advances by a constant,
+  // so the source address advances by a constant too -- one 64-bit add per element)
+  const bool fixc = lv.cs >= 0 && lv.C <= kColThreads;
   auto issue = [&](const TG& q, V* dst) {
+    if (fixc) {
+      const int cc = threadIdx.x & (lv.C - 1), f0 = threadIdx.x >> lv.cs, df = kColThreads >> lv.cs;
+      const V* src = q.src + q.base + (int64_t)f0 * lv.S + cc;
+      const int64_t step = (int64_t)df * lv.S;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int f = f0 + j * df;
+        if (f < lv.F) cp_async<(int)sizeof(V)>(dst + sidx<V>(cc, f, lv.pitch, lv.swz), src);
+        src += step;
+      }
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int i = threadIdx.x + j * kColThreads;
@@ -984,12 +1005,27 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         const int64_t df = kColThreads >> lv.cs;
         if (DIR < 0) {
           w = cconj(Er(tb, g.eb, lv.E2 * (cur.s0 + c0) * f0));
-          ws = cconj(Er(tb, g.eb, lv.E2 * ((cur.s0 + c0) * df % ((int64_t)lv.F * lv.S))));
+          ws = cconj(Er(tb, g.eb, mod2n(g, lv.E2 * ((cur.s0 + c0) * df))));
         } else {
-          w = Er(tb, g.eb, lvn.E2 * (((int64_t)f0 * lv.S + cur.s0 + c0) * kn % ((int64_t)lvn.F * lvn.S)));
-          ws = Er(tb, g.eb, lvn.E2 * ((df * lv.S * kn) % ((int64_t)lvn.F * lvn.S)));
+          w = Er(tb, g.eb, mod2n(g, lvn.E2 * (((int64_t)f0 * lv.S + cur.s0 + c0) * kn)));
+          ws = Er(tb, g.eb, mod2n(g, lvn.E2 * (df * lv.S * kn)));
         }
       }
+      if (geom) {  // (fixc: the thread's column is fixed, its digit and address advance by constants)
+        const int cc = threadIdx.x & (lv.C - 1), f0 = threadIdx.x >> lv.cs, df = kColThreads >> lv.cs;
+        V* dstp = cur.buf + cur.base + (int64_t)f0 * lv.S + cc;
+        const int64_t step = (int64_t)df * lv.S;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int f = f0 + j * df;
+          if (f < lv.F) {
+            const V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
+            *dstp = cmul(x, w);
+            w = cmul(w, ws);
+          }
+          dstp += step;
+        }
+      } else
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int i = threadIdx.x + j * kColThreads;
@@ -1003,7 +1039,7 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
           } else if (DIR < 0) {
             x = cmul(x, cconj(Er(tb, g.eb, lv.E2 * (cur.s0 + cc) * f)));
           } else {
-            x = cmul(x, Er(tb, g.eb, lvn.E2 * (((int64_t)f * lv.S + cur.s0 + cc) * kn % ((int64_t)lvn.F * lvn.S))));
+            x = cmul(x, Er(tb, g.eb, mod2n(g, lvn.E2 * (((int64_t)f * lv.S + cur.s0 + cc) * kn))));
           }
           cur.buf[cur.base + (int64_t)f * lv.S + cc] = x;
         }
@@ -1383,10 +1419,9 @@ __global__ void __launch_bounds__(kThreads, FIF_ROWS_MINB) k_rows_inv(
     // the next (coarser) level's conjugate twiddle e^{+2 pi i s k'/(F' S')}: s = element, k' = row mod F'
     // (geometric in i: two table products per row and thread, one multiply per element)
     const int64_t ka = ra % lvn.F, kb = rb % lvn.F;
-    const int64_t FSn = (int64_t)lvn.F * lvn.S;
-    V wa = Er(tb, g.eb, lvn.E2 * ((int64_t)threadIdx.x * ka % FSn)), wb = Er(tb, g.eb, lvn.E2 * ((int64_t)threadIdx.x * kb % FSn));
-    const V sa = Er(tb, g.eb, lvn.E2 * ((int64_t)blockDim.x * ka % FSn));
-    const V sb = Er(tb, g.eb, lvn.E2 * ((int64_t)blockDim.x * kb % FSn));
+    V wa = Er(tb, g.eb, mod2n(g, lvn.E2 * ((int64_t)threadIdx.x * ka))), wb = Er(tb, g.eb, mod2n(g, lvn.E2 * ((int64_t)threadIdx.x * kb)));
+    const V sa = Er(tb, g.eb, mod2n(g, lvn.E2 * ((int64_t)blockDim.x * ka)));
+    const V sb = Er(tb, g.eb, mod2n(g, lvn.E2 * ((int64_t)blockDim.x * kb)));
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
       W[ra * F + i] = cmul(out[sidx<V>(0, i, lv.pitch, lv.swz)], wa);
       wa = cmul(wa, sa);
