@@ -255,11 +255,21 @@ static void for_col_instances(F&& f) {
     f(st::k_col<Real, DIR, KIND, 4>);
     f(st::k_col<Real, DIR, KIND, 9>);
     f(st::k_col<Real, DIR, KIND, 10>);
+    f(st::k_col<Real, DIR, KIND, 21>);
+    f(st::k_col<Real, DIR, KIND, 22>);
+    f(st::k_col<Real, DIR, KIND, 23>);
+    f(st::k_col<Real, DIR, KIND, 24>);
+    f(st::k_col<Real, DIR, KIND, 29>);
+    f(st::k_col<Real, DIR, KIND, 30>);
   } else {
     f(st::k_col<Real, DIR, KIND, 5>);
     f(st::k_col<Real, DIR, KIND, 6>);
     f(st::k_col<Real, DIR, KIND, 7>);
     f(st::k_col<Real, DIR, KIND, 8>);
+    f(st::k_col<Real, DIR, KIND, 25>);
+    f(st::k_col<Real, DIR, KIND, 26>);
+    f(st::k_col<Real, DIR, KIND, 27>);
+    f(st::k_col<Real, DIR, KIND, 28>);
   }
 }
 template <typename Real, int DIR, int KIND, typename... A>
@@ -275,6 +285,16 @@ static void launch_col(int cs, int grid, size_t smem, cudaStream_t s, A... a) {
     case 6: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 6><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 7: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 7><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     case 8: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 8><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 21: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 21><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 22: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 22><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 23: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 23><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 24: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 24><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 29: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 29><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 30: if constexpr (sizeof(Real) == 4) { st::k_col<Real, DIR, KIND, 30><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 25: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 25><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 26: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 26><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 27: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 27><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
+    case 28: if constexpr (sizeof(Real) == 8) { st::k_col<Real, DIR, KIND, 28><<<grid, st::kColThreads, smem, s>>>(a...); return; } break;
     default: break;
   }
   st::k_col<Real, DIR, KIND, 0><<<grid, st::kColThreads, smem, s>>>(a...);
@@ -336,6 +356,19 @@ fif_status st_setup_t(fif_plan_s* p) {
   for_col_instances<Real, 1, st::PASS_MID>(attr);
   for_col_instances<Real, 1, st::PASS_INV_LAST>(attr);
   for (int i = 0; i < g.L - 1; ++i) p->st_col_cs[i] = col_schedule(g.lv[i], sizeof(Real) == 8);
+  // opt-in (FIF_ST_RM=1 at plan creation): row-major column tiles staged by cp.async.bulk (the TMA engine, one
+  // copy per tile row), for a compile-time schedule and 16-byte aligned rows (row length, digit stride and
+  // signal length multiples of 16 bytes).  Same arithmetic in the same order as the default cp.async tiles
+  // (bit-identical decompositions, tests/test_gpu_streamed.py) but measured slower on B200 (config 3 +1.3%,
+  // config 4 2^17 +1.3%, 3 2^14 +4%, 2^20 +27%: many short row copies per tile), so not the default.
+  const char* rmenv = getenv("FIF_ST_RM");
+  const bool rm_on = rmenv && rmenv[0] == '1';
+  for (int i = 0; i < g.L - 1; ++i) {
+    const st::Level& lv = g.lv[i];
+    const bool ok = p->st_col_cs[i] >= 1 && p->st_col_cs[i] <= 10 && (lv.C * sizeof(V)) % 16 == 0 &&
+                    (lv.S * sizeof(V)) % 16 == 0 && (g.n * sizeof(Real)) % 16 == 0;
+    p->st_col_rm[i] = rm_on && ok ? p->st_col_cs[i] + 20 : 0;
+  }
   attr(st::k_rows_fwd<Real, 0>);
   attr(st::k_rows_fwd<Real, 1>);
   attr(st::k_rows_inv<Real, 0, 0, 0>);
@@ -429,12 +462,15 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     const int gfold = grid_for(g.batch * g.ngrp, capped(p, p->num_sms * 4));
     const int gsig = (int)((g.batch + TB - 1) / TB);
     auto col = [&](int i) { return grid_for(g.batch * g.lv[i].tiles, gcol); };
+    // the column passes' instance: row-major bulk-copy tiles when the level and this call's buffers allow
+    const bool aligned16 = ((uintptr_t)sg % 16) == 0 && ((uintptr_t)out % 16) == 0;
+    auto ccs = [&](int i) { return aligned16 && p->st_col_rm[i] ? p->st_col_rm[i] : p->st_col_cs[i]; };
     Nvtx wave("streamed/wave");
     st::k_init<<<gsig, TB, 0, s>>>(g, c);
-    launch_col<Real, -1, st::PASS_FWD_FIRST>(p->st_col_cs[0], col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+    launch_col<Real, -1, st::PASS_FWD_FIRST>(ccs(0), col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
     st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
     for (int i = 1; i < Lv - 1; ++i)
-      launch_col<Real, -1, st::PASS_MID>(p->st_col_cs[i], col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i], sg, out, X, tb, c);
+      launch_col<Real, -1, st::PASS_MID>(ccs(i), col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i], sg, out, X, tb, c);
     if (p->st_row_rs) st::k_rows_fwd<Real, 1><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     else st::k_rows_fwd<Real, 0><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     auto peaks = [&](const V* Xs, const V* Xns) {  // spectral-peak rule: L for the next IMF
@@ -478,8 +514,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
         if (fast) rows(F0{}, FC{}, 0); else rows(F0{}, F0{}, 0);
       }
       for (int i = Lv - 2; i >= 1; --i)
-        launch_col<Real, 1, st::PASS_MID>(p->st_col_cs[i], col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
-      launch_col<Real, 1, st::PASS_INV_LAST>(p->st_col_cs[0], col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+        launch_col<Real, 1, st::PASS_MID>(ccs(i), col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
+      launch_col<Real, 1, st::PASS_INV_LAST>(ccs(0), col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
       st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 1, ln, it);
       peaks(Xo, Xno);
     }

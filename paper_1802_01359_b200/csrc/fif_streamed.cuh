@@ -378,6 +378,43 @@ __device__ __forceinline__ V* cta_fft_c_odd(V* a, V* b, int cols, const V* __res
     return cta_fft_c_odd<DIR, V, F, NS * P, Rest...>(b, a, cols, tw);
   }
 }
+// Row-major tiles (the column passes whose tiles are staged by cp.async.bulk, one copy per tile row): element
+// (column c, digit i) at i * cols + c.  Column fastest over the threads, so the lanes of a warp read and write
+// contiguous row segments (conflict-free without a swizzle) and share their twiddle.
+template <int P, int DIR, typename V, int F, int NS>
+__device__ __forceinline__ void cta_pass_rm(const V* src, V* dst, int cols, const V* __restrict__ tw) {
+  constexpr int per = F / P, tstride = F / (NS * P);
+  for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
+    const int vt = idx / cols, c = idx - vt * cols, k = vt % NS;
+    V x[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) x[r] = src[(vt + r * per) * cols + c];
+    if constexpr (NS > 1) {
+      const int kt = k * tstride;
+#pragma unroll
+      for (int r = 1; r < P; ++r) {
+        V t = tw[r * kt];
+        if (DIR > 0) t.y = -t.y;
+        x[r] = cmul(x[r], t);
+      }
+    }
+    dft_small<P, DIR>(x);
+    const int j0 = (vt - k) * P + k;
+#pragma unroll
+    for (int r = 0; r < P; ++r) dst[(j0 + r * NS) * cols + c] = x[r];
+  }
+}
+template <int DIR, typename V, int F, int NS, int P, int... Rest>
+__device__ __forceinline__ V* cta_fft_rm(V* a, V* b, int cols, const V* __restrict__ tw) {
+  __syncthreads();
+  cta_pass_rm<P, DIR, V, F, NS>(a, b, cols, tw);
+  if constexpr (sizeof...(Rest) == 0) {
+    __syncthreads();
+    return b;
+  } else {
+    return cta_fft_rm<DIR, V, F, NS * P, Rest...>(b, a, cols, tw);
+  }
+}
 template <int F, int... R>
 __device__ __forceinline__ bool sched_is(const Level& lv) {
   constexpr int r[] = {R...};
@@ -417,6 +454,17 @@ __device__ __forceinline__ V* col_fft(V* a, V* b, const Level& lv, int cols, con
   else if constexpr (CS == 10) return cta_fft_c_odd<DIR, V, 20, 1, 4, 5>(a, b, cols, tw);
   else if constexpr (CS == 11) return cta_fft_c<DIR, V, 1024, 1, 2, 8, 8, 8>(a, b, cols, tw);
   else if constexpr (CS == 12) return cta_fft_c<DIR, V, 2048, 1, 8, 16, 16>(a, b, cols, tw);
+  // 21-30: CS - 20 on row-major tiles (k_col with bulk-copy staging)
+  else if constexpr (CS == 21) return cta_fft_rm<DIR, V, 32, 1, 8, 4>(a, b, cols, tw);
+  else if constexpr (CS == 22) return cta_fft_rm<DIR, V, 64, 1, 4, 16>(a, b, cols, tw);
+  else if constexpr (CS == 23) return cta_fft_rm<DIR, V, 128, 1, 8, 16>(a, b, cols, tw);
+  else if constexpr (CS == 24) return cta_fft_rm<DIR, V, 256, 1, 16, 16>(a, b, cols, tw);
+  else if constexpr (CS == 25) return cta_fft_rm<DIR, V, 128, 1, 2, 8, 8>(a, b, cols, tw);
+  else if constexpr (CS == 26) return cta_fft_rm<DIR, V, 256, 1, 4, 8, 8>(a, b, cols, tw);
+  else if constexpr (CS == 27) return cta_fft_rm<DIR, V, 32, 1, 4, 8>(a, b, cols, tw);
+  else if constexpr (CS == 28) return cta_fft_rm<DIR, V, 64, 1, 8, 8>(a, b, cols, tw);
+  else if constexpr (CS == 29) return cta_fft_rm<DIR, V, 12, 1, 4, 3>(a, b, cols, tw);
+  else if constexpr (CS == 30) return cta_fft_rm<DIR, V, 20, 1, 4, 5>(a, b, cols, tw);
   else return cta_fft<DIR, V, sizeof(V) == 16 ? 8 : 16>(a, b, lv, cols, tw);
 }
 
@@ -607,7 +655,7 @@ __device__ __forceinline__ Mono block_mono(Mono m, Mono* sm) {
 // inside a lane + the lane-boundary transitions, summed with a warp reduction.  A zero difference
 // anywhere in the segment (plateau collapse, reading A4) switches the warp to the exact ordered
 // monoid fold.
-template <typename Real>
+template <typename Real, bool RM = false>
 __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, int64_t seg0, int64_t segstep,
                               uint32_t* __restrict__ segi, Real* __restrict__ segv) {
   using V = typename Cx<Real>::V;
@@ -617,7 +665,7 @@ __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, 
   const int j0 = lane * per, j1 = min(j0 + per, nr);
   for (int f = warp; f < lv.F; f += nw) {
     auto x_at = [&](int j) -> Real {
-      const V v = buf[sidx<V>(j >> 1, f, lv.pitch, lv.swz)];
+      const V v = RM ? buf[f * lv.C + (j >> 1)] : buf[sidx<V>(j >> 1, f, lv.pitch, lv.swz)];
       return (j & 1) ? v.y : v.x;
     };
     // this lane's reals and the first real of the next lane
@@ -673,8 +721,8 @@ __device__ void tile_segments(const typename Cx<Real>::V* buf, const Level& lv, 
     if (lane == 0) {
       const int64_t sg = seg0 + (int64_t)f * segstep;
       segi[sg] = mpack(m);
-      segv[2 * sg] = buf[sidx<V>(0, f, lv.pitch, lv.swz)].x;
-      segv[2 * sg + 1] = buf[sidx<V>(lv.C - 1, f, lv.pitch, lv.swz)].y;
+      segv[2 * sg] = x_at(0);
+      segv[2 * sg + 1] = x_at(nr - 1);
     }
   }
 }
@@ -860,8 +908,14 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
                                                      const __grid_constant__ Tabs<Real> tb,
                                                      const __grid_constant__ Ctl c) {
   using V = typename Cx<Real>::V;
+  // CS >= 21: row-major tiles staged by the bulk-copy engine (one cp.async.bulk per tile row, completion
+  // counted in bytes on the buffer's mbarrier); else column-major XOR-swizzled tiles loaded by cp.async
+  constexpr bool RMk = CS >= 21;
   extern __shared__ __align__(16) char smem_raw[];
+  __shared__ __align__(8) uint64_t cmb[3];
   const size_t bufsz = (size_t)lv.C * lv.pitch;
+  // tile slot of element (column cc, digit f)
+  auto TI = [&](int cc, int f) { return RMk ? f * lv.C + cc : sidx<V>(cc, f, lv.pitch, lv.swz); };
   V* S[3] = {reinterpret_cast<V*>(smem_raw), reinterpret_cast<V*>(smem_raw) + bufsz,
              reinterpret_cast<V*>(smem_raw) + 2 * bufsz};
   // the level's Stockham twiddles e^{-2 pi i j/F} in shared memory (the FFT passes read 1 per point)
@@ -902,6 +956,16 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
   // so the source address advances by a constant too -- one 64-bit add per element)
   const bool fixc = lv.cs >= 0 && lv.C <= kColThreads;
   auto issue = [&](const TG& q, V* dst) {
+    if constexpr (RMk) {  // F rows of C contiguous values: one bulk copy each, by the first F threads
+      const int bi = (int)((dst - S[0]) / bufsz);
+      const uint32_t rowb = (uint32_t)(lv.C * sizeof(V));
+      if (threadIdx.x == 0) mbar_expect_tx(&cmb[bi], rowb * (uint32_t)lv.F);
+      for (int f = threadIdx.x; f < lv.F; f += blockDim.x) {
+        fence_proxy_async();  // this buffer's generic-proxy reads (ordered by the last barrier) precede the copy
+        bulk_g2s(dst + f * lv.C, q.src + q.base + (int64_t)f * lv.S, rowb, &cmb[bi]);
+      }
+      return;
+    }
     if (fixc) {
       const int cc = threadIdx.x & (lv.C - 1), f0 = threadIdx.x >> lv.cs, df = kColThreads >> lv.cs;
       const V* src = q.src + q.base + (int64_t)f0 * lv.S + cc;
@@ -924,13 +988,23 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
       }
     }
   };
+  if constexpr (RMk) {
+    if (threadIdx.x == 0) {
+      mbar_init(&cmb[0], 1);
+      mbar_init(&cmb[1], 1);
+      mbar_init(&cmb[2], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
+  uint32_t mph = 0;  // RMk: bit i = parity of the next wait on cmb[i]
   uint32_t t = next_tile(blockIdx.x);
   TG cur{};
   if (t < total) {
     cur = geo(t);
     issue(cur, S[0]);
   }
-  cp_async_commit();
+  if constexpr (!RMk) cp_async_commit();
   for (int it = 0; t < total; ++it) {
     const uint32_t tn = next_tile(t + gridDim.x);
     TG nxt{};
@@ -938,8 +1012,14 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
       nxt = geo(tn);
       issue(nxt, S[(it + 1) % 3]);
     }
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (RMk) {
+      const int bi = it % 3;
+      mbar_wait(&cmb[bi], (mph >> bi) & 1u);
+      mph ^= 1u << bi;
+    } else {
+      cp_async_commit();
+      cp_async_wait<1>();
+    }
     __syncthreads();
     V* In = S[it % 3];
     V* Sc = S[(it + 2) % 3];
@@ -952,13 +1032,14 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
-          const V x = In[sidx<V>(cc, f, lv.pitch, lv.swz)];
+          const V x = In[TI(cc, f)];
           finite &= isfinite(x.x) && isfinite(x.y);
           reinterpret_cast<V*>(Rb)[cur.base + (int64_t)f * lv.S + cc] = x;
         }
       }
       if (!finite) atomicOr(c.bad + cur.b, 1);
-      if (!tile_segments_thr<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
+      if (RMk) tile_segments<Real, true>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+      else if (!tile_segments_thr<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
         tile_segments<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     }
     V r[KIND == PASS_INV_LAST ? U : 1];
@@ -981,15 +1062,16 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
           int f, cc;
           tile_fc(lv, i, f, cc);
           const int64_t gi = cur.base + (int64_t)f * lv.S + cc;
-          const V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
+          const V x = out[TI(cc, f)];
           __stcs(cur.buf + gi, x);
           const V rn = csub(r[j], x);
           reinterpret_cast<V*>(Rb)[gi] = rn;
-          stage[sidx<V>(cc, f, lv.pitch, lv.swz)] = rn;
+          stage[TI(cc, f)] = rn;
         }
       }
       __syncthreads();
-      if (!tile_segments_thr<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
+      if (RMk) tile_segments<Real, true>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+      else if (!tile_segments_thr<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
         tile_segments<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     } else {
       // forward: this level's twiddle e^{-2 pi i s k/(F S)}; inverse: the next coarser level's
@@ -1019,7 +1101,7 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         for (int j = 0; j < U; ++j) {
           const int f = f0 + j * df;
           if (f < lv.F) {
-            const V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
+            const V x = out[TI(cc, f)];
             *dstp = cmul(x, w);
             w = cmul(w, ws);
           }
@@ -1032,7 +1114,7 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         if (i < FC) {
           int f, cc;
           tile_fc(lv, i, f, cc);
-          V x = out[sidx<V>(cc, f, lv.pitch, lv.swz)];
+          V x = out[TI(cc, f)];
           if (geom) {
             x = cmul(x, w);
             w = cmul(w, ws);
