@@ -93,6 +93,7 @@ struct fif_plan_s {
   size_t st_smem_col[fifgpu::st::kMaxLev] = {}, st_smem_rows = 0, st_smem_rows_inv = 0;
   int st_col_cs[fifgpu::st::kMaxLev] = {};  // column transform path per level (st::col_fft CS)
   int st_col_rm[fifgpu::st::kMaxLev] = {};  // the same with row-major bulk-copy-staged tiles (CS + 20), 0: unavailable
+  int st_col_tm[fifgpu::st::kMaxLev] = {};  // 1: the row-major tile is one cp.async.bulk.tensor box (tensor map per call)
   int st_row_rs = 0;                         // row transform path (st::row_fft RS)
   // host (e2e) path staging
   int64_t chunk = 0;

@@ -204,6 +204,41 @@ int occ_grid(const fif_plan_s* p, K kern, size_t smem) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, st::kThreads, smem);
   return p->num_sms * (occ > 0 ? occ : 1);
 }
+// Tensor maps for the row-major column tiles (cp.async.bulk.tensor): cuTensorMapEncodeTiled through the
+// runtime's driver entry point (no link against libcuda).  The pass's source as a 3-D tensor of 8-byte
+// elements {lower index s (S values), digit row a F + f (NC / S rows), slot}: a tile is the box {C, F, 1}.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return (EncodeTiledFn)f;
+  }();
+  return fn;
+}
+// box limits of the tensor-map tile of a level (each box side <= 256 elements)
+static bool tile_box_ok(const st::Level& lv, size_t vbytes) {
+  return lv.C * (vbytes / 8) <= 256 && lv.F <= 256 && (lv.C * vbytes) % 16 == 0;
+}
+static bool tile_map(CUtensorMap* tm, const void* base, const st::Level& lv, size_t vbytes, int64_t NC, int64_t slots,
+                     int64_t slot_bytes) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || !tile_box_ok(lv, vbytes) || ((uintptr_t)base % 16) != 0) return false;
+  const cuuint64_t epv = vbytes / 8;
+  const cuuint64_t dims[3] = {(cuuint64_t)lv.S * epv, (cuuint64_t)(NC / lv.S), (cuuint64_t)slots};
+  const cuuint64_t strides[2] = {(cuuint64_t)lv.S * vbytes, (cuuint64_t)slot_bytes};
+  const cuuint32_t box[3] = {(cuuint32_t)(lv.C * epv), (cuuint32_t)lv.F, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 // the k_col instance for a column level: its compile-time transform path (st::col_fft CS), 0 = generic
 static int col_schedule(const st::Level& lv, bool f64) {
   auto is = [&](int F, std::initializer_list<int> r) {
@@ -361,13 +396,17 @@ fif_status st_setup_t(fif_plan_s* p) {
   // signal length multiples of 16 bytes).  Same arithmetic in the same order as the default cp.async tiles
   // (bit-identical decompositions, tests/test_gpu_streamed.py) but measured slower on B200 (config 3 +1.3%,
   // config 4 2^17 +1.3%, 3 2^14 +4%, 2^20 +27%: many short row copies per tile), so not the default.
+  // FIF_ST_RM=2: the same tiles landed by ONE cp.async.bulk.tensor each (a 3-D box of a tensor map encoded per
+  // call over the pass's source), when the level's box fits the tensor-map limits.
   const char* rmenv = getenv("FIF_ST_RM");
-  const bool rm_on = rmenv && rmenv[0] == '1';
+  const bool rm_on = rmenv && (rmenv[0] == '1' || rmenv[0] == '2');
+  const bool tm_on = rmenv && rmenv[0] == '2' && encode_tiled() != nullptr;
   for (int i = 0; i < g.L - 1; ++i) {
     const st::Level& lv = g.lv[i];
     const bool ok = p->st_col_cs[i] >= 1 && p->st_col_cs[i] <= 10 && (lv.C * sizeof(V)) % 16 == 0 &&
                     (lv.S * sizeof(V)) % 16 == 0 && (g.n * sizeof(Real)) % 16 == 0;
     p->st_col_rm[i] = rm_on && ok ? p->st_col_cs[i] + 20 : 0;
+    p->st_col_tm[i] = p->st_col_rm[i] && tm_on && tile_box_ok(lv, sizeof(V)) ? 1 : 0;
   }
   attr(st::k_rows_fwd<Real, 0>);
   attr(st::k_rows_fwd<Real, 1>);
@@ -465,12 +504,23 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
     // the column passes' instance: row-major bulk-copy tiles when the level and this call's buffers allow
     const bool aligned16 = ((uintptr_t)sg % 16) == 0 && ((uintptr_t)out % 16) == 0;
     auto ccs = [&](int i) { return aligned16 && p->st_col_rm[i] ? p->st_col_rm[i] : p->st_col_cs[i]; };
+    // tensor maps of this wave's sources (tile = one box): the signals (level 0 forward), X (the other forward
+    // levels), the IMF slots of d_imfs (inverse levels); a level whose map cannot be encoded copies row by row
+    CUtensorMap tmf[st::kMaxLev] = {}, tmi[st::kMaxLev] = {};
+    int tmf_on[st::kMaxLev] = {}, tmi_on[st::kMaxLev] = {};
+    for (int i = 0; i < Lv - 1; ++i) {
+      if (!(aligned16 && p->st_col_rm[i] && p->st_col_tm[i])) continue;
+      tmf_on[i] = i == 0 ? tile_map(&tmf[i], sg, g.lv[i], sizeof(V), g.NC, g.batch, g.n * (int64_t)sizeof(Real))
+                         : tile_map(&tmf[i], X, g.lv[i], sizeof(V), g.NC, g.batch, g.NC * (int64_t)sizeof(V));
+      tmi_on[i] = tile_map(&tmi[i], out, g.lv[i], sizeof(V), g.NC, g.batch * (g.max_imfs + 1),
+                           g.n * (int64_t)sizeof(Real));
+    }
     Nvtx wave("streamed/wave");
     st::k_init<<<gsig, TB, 0, s>>>(g, c);
-    launch_col<Real, -1, st::PASS_FWD_FIRST>(ccs(0), col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+    launch_col<Real, -1, st::PASS_FWD_FIRST>(ccs(0), col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c, tmf[0], tmf_on[0]);
     st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 0, ln, it);
     for (int i = 1; i < Lv - 1; ++i)
-      launch_col<Real, -1, st::PASS_MID>(ccs(i), col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i], sg, out, X, tb, c);
+      launch_col<Real, -1, st::PASS_MID>(ccs(i), col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i], sg, out, X, tb, c, tmf[i], tmf_on[i]);
     if (p->st_row_rs) st::k_rows_fwd<Real, 1><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     else st::k_rows_fwd<Real, 0><<<grow, TB, p->st_smem_rows, s>>>(g, top, X, Xn, tb, c);
     auto peaks = [&](const V* Xs, const V* Xns) {  // spectral-peak rule: L for the next IMF
@@ -514,8 +564,8 @@ void st_decompose_t(fif_plan_s* p, const void* sig, void* imfs, int32_t* cnt, in
         if (fast) rows(F0{}, FC{}, 0); else rows(F0{}, F0{}, 0);
       }
       for (int i = Lv - 2; i >= 1; --i)
-        launch_col<Real, 1, st::PASS_MID>(ccs(i), col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c);
-      launch_col<Real, 1, st::PASS_INV_LAST>(ccs(0), col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c);
+        launch_col<Real, 1, st::PASS_MID>(ccs(i), col(i), p->st_smem_col[i], s, g, g.lv[i], g.lv[i - 1], sg, out, X, tb, c, tmi[i], tmi_on[i]);
+      launch_col<Real, 1, st::PASS_INV_LAST>(ccs(0), col(0), p->st_smem_col[0], s, g, g.lv[0], g.lv[0], sg, out, X, tb, c, tmi[0], tmi_on[0]);
       st::k_fold<Real><<<gfold, TB, 0, s>>>(g, c, 1, ln, it);
       peaks(Xo, Xno);
     }

@@ -29,6 +29,7 @@
 //       passes; k_col<INV_LAST>: level-0 IDFT, IMF store, R -= IMF, extrema partials
 //   a7  k_fold bookkeeping (l_m, N_m, M), k_final: trend in slot M, zero fill
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -865,6 +866,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// cp.async.bulk.tensor: one instruction lands a whole F x C tile (a 3-D box {C, F, 1} of the tensor map
+// {lower index s, digit row a F + f, signal / IMF slot}) in row-major order, completion on the mbarrier
+__device__ __forceinline__ void tensor_g2s(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(smem_u32(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -906,12 +914,15 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
                                                      const __grid_constant__ Level lvn, const Real* __restrict__ sig,
                                                      Real* __restrict__ imfs, typename Cx<Real>::V* __restrict__ X,
                                                      const __grid_constant__ Tabs<Real> tb,
-                                                     const __grid_constant__ Ctl c) {
+                                                     const __grid_constant__ Ctl c,
+                                                     const __grid_constant__ CUtensorMap tm, const int tmode) {
   using V = typename Cx<Real>::V;
+  // tmode (row-major instances only): the tile is one cp.async.bulk.tensor box of the map tm (built per call by
+  // the host over the source of this pass: the signals, X, or the IMF slots of d_imfs)
   // CS >= 21: row-major tiles staged by the bulk-copy engine (one cp.async.bulk per tile row, completion
   // counted in bytes on the buffer's mbarrier); else column-major XOR-swizzled tiles loaded by cp.async
   constexpr bool RMk = CS >= 21;
-  extern __shared__ __align__(16) char smem_raw[];
+  extern __shared__ __align__(128) char smem_raw[];
   __shared__ __align__(8) uint64_t cmb[3];
   const size_t bufsz = (size_t)lv.C * lv.pitch;
   // tile slot of element (column cc, digit f)
@@ -959,6 +970,14 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
     if constexpr (RMk) {  // F rows of C contiguous values: one bulk copy each, by the first F threads
       const int bi = (int)((dst - S[0]) / bufsz);
       const uint32_t rowb = (uint32_t)(lv.C * sizeof(V));
+      if (tmode) {  // (the buffer's generic-proxy accesses were fenced by every thread before the last barrier)
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(&cmb[bi], rowb * (uint32_t)lv.F);
+          const int slot = (DIR < 0) ? (int)q.b : (int)q.b * (g.max_imfs + 1) + c.M[q.b];
+          tensor_g2s(dst, &tm, (int)(q.s0 * (int64_t)(sizeof(V) / 8)), (int)(q.a * (uint32_t)lv.F), slot, &cmb[bi]);
+        }
+        return;
+      }
       if (threadIdx.x == 0) mbar_expect_tx(&cmb[bi], rowb * (uint32_t)lv.F);
       for (int f = threadIdx.x; f < lv.F; f += blockDim.x) {
         fence_proxy_async();  // this buffer's generic-proxy reads (ordered by the last barrier) precede the copy
@@ -1127,6 +1146,9 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
         }
       }
     }
+    if constexpr (RMk) {
+      if (tmode) fence_proxy_async();  // this thread's shared-memory accesses precede the tensor copies that refill
+    }
     __syncthreads();
     t = tn;
     cur = nxt;
@@ -1216,7 +1238,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ST_MINB) k_rows_fwd(const __grid
                                                        const __grid_constant__ Tabs<Real> tb,
                                                        const __grid_constant__ Ctl c) {
   using V = typename Cx<Real>::V;
-  extern __shared__ __align__(16) char smem_raw[];
+  extern __shared__ __align__(128) char smem_raw[];
   V* A = reinterpret_cast<V*>(smem_raw);
   V* Bf = A + 2 * lv.pitch;
   const int F = lv.F;
@@ -1297,7 +1319,7 @@ __global__ void __launch_bounds__(kThreads, FIF_ROWS_MINB) k_rows_inv(
     const typename Cx<Real>::V* __restrict__ Xnin, typename Cx<Real>::V* __restrict__ Xnout,
     const __grid_constant__ Tabs<Real> tb, const __grid_constant__ Ctl c, int redo_only) {
   using V = typename Cx<Real>::V;
-  extern __shared__ __align__(16) char smem_raw[];
+  extern __shared__ __align__(128) char smem_raw[];
   __shared__ double sred[kNW][2];
   __shared__ int last;
   __shared__ __align__(8) uint64_t mbar[2];

@@ -196,10 +196,12 @@ def test_streamed_empty_batch():
 @pytest.mark.parametrize("n,dtype,rowmax,colmax", [(1 << 17, "f64", None, None), (1 << 14, "f64", 64, 64),
                                                    (1 << 17, "f32", None, None), (3 << 14, "f32", None, None),
                                                    (5 << 14, "f32", None, None), (1 << 20, "f32", None, None)])
-def test_streamed_bulk_copy_tiles_bit_identical(n, dtype, rowmax, colmax, monkeypatch):
-    """The opt-in column tiles staged by cp.async.bulk (row-major, FIF_ST_RM=1 at plan creation) run the same
-    butterflies in the same order as the default cp.async tiles: identical decompositions, bit for bit
-    (2-, 3-level, mixed-radix geometries; both dtypes)."""
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_streamed_bulk_copy_tiles_bit_identical(n, dtype, rowmax, colmax, mode, monkeypatch):
+    """The opt-in column tiles staged by the TMA engine (row-major; FIF_ST_RM=1: one cp.async.bulk per tile row,
+    FIF_ST_RM=2: one cp.async.bulk.tensor box per tile from a per-call tensor map) run the same butterflies in the
+    same order as the default cp.async tiles: identical decompositions, bit for bit (2-, 3-level, mixed-radix
+    geometries; both dtypes)."""
     if rowmax:
         monkeypatch.setenv("FIF_ST_ROWMAX", str(rowmax))
         monkeypatch.setenv("FIF_ST_COLMAX", str(colmax))
@@ -208,7 +210,7 @@ def test_streamed_bulk_copy_tiles_bit_identical(n, dtype, rowmax, colmax, monkey
          else np.stack([signals.tones_signal(n, 27, i) for i in range(B)]))
     monkeypatch.delenv("FIF_ST_RM", raising=False)
     a = run_gpu(s, dtype, regime=ST)
-    monkeypatch.setenv("FIF_ST_RM", "1")
+    monkeypatch.setenv("FIF_ST_RM", mode)
     b = run_gpu(s, dtype, regime=ST)
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
