@@ -391,16 +391,18 @@ fif_status st_setup_t(fif_plan_s* p) {
   for_col_instances<Real, 1, st::PASS_MID>(attr);
   for_col_instances<Real, 1, st::PASS_INV_LAST>(attr);
   for (int i = 0; i < g.L - 1; ++i) p->st_col_cs[i] = col_schedule(g.lv[i], sizeof(Real) == 8);
-  // opt-in (FIF_ST_RM=1 at plan creation): row-major column tiles staged by cp.async.bulk (the TMA engine, one
-  // copy per tile row), for a compile-time schedule and 16-byte aligned rows (row length, digit stride and
-  // signal length multiples of 16 bytes).  Same arithmetic in the same order as the default cp.async tiles
-  // (bit-identical decompositions, tests/test_gpu_streamed.py) but measured slower on B200 (config 3 +1.3%,
-  // config 4 2^17 +1.3%, 3 2^14 +4%, 2^20 +27%: many short row copies per tile), so not the default.
+  // Row-major column tiles staged by the TMA engine, for a compile-time schedule and 16-byte aligned rows (row
+  // length, digit stride and signal length multiples of 16 bytes).  Same arithmetic in the same order as the
+  // cp.async tiles (bit-identical decompositions, tests/test_gpu_streamed.py).  FIF_ST_RM=1: one cp.async.bulk per
+  // tile row (measured slower than cp.async: many short row copies per tile).
   // FIF_ST_RM=2: the same tiles landed by ONE cp.async.bulk.tensor each (a 3-D box of a tensor map encoded per
   // call over the pass's source), when the level's box fits the tensor-map limits.
+  // Default (FIF_ST_RM unset): the tensor-map tiles (measured faster on every geometry of configs 2-4, DESIGN.md
+  // §8); FIF_ST_RM=0 forces the cp.async tiles, 1 the row-by-row bulk copies.
   const char* rmenv = getenv("FIF_ST_RM");
-  const bool rm_on = rmenv && (rmenv[0] == '1' || rmenv[0] == '2');
-  const bool tm_on = rmenv && rmenv[0] == '2' && encode_tiled() != nullptr;
+  const int rm_mode = rmenv ? atoi(rmenv) : 2;
+  const bool rm_on = rm_mode == 1 || rm_mode == 2;
+  const bool tm_on = rm_mode == 2 && encode_tiled() != nullptr;
   for (int i = 0; i < g.L - 1; ++i) {
     const st::Level& lv = g.lv[i];
     const bool ok = p->st_col_cs[i] >= 1 && p->st_col_cs[i] <= 10 && (lv.C * sizeof(V)) % 16 == 0 &&

@@ -1085,12 +1085,13 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
           __stcs(cur.buf + gi, x);
           const V rn = csub(r[j], x);
           reinterpret_cast<V*>(Rb)[gi] = rn;
-          stage[TI(cc, f)] = rn;
+          // (the new remainder is staged column-major swizzled in every mode: the layout is this kernel's
+          // choice here, and the thread-chunk segment reduction reads it conflict-free)
+          stage[sidx<V>(cc, f, lv.pitch, lv.swz)] = rn;
         }
       }
       __syncthreads();
-      if (RMk) tile_segments<Real, true>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
-      else if (!tile_segments_thr<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
+      if (!tile_segments_thr<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
         tile_segments<Real>(stage, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     } else {
       // forward: this level's twiddle e^{-2 pi i s k/(F S)}; inverse: the next coarser level's

@@ -198,7 +198,7 @@ def test_streamed_empty_batch():
                                                    (5 << 14, "f32", None, None), (1 << 20, "f32", None, None)])
 @pytest.mark.parametrize("mode", ["1", "2"])
 def test_streamed_bulk_copy_tiles_bit_identical(n, dtype, rowmax, colmax, mode, monkeypatch):
-    """The opt-in column tiles staged by the TMA engine (row-major; FIF_ST_RM=1: one cp.async.bulk per tile row,
+    """The column tiles staged by the TMA engine (row-major; FIF_ST_RM=1: one cp.async.bulk per tile row,
     FIF_ST_RM=2: one cp.async.bulk.tensor box per tile from a per-call tensor map) run the same butterflies in the
     same order as the default cp.async tiles: identical decompositions, bit for bit (2-, 3-level, mixed-radix
     geometries; both dtypes)."""
@@ -208,7 +208,7 @@ def test_streamed_bulk_copy_tiles_bit_identical(n, dtype, rowmax, colmax, mode, 
     B = 3
     s = (np.stack([signals.cfg4_signal(n, i) for i in range(B)]) if dtype == "f32"
          else np.stack([signals.tones_signal(n, 27, i) for i in range(B)]))
-    monkeypatch.delenv("FIF_ST_RM", raising=False)
+    monkeypatch.setenv("FIF_ST_RM", "0")  # the cp.async tiles (the default is the tensor-map tiles, mode 2)
     a = run_gpu(s, dtype, regime=ST)
     monkeypatch.setenv("FIF_ST_RM", mode)
     b = run_gpu(s, dtype, regime=ST)
