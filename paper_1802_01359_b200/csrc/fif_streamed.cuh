@@ -1054,12 +1054,15 @@ __global__ void __launch_bounds__(kColThreads, 2) k_col(const __grid_constant__ 
           const V x = In[TI(cc, f)];
           finite &= isfinite(x.x) && isfinite(x.y);
           reinterpret_cast<V*>(Rb)[cur.base + (int64_t)f * lv.S + cc] = x;
+          // (row-major tiles: a column-major swizzled copy in the scratch buffer for the segment reduction)
+          if (RMk) Sc[sidx<V>(cc, f, lv.pitch, lv.swz)] = x;
         }
       }
       if (!finite) atomicOr(c.bad + cur.b, 1);
-      if (RMk) tile_segments<Real, true>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
-      else if (!tile_segments_thr<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
-        tile_segments<Real>(In, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
+      if (RMk) __syncthreads();
+      const V* Sg = RMk ? Sc : In;
+      if (!tile_segments_thr<Real>(Sg, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv)))
+        tile_segments<Real>(Sg, lv, cur.b * g.nseg + cur.s0 / lv.C, spt, c.segi, reinterpret_cast<Real*>(c.segv));
     }
     V r[KIND == PASS_INV_LAST ? U : 1];
     if (KIND == PASS_INV_LAST) {  // remainder loads in flight during the transform (clamped: no local array)
