@@ -222,9 +222,11 @@ static EncodeTiledFn encode_tiled() {
   }();
   return fn;
 }
-// box limits of the tensor-map tile of a level (each box side <= 256 elements)
+// box limits of the tensor-map tile of a level (each box side <= 256 elements) and the 128-byte alignment of
+// every ring buffer (the shared-memory destination of a tensor copy)
 static bool tile_box_ok(const st::Level& lv, size_t vbytes) {
-  return lv.C * (vbytes / 8) <= 256 && lv.F <= 256 && (lv.C * vbytes) % 16 == 0;
+  return lv.C * (vbytes / 8) <= 256 && lv.F <= 256 && (lv.C * vbytes) % 16 == 0 &&
+         ((size_t)lv.C * lv.pitch * vbytes) % 128 == 0;
 }
 static bool tile_map(CUtensorMap* tm, const void* base, const st::Level& lv, size_t vbytes, int64_t NC, int64_t slots,
                      int64_t slot_bytes) {
