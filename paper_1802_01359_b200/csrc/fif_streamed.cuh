@@ -385,8 +385,10 @@ __device__ __forceinline__ V* cta_fft_c_odd(V* a, V* b, int cols, const V* __res
 template <int P, int DIR, typename V, int F, int NS>
 __device__ __forceinline__ void cta_pass_rm(const V* src, V* dst, int cols, const V* __restrict__ tw) {
   constexpr int per = F / P, tstride = F / (NS * P);
+  // (power-of-two tile widths -- every benchmark geometry -- split the index by a shift, not a division)
+  const int csh = (cols & (cols - 1)) == 0 ? 31 - __clz(cols) : -1;
   for (int idx = threadIdx.x; idx < cols * per; idx += blockDim.x) {
-    const int vt = idx / cols, c = idx - vt * cols, k = vt % NS;
+    const int vt = csh >= 0 ? idx >> csh : idx / cols, c = idx - vt * cols, k = vt % NS;
     V x[P];
 #pragma unroll
     for (int r = 0; r < P; ++r) x[r] = src[(vt + r * per) * cols + c];
